@@ -1,0 +1,578 @@
+// TEST INFRASTRUCTURE ONLY — never linked into the product.
+//
+// C ABI over the unmodified reference solver (/root/reference/proj, namespace
+// dg2d) so the parity tests and the benchmark's CPU arm can drive the real
+// reference from Python.  Built by oracle/Makefile straight from the
+// reference's own source files into oracle/_ref/libdg2dref.so.
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <random>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#include "dg2d/problems.hpp"
+#include "dg2d/reference.hpp"
+#include "dg2d/solver.hpp"
+
+using namespace dg2d;
+
+namespace {
+
+std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const SolverAbort& e) {
+    g_err = e.what();
+    return 1;
+  } catch (const MeshError& e) {
+    g_err = e.what();
+    return 5;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return 3;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 9;
+  }
+}
+
+struct RefCtx {
+  const Mesh* mesh;
+  const BasisTables* tables;
+  const BoundaryConditions* bc;
+  SolverContext ctx;
+  RhsBuffers bufs;
+};
+
+CoefficientArray make_coeffs(const RefCtx* r, const double* c) {
+  CoefficientArray a(kEq, r->tables->n_p, r->mesh->n_elements());
+  std::memcpy(a.data.data(), c, a.data.size() * sizeof(double));
+  return a;
+}
+
+std::string text_for(int kind, int nx, int ny, const double* p, int n) {
+  auto prm = [&](int i, double d) { return i < n ? p[i] : d; };
+  switch (kind) {
+    case 0: return gen_box_msh(nx, ny, prm(0, 1.0), prm(1, 1.0), static_cast<int>(prm(2, 1.0)));
+    case 1: return gen_sheared_box_msh(nx, ny, prm(0, 1.0), prm(1, 1.0), prm(2, 0.0), static_cast<int>(prm(3, 1.0)));
+    case 2: return gen_double_mach_msh(nx, ny, prm(0, 1.0 / 6.0));
+    case 3: {
+      VortexGeometry g;
+      g.r_inner = prm(0, 1.0);
+      g.r_outer = prm(1, 1.384);
+      return gen_vortex_msh(nx, g);
+    }
+    default: throw std::invalid_argument("kind not available in the reference");
+  }
+}
+
+// acceptance.cpp:37-49 smooth_field(seed)
+EulerState acceptance_state(double rho, double u, double v, double p) {
+  return {rho, rho * u, rho * v, p / 0.4 + 0.5 * rho * (u * u + v * v)};
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+int ref_num_threads() {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
+
+void* ref_mesh_from_msh(const char* text) {
+  Mesh* m = nullptr;
+  if (guard([&] { m = new Mesh(build_connectivity(parse_msh(text))); })) return nullptr;
+  return m;
+}
+
+void* ref_mesh_generate(int kind, int nx, int ny, const double* p, int n) {
+  Mesh* m = nullptr;
+  if (guard([&] { m = new Mesh(build_connectivity(parse_msh(text_for(kind, nx, ny, p, n)))); })) return nullptr;
+  return m;
+}
+
+int ref_mesh_text(int kind, int nx, int ny, const double* p, int n, char* buf, size_t cap, size_t* needed) {
+  return guard([&] {
+    std::string s = text_for(kind, nx, ny, p, n);
+    *needed = s.size() + 1;
+    if (buf && cap >= s.size() + 1) std::memcpy(buf, s.c_str(), s.size() + 1);
+  });
+}
+
+// Reference Mesh from raw arrays (same content as build_connectivity output);
+// lets the CPU arm run on meshes too large for the GMSH text round trip.
+void* ref_mesh_from_arrays(int nv, const double* vx, const double* vy, int ne, const int* ev, const int* eedge,
+                           const double* det, const double* tau, const double* inr, int ned, int nbnd, const int* v0,
+                           const int* v1, const int* l, const int* r, const int* sl, const int* sr, const double* nx,
+                           const double* ny, const double* h) {
+  Mesh* m = new Mesh;
+  m->vertices.resize(nv);
+  for (int i = 0; i < nv; ++i) m->vertices[i] = {vx[i], vy[i]};
+  m->elements.resize(ne);
+  for (int i = 0; i < ne; ++i) {
+    Element& e = m->elements[i];
+    for (int k = 0; k < 3; ++k) {
+      e.v[k] = ev[3 * i + k];
+      e.edge[k] = eedge[3 * i + k];
+    }
+    e.det_jac = det[i];
+    for (int k = 0; k < 4; ++k) e.tau[k] = tau[4 * i + k];
+    e.inradius = inr[i];
+  }
+  m->edges.resize(ned);
+  for (int k = 0; k < ned; ++k) {
+    Edge& e = m->edges[k];
+    e.v0 = v0[k];
+    e.v1 = v1[k];
+    e.left = l[k];
+    e.right = r[k];
+    e.side_left = sl[k];
+    e.side_right = sr[k];
+    e.nx = nx[k];
+    e.ny = ny[k];
+    e.half_length = h[k];
+  }
+  m->n_boundary_edges = nbnd;
+  return m;
+}
+
+void ref_mesh_free(void* m) { delete static_cast<Mesh*>(m); }
+
+void ref_mesh_sizes(void* mp, int* nv, int* ne, int* ned, int* nbnd) {
+  const Mesh& m = *static_cast<Mesh*>(mp);
+  *nv = static_cast<int>(m.vertices.size());
+  *ne = m.n_elements();
+  *ned = m.n_edges();
+  *nbnd = m.n_boundary_edges;
+}
+
+void ref_mesh_export(void* mp, double* vx, double* vy, int* ev, int* eedge, double* det, double* tau, double* inr,
+                     int* v0, int* v1, int* l, int* r, int* sl, int* sr, double* nx, double* ny, double* h) {
+  const Mesh& m = *static_cast<Mesh*>(mp);
+  for (size_t i = 0; i < m.vertices.size(); ++i) {
+    vx[i] = m.vertices[i].x;
+    vy[i] = m.vertices[i].y;
+  }
+  for (int i = 0; i < m.n_elements(); ++i) {
+    const Element& e = m.elements[i];
+    for (int k = 0; k < 3; ++k) {
+      ev[3 * i + k] = e.v[k];
+      eedge[3 * i + k] = e.edge[k];
+    }
+    det[i] = e.det_jac;
+    for (int k = 0; k < 4; ++k) tau[4 * i + k] = e.tau[k];
+    inr[i] = e.inradius;
+  }
+  for (int k = 0; k < m.n_edges(); ++k) {
+    const Edge& e = m.edges[k];
+    v0[k] = e.v0;
+    v1[k] = e.v1;
+    l[k] = e.left;
+    r[k] = e.right;
+    sl[k] = e.side_left;
+    sr[k] = e.side_right;
+    nx[k] = e.nx;
+    ny[k] = e.ny;
+    h[k] = e.half_length;
+  }
+}
+
+int ref_mesh_dump_edges(void* mp, char* buf, size_t cap, size_t* needed) {
+  std::ostringstream os;
+  dump_edges(*static_cast<Mesh*>(mp), os);
+  std::string s = os.str();
+  *needed = s.size() + 1;
+  if (buf && cap >= s.size() + 1) std::memcpy(buf, s.c_str(), s.size() + 1);
+  return 0;
+}
+
+void* ref_tables(int p) {
+  BasisTables* t = nullptr;
+  if (guard([&] { t = new BasisTables(build_tables(p)); })) return nullptr;
+  return t;
+}
+void ref_tables_free(void* t) { delete static_cast<BasisTables*>(t); }
+void ref_tables_sizes(void* tp, int* sizes) {
+  const BasisTables& t = *static_cast<BasisTables*>(tp);
+  sizes[0] = t.p;
+  sizes[1] = t.n_p;
+  sizes[2] = t.n_quad;
+  sizes[3] = t.n_edge_pts;
+  sizes[4] = static_cast<int>(t.total_stored_doubles());
+}
+void ref_tables_export(void* tp, double* phi, double* dr, double* ds, double* w, double* rs, double* phe, double* we,
+                       double* xi, double* phm) {
+  const BasisTables& t = *static_cast<BasisTables*>(tp);
+  std::memcpy(phi, t.phi_interior.data(), t.phi_interior.size() * 8);
+  std::memcpy(dr, t.dphi_dr_interior.data(), t.dphi_dr_interior.size() * 8);
+  std::memcpy(ds, t.dphi_ds_interior.data(), t.dphi_ds_interior.size() * 8);
+  std::memcpy(w, t.w_interior.data(), t.w_interior.size() * 8);
+  for (int k = 0; k < t.n_quad; ++k) {
+    rs[2 * k] = t.r_interior[k].x;
+    rs[2 * k + 1] = t.r_interior[k].y;
+  }
+  std::memcpy(phe, t.phi_edge.data(), t.phi_edge.size() * 8);
+  std::memcpy(we, t.w_edge.data(), t.w_edge.size() * 8);
+  std::memcpy(xi, t.xi_edge.data(), t.xi_edge.size() * 8);
+  std::memcpy(phm, t.phi_edge_mid.data(), t.phi_edge_mid.size() * 8);
+}
+
+// --------------------------------------------------------------- boundary conditions
+void* ref_bc_new() { return new BoundaryConditions; }
+void ref_bc_free(void* b) { delete static_cast<BoundaryConditions*>(b); }
+void ref_bc_set_inflow(void* b, const double* s) {
+  static_cast<BoundaryConditions*>(b)->inflow_state = {s[0], s[1], s[2], s[3]};
+}
+void ref_bc_set_const_dirichlet(void* b, const double* s) {
+  EulerState st{s[0], s[1], s[2], s[3]};
+  static_cast<BoundaryConditions*>(b)->dirichlet = [st](Vec2, double) { return st; };
+}
+void ref_bc_set_radial_wall(void* b) {
+  static_cast<BoundaryConditions*>(b)->wall_normal = [](Vec2 x) {
+    double r = norm(x);
+    return Vec2{x.x / r, x.y / r};
+  };
+}
+void ref_bc_set_vortex(void* b, double r_in, double r_out, double mach, double rho, double c, double gamma) {
+  VortexGeometry g{r_in, r_out, mach, rho, c};
+  GasModel gas{gamma};
+  *static_cast<BoundaryConditions*>(b) = vortex_boundary(g, gas);
+}
+void ref_bc_set_double_mach(void* b, double x0, double mach, double angle, double gamma) {
+  DoubleMachSetup dm;
+  dm.x0 = x0;
+  dm.shock_mach = mach;
+  dm.angle_deg = angle;
+  GasModel gas{gamma};
+  dm.post = rankine_hugoniot_post(dm.pre, mach, {std::sin(angle * M_PI / 180.0), -std::cos(angle * M_PI / 180.0)}, gas);
+  *static_cast<BoundaryConditions*>(b) = double_mach_boundary(dm, gas);
+}
+void ref_bc_set_shock(void* b, double x0, double angle, double speed, const double* post, const double* pre) {
+  MovingShock s;
+  s.x0 = x0;
+  s.angle_deg = angle;
+  s.speed = speed;
+  s.post = {post[0], post[1], post[2], post[3]};
+  s.pre = {pre[0], pre[1], pre[2], pre[3]};
+  static_cast<BoundaryConditions*>(b)->shock = s;
+}
+// Evaluate the closures at given points (to build the device tables from the
+// reference's own closures).
+int ref_bc_eval(void* b, int code, const double* xy, int n, double t, double* out) {
+  const BoundaryConditions& bc = *static_cast<BoundaryConditions*>(b);
+  return guard([&] {
+    for (int i = 0; i < n; ++i) {
+      Vec2 x{xy[2 * i], xy[2 * i + 1]};
+      if (code == -3) {
+        EulerState s = bc.dirichlet ? bc.dirichlet(x, t) : bc.inflow_state;
+        for (int m = 0; m < 4; ++m) out[4 * i + m] = s[m];
+      } else if (code == -2) {
+        Vec2 w = bc.wall_normal(x);
+        out[2 * i] = w.x;
+        out[2 * i + 1] = w.y;
+      }
+    }
+  });
+}
+void ref_bc_shock_params(void* b, int* has, double* prm, double* post, double* pre) {
+  const BoundaryConditions& bc = *static_cast<BoundaryConditions*>(b);
+  *has = bc.shock ? 1 : 0;
+  if (bc.shock) {
+    prm[0] = bc.shock->x0;
+    prm[1] = bc.shock->angle_deg;
+    prm[2] = bc.shock->speed;
+    for (int m = 0; m < 4; ++m) {
+      post[m] = bc.shock->post[m];
+      pre[m] = bc.shock->pre[m];
+    }
+  }
+  for (int m = 0; m < 4; ++m) prm[3 + m] = bc.inflow_state[m];
+}
+
+// --------------------------------------------------------------- solver
+void* ref_ctx_new(void* mesh, void* tables, void* bc, double gamma, int rk_order, double cfl, int limiting,
+                  int workers) {
+  auto* r = new RefCtx;
+  r->mesh = static_cast<Mesh*>(mesh);
+  r->tables = static_cast<BasisTables*>(tables);
+  r->bc = static_cast<BoundaryConditions*>(bc);
+  r->ctx.mesh = r->mesh;
+  r->ctx.tables = r->tables;
+  r->ctx.gas.gamma = gamma;
+  r->ctx.bc = r->bc;
+  r->ctx.options.rk_order = rk_order;
+  r->ctx.options.cfl = cfl;
+  r->ctx.options.limiting = limiting != 0;
+  r->ctx.options.workers = workers;
+  r->bufs = RhsBuffers(kEq, r->tables->n_p, r->mesh->n_elements());
+  return r;
+}
+void ref_ctx_free(void* r) { delete static_cast<RefCtx*>(r); }
+void ref_ctx_set(void* rp, int rk_order, double cfl, int limiting, int workers) {
+  RefCtx* r = static_cast<RefCtx*>(rp);
+  r->ctx.options.rk_order = rk_order;
+  r->ctx.options.cfl = cfl;
+  r->ctx.options.limiting = limiting != 0;
+  r->ctx.options.workers = workers;
+}
+
+int ref_volume(void* rp, const double* c, double* vol) {
+  RefCtx* r = static_cast<RefCtx*>(rp);
+  return guard([&] {
+    CoefficientArray a = make_coeffs(r, c);
+    eval_volume_pass(r->ctx, a, r->bufs.volume);
+    std::memcpy(vol, r->bufs.volume.data.data(), r->bufs.volume.data.size() * 8);
+  });
+}
+
+int ref_surface(void* rp, const double* c, double t, double* sl, double* sr) {
+  RefCtx* r = static_cast<RefCtx*>(rp);
+  return guard([&] {
+    CoefficientArray a = make_coeffs(r, c);
+    std::fill(r->bufs.surface_left.begin(), r->bufs.surface_left.end(), 0.0);
+    std::fill(r->bufs.surface_right.begin(), r->bufs.surface_right.end(), 0.0);
+    eval_surface_pass(r->ctx, a, t, r->bufs);
+    std::memcpy(sl, r->bufs.surface_left.data(), r->bufs.surface_left.size() * 8);
+    std::memcpy(sr, r->bufs.surface_right.data(), r->bufs.surface_right.size() * 8);
+  });
+}
+
+int ref_gather(void* rp, const double* vol, const double* sl, const double* sr, double* deriv) {
+  RefCtx* r = static_cast<RefCtx*>(rp);
+  return guard([&] {
+    std::memcpy(r->bufs.volume.data.data(), vol, r->bufs.volume.data.size() * 8);
+    std::memcpy(r->bufs.surface_left.data(), sl, r->bufs.surface_left.size() * 8);
+    std::memcpy(r->bufs.surface_right.data(), sr, r->bufs.surface_right.size() * 8);
+    CoefficientArray d(kEq, r->tables->n_p, r->mesh->n_elements());
+    eval_rhs_pass(r->ctx, r->bufs, d);
+    std::memcpy(deriv, d.data.data(), d.data.size() * 8);
+  });
+}
+
+int ref_compute_rhs(void* rp, const double* c, double t, double* deriv) {
+  RefCtx* r = static_cast<RefCtx*>(rp);
+  return guard([&] {
+    CoefficientArray a = make_coeffs(r, c);
+    CoefficientArray d(kEq, r->tables->n_p, r->mesh->n_elements());
+    compute_rhs(r->ctx, a, t, r->bufs, d);
+    std::memcpy(deriv, d.data.data(), d.data.size() * 8);
+  });
+}
+
+int ref_serial_rhs(void* rp, const double* c, double t, double* deriv) {
+  RefCtx* r = static_cast<RefCtx*>(rp);
+  return guard([&] {
+    CoefficientArray a = make_coeffs(r, c);
+    CoefficientArray d = ref::rhs(*r->mesh, *r->tables, r->ctx.gas, *r->bc, a, t);
+    std::memcpy(deriv, d.data.data(), d.data.size() * 8);
+  });
+}
+
+int ref_limit(void* rp, double* c) {
+  RefCtx* r = static_cast<RefCtx*>(rp);
+  return guard([&] {
+    CoefficientArray a = make_coeffs(r, c);
+    limit(r->ctx, a);
+    std::memcpy(c, a.data.data(), a.data.size() * 8);
+  });
+}
+
+int ref_stable_dt(void* rp, const double* c, double* dt) {
+  RefCtx* r = static_cast<RefCtx*>(rp);
+  return guard([&] {
+    CoefficientArray a = make_coeffs(r, c);
+    *dt = stable_dt(r->ctx, a);
+  });
+}
+
+static void on_hist(double* hist, int64_t cap, int64_t s, double res) {
+  if (hist && s - 1 < cap) hist[s - 1] = res;
+}
+
+int ref_rk_step(void* rp, double* c, double* t, int64_t* step, double dt, double* resid) {
+  RefCtx* r = static_cast<RefCtx*>(rp);
+  return guard([&] {
+    SolverState st;
+    st.coeffs = make_coeffs(r, c);
+    st.t = *t;
+    st.step_count = *step;
+    double res = rk_step(r->ctx, st, dt);
+    std::memcpy(c, st.coeffs.data.data(), st.coeffs.data.size() * 8);
+    *t = st.t;
+    *step = st.step_count;
+    *resid = res;
+  });
+}
+
+int ref_run_fixed_steps(void* rp, double* c, double* t, int64_t* step, int64_t n, double* resid, double* hist) {
+  RefCtx* r = static_cast<RefCtx*>(rp);
+  SolverState st;
+  st.coeffs = make_coeffs(r, c);
+  st.t = *t;
+  st.step_count = *step;
+  int rc = guard([&] {
+    *resid = run_fixed_steps(r->ctx, st, n, [&](int64_t s, double res) { on_hist(hist, n, s, res); });
+  });
+  std::memcpy(c, st.coeffs.data.data(), st.coeffs.data.size() * 8);
+  *t = st.t;
+  *step = st.step_count;
+  return rc;
+}
+
+int ref_run_to_time(void* rp, double* c, double* t, int64_t* step, double t_end, int64_t max_steps, double* resid) {
+  RefCtx* r = static_cast<RefCtx*>(rp);
+  SolverState st;
+  st.coeffs = make_coeffs(r, c);
+  st.t = *t;
+  st.step_count = *step;
+  int rc = guard([&] { *resid = run_to_time(r->ctx, st, t_end, max_steps); });
+  std::memcpy(c, st.coeffs.data.data(), st.coeffs.data.size() * 8);
+  *t = st.t;
+  *step = st.step_count;
+  return rc;
+}
+
+int ref_run_to_steady(void* rp, double* c, double* t, int64_t* step, double tol, int64_t max_steps, int64_t* steps,
+                      double* resid, int* converged, double* hist, int64_t cap) {
+  RefCtx* r = static_cast<RefCtx*>(rp);
+  SolverState st;
+  st.coeffs = make_coeffs(r, c);
+  st.t = *t;
+  st.step_count = *step;
+  int rc = guard([&] {
+    SteadyResult sr = run_to_steady(r->ctx, st, tol, max_steps, [&](int64_t s, double res) { on_hist(hist, cap, s, res); });
+    *steps = sr.steps;
+    *resid = sr.residual;
+    *converged = sr.converged ? 1 : 0;
+  });
+  std::memcpy(c, st.coeffs.data.data(), st.coeffs.data.size() * 8);
+  *t = st.t;
+  *step = st.step_count;
+  return rc;
+}
+
+// SSP-RK2 / SSP-RK3 composed from the reference's compute_rhs and limit (the
+// reference has no SSP scheme; this is the harness composition SURVEY.md
+// Appendix A prescribes as their oracle).  scheme: 102 or 103.
+int ref_ssp_step(void* rp, double* c, double* t, int64_t* step, double dt, int scheme, int limiting, double* resid) {
+  RefCtx* r = static_cast<RefCtx*>(rp);
+  return guard([&] {
+    const int n = r->mesh->n_elements();
+    CoefficientArray u = make_coeffs(r, c), s1(kEq, r->tables->n_p, n), s2(kEq, r->tables->n_p, n),
+                     k(kEq, r->tables->n_p, n), out(kEq, r->tables->n_p, n);
+    const size_t sz = u.data.size();
+    compute_rhs(r->ctx, u, *t, r->bufs, k);
+    for (size_t i = 0; i < sz; ++i) s1.data[i] = u.data[i] + dt * k.data[i];
+    if (limiting) limit(r->ctx, s1);
+    compute_rhs(r->ctx, s1, *t + dt, r->bufs, k);
+    if (scheme == 102) {
+      for (size_t i = 0; i < sz; ++i) out.data[i] = std::fma(0.5 * dt, k.data[i], std::fma(0.5, u.data[i], 0.5 * s1.data[i]));
+    } else {
+      for (size_t i = 0; i < sz; ++i)
+        s2.data[i] = std::fma(0.25 * dt, k.data[i], std::fma(0.75, u.data[i], 0.25 * s1.data[i]));
+      if (limiting) limit(r->ctx, s2);
+      compute_rhs(r->ctx, s2, *t + 0.5 * dt, r->bufs, k);
+      const double a = 1.0 / 3.0, b = 2.0 / 3.0;
+      for (size_t i = 0; i < sz; ++i) out.data[i] = std::fma(b * dt, k.data[i], std::fma(a, u.data[i], b * s2.data[i]));
+    }
+    if (limiting) limit(r->ctx, out);
+    *resid = max_abs_diff(u, out);
+    std::memcpy(c, out.data.data(), sz * 8);
+    *t += dt;
+    *step += 1;
+  });
+}
+
+double ref_total_mass(void* rp, const double* c) {
+  RefCtx* r = static_cast<RefCtx*>(rp);
+  CoefficientArray a = make_coeffs(r, c);
+  return total_mass(*r->mesh, a);
+}
+
+// --------------------------------------------------------------- initial data
+// kind 0: constant state prm[0..3]; 1: acceptance smooth_field(seed=prm[0]);
+// 2: vortex_exact (prm: r_in, r_out, mach, rho, c); 3: double Mach initial with
+// front-cut slope zeroing (runner.cpp:100-108, 168-176), prm: x0, mach, angle;
+// 4: test_util smooth_random_field(seed=prm[0], amplitude=prm[1]).
+int ref_project(void* mp, void* tp, double gamma, int kind, const double* prm, double* out) {
+  const Mesh& mesh = *static_cast<Mesh*>(mp);
+  const BasisTables& tb = *static_cast<BasisTables*>(tp);
+  GasModel gas{gamma};
+  return guard([&] {
+    std::function<EulerState(Vec2)> f;
+    if (kind == 0) {
+      EulerState s{prm[0], prm[1], prm[2], prm[3]};
+      f = [s](Vec2) { return s; };
+    } else if (kind == 1) {
+      const unsigned seed = static_cast<unsigned>(prm[0]);
+      double a1 = 0.7 + 0.13 * (seed % 7), a2 = 1.1 + 0.09 * (seed % 5);
+      double ph = 0.31 * (seed % 11);
+      f = [=](Vec2 x) {
+        double s1 = std::sin(a1 * x.x + a2 * x.y + ph);
+        double s2 = std::sin(a2 * x.x - a1 * x.y + 2.0 * ph);
+        return acceptance_state(1.0 + 0.22 * s1, 0.3 * s2, 0.25 * s1, 1.0 + 0.2 * s2);
+      };
+    } else if (kind == 2) {
+      VortexGeometry g{prm[0], prm[1], prm[2], prm[3], prm[4]};
+      f = [g, gas](Vec2 x) { return vortex_exact(x, g, gas); };
+    } else if (kind == 3) {
+      DoubleMachSetup dm;
+      dm.x0 = prm[0];
+      dm.shock_mach = prm[1];
+      dm.angle_deg = prm[2];
+      dm.post = rankine_hugoniot_post(dm.pre, dm.shock_mach,
+                                      {std::sin(dm.angle_deg * M_PI / 180.0), -std::cos(dm.angle_deg * M_PI / 180.0)}, gas);
+      f = [dm](Vec2 x) { return double_mach_initial(x, dm); };
+      CoefficientArray c = project_initial(f, mesh, tb, gas);
+      const double rad = dm.angle_deg * M_PI / 180.0;
+      auto side = [&](Vec2 v) { return v.x < dm.x0 + v.y * std::cos(rad) / std::sin(rad); };
+      for (int i = 0; i < mesh.n_elements(); ++i) {
+        bool sa = side(mesh.vertex_of(i, 0)), sb = side(mesh.vertex_of(i, 1)), sc = side(mesh.vertex_of(i, 2));
+        if (sa == sb && sb == sc) continue;
+        for (int m = 0; m < kEq; ++m)
+          for (int j = 1; j < tb.n_p; ++j) c.at(m, j, i) = 0.0;
+      }
+      std::memcpy(out, c.data.data(), c.data.size() * 8);
+      return;
+    } else if (kind == 4) {
+      std::mt19937 rng(static_cast<unsigned>(prm[0]));
+      const double amplitude = prm[1];
+      std::uniform_real_distribution<double> freq(0.5, 2.5), phase(0.0, 6.28), amp(-1.0, 1.0);
+      struct Wave {
+        double ax, ay, ph, scale;
+      };
+      std::array<Wave, 4> waves;
+      for (Wave& w : waves) w = {freq(rng), freq(rng), phase(rng), amp(rng)};
+      f = [waves, amplitude](Vec2 x) {
+        auto g = [&](int i) {
+          const Wave& w = waves[i];
+          return amplitude * w.scale * std::sin(w.ax * x.x + w.ay * x.y + w.ph);
+        };
+        double rho = 1.0 + g(0), u = 0.5 * g(1), v = 0.5 * g(2), p = 1.0 + g(3);
+        return EulerState{rho, rho * u, rho * v, p / 0.4 + 0.5 * rho * (u * u + v * v)};
+      };
+    } else {
+      throw std::invalid_argument("unknown initial-data kind");
+    }
+    CoefficientArray c = project_initial(f, mesh, tb, gas);
+    std::memcpy(out, c.data.data(), c.data.size() * 8);
+  });
+}
+
+}  // extern "C"

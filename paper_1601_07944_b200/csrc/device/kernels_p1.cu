@@ -1,0 +1,177 @@
+// Kernels for polynomial degree 1 (see kernels_tu.cuh) plus the p = 1
+// Barth-Jespersen limiter with the positivity guard (solver.cpp:286-425).
+#define DGB_P 1
+#include "kernels_tu.cuh"
+
+namespace dgbk {
+
+namespace {
+__constant__ LimTab c_lim;
+
+__device__ __forceinline__ double ref_pressure(double rho, double mx, double my, double E, double g1) {
+  return g1 * (E - 0.5 * (mx * mx + my * my) / rho);
+}
+}  // namespace
+
+namespace {
+// One thread per element, in place on modes 1..2 (mode 0 is never written, so
+// reading the neighbours' means while limiting is race-free, solver.cpp:419-422).
+__global__ void __launch_bounds__(kBlock) k_limit(Geo geo, LimArgs a) {
+  constexpr int NP = 3;
+  const long long ld = geo.ld;
+  const double g1 = geo.gamma - 1.0;
+  const double sqrt2 = sqrt(2.0);
+  Scalars* sc = a.sc;
+  __shared__ int s_stop;
+  if (threadIdx.x == 0) s_stop = (sc->err_key != kNoError || sc->halt) ? 1 : 0;
+  __syncthreads();
+  if (s_stop) return;
+
+  const LimTab& L = c_lim;
+  const Tab<1>& T = c_tab;
+  double lam_min = __longlong_as_double(0x7ff0000000000000ll);
+  double res_max = 0.0;
+
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < geo.ld; e += gridDim.x * blockDim.x) {
+    if (e >= geo.N) continue;
+    double c0[4], c1[4], c2[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      c0[m] = a.c[(m * NP + 0) * ld + e];
+      c1[m] = a.c[(m * NP + 1) * ld + e];
+      c2[m] = a.c[(m * NP + 2) * ld + e];
+    }
+    int nb[3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) nb[q] = __ldg(geo.nbr + q * ld + e);
+
+    // Barth-Jespersen per conserved variable against the neighbours' centroid range
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const double uc = c0[m] * sqrt2;
+      double umax = uc, umin = uc;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        if (nb[q] < 0) continue;
+        const double un = a.c[(m * NP) * ld + nb[q]] * sqrt2;
+        umax = fmax(umax, un);
+        umin = fmin(umin, un);
+      }
+      const double tol = 1e-13 * (fabs(uc) + (umax - umin));
+      double alpha = 1.0;
+      for (int k = L.edge_begin; k < L.edge_begin + L.n_edge; ++k) {
+        const double d = c1[m] * L.phi1[k] + c2[m] * L.phi2[k];
+        double r = 1.0;
+        if (d > tol)
+          r = (umax - uc) / d;
+        else if (d < -tol)
+          r = (umin - uc) / d;
+        alpha = fmin(alpha, fmin(fmax(r, 0.0), 1.0));
+      }
+      c1[m] *= alpha;
+      c2[m] *= alpha;
+    }
+
+    // positivity guard toward the cell mean (solver.cpp:363-417)
+    const double mr = c0[0] * sqrt2, mmx = c0[1] * sqrt2, mmy = c0[2] * sqrt2, mE = c0[3] * sqrt2;
+    const double p_mean = ref_pressure(mr, mmx, mmy, mE, g1);
+    if (mr > 0.0 && p_mean > 0.0) {
+      const double eps_rho = 1e-8 * mr;
+      const double eps_p = 1e-8 * p_mean;
+      double dev[4];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) dev[m] = fabs(c1[m]) * L.max_phi1 + fabs(c2[m]) * L.max_phi2;
+      const double rho_floor = mr - dev[0];
+      bool safe = rho_floor > eps_rho;
+      if (safe) {
+        const double mx_peak = fabs(mmx) + dev[1];
+        const double my_peak = fabs(mmy) + dev[2];
+        const double p_floor = g1 * (mE - dev[3] - 0.5 * (mx_peak * mx_peak + my_peak * my_peak) / rho_floor);
+        safe = p_floor > eps_p;
+      }
+      if (!safe) {
+        double rho_min = mr;
+        for (int k = 0; k < L.n_pts; ++k)
+          rho_min = fmin(rho_min, c0[0] * sqrt2 + c1[0] * L.phi1[k] + c2[0] * L.phi2[k]);
+        if (rho_min < eps_rho) {
+          const double th = fmin(fmax((mr - eps_rho) / (mr - rho_min), 0.0), 1.0);
+          c1[0] *= th;
+          c2[0] *= th;
+        }
+        double th_p = 1.0;
+        for (int k = 0; k < L.n_pts; ++k) {
+          double u[4];
+#pragma unroll
+          for (int m = 0; m < 4; ++m) u[m] = c0[m] * sqrt2 + c1[m] * L.phi1[k] + c2[m] * L.phi2[k];
+          if (u[0] <= 0.0) {
+            th_p = 0.0;
+            break;
+          }
+          const double pk = ref_pressure(u[0], u[1], u[2], u[3], g1);
+          if (pk < eps_p) th_p = fmin(th_p, (p_mean - eps_p) / (p_mean - pk));
+        }
+        if (th_p < 1.0) {
+          th_p = fmax(th_p, 0.0);
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            c1[m] *= th_p;
+            c2[m] *= th_p;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      a.c[(m * NP + 1) * ld + e] = c1[m];
+      a.c[(m * NP + 2) * ld + e] = c2[m];
+    }
+    if (a.want_resid) {
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        res_max = fmax(res_max, fabs(__ldg(a.u + (m * NP + 0) * ld + e) - c0[m]));
+        res_max = fmax(res_max, fabs(__ldg(a.u + (m * NP + 1) * ld + e) - c1[m]));
+        res_max = fmax(res_max, fabs(__ldg(a.u + (m * NP + 2) * ld + e) - c2[m]));
+      }
+    }
+    if (a.want_lambda) {  // CFL bound of the limited state (solver.cpp:439-457)
+      double lam = 0.0;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        double U[4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) U[m] = fma(T.phm[q][2], c2[m], fma(T.phm[q][1], c1[m], T.phm[q][0] * c0[m]));
+        const Prim w = primitives(U, g1);
+        if (!admissible(U, w)) {
+          record_error(sc, err_key(a.seq, kPassDt, __ldg(geo.ref_id + e), q + 1));
+          continue;
+        }
+        const int ed = __ldg(geo.eid + q * ld + e);
+        lam = fmax(lam, fabs(w.vx * __ldg(geo.enx + ed) + w.vy * __ldg(geo.eny + ed)) +
+                            sqrt(geo.gamma * w.p * w.inv));
+      }
+      lam_min = fmin(lam_min, 2.0 * __ldg(geo.inradius + e) / (3.0 * lam));
+    }
+  }
+  const int par = a.step & 1;
+  if (a.want_lambda) block_reduce_atomic<true>(lam_min, &sc->dtmin[par ^ 1]);
+  if (a.want_resid) block_reduce_atomic<false>(res_max, &sc->resid[par]);
+}
+}  // namespace
+
+cudaError_t upload_limtab(const LimTab& t, cudaStream_t s) {
+  return cudaMemcpyToSymbolAsync(c_lim, &t, sizeof(t), 0, cudaMemcpyHostToDevice, s);
+}
+
+int limit_resident_blocks() {
+  static int occ = 0;
+  if (!occ) occ = occupancy(k_limit);
+  return occ;
+}
+
+cudaError_t launch_limit(int grid, const Geo& g, const LimArgs& a, cudaStream_t s) {
+  if (grid <= 0) grid = grid_for(g.ld, limit_resident_blocks());
+  k_limit<<<grid, kBlock, 0, s>>>(g, a);
+  return cudaGetLastError();
+}
+
+}  // namespace dgbk

@@ -1,0 +1,27 @@
+// Host-side launchers exported by the per-degree translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "dg_kernels.cuh"
+
+namespace dgbk {
+
+constexpr int kBlock = 128;
+
+template <int P>
+struct Launch {
+  static cudaError_t upload(const Tab<P>& t, cudaStream_t s);
+  // grid = 0 -> occupancy-sized grid (one wave of resident blocks)
+  static cudaError_t element(int mode, int grid, const Geo& g, const StageArgs& a, cudaStream_t s);
+  static cudaError_t dt(int grid, const Geo& g, const double* c, Scalars* sc, int slot, unsigned long long seq,
+                        cudaStream_t s);
+  static int resident_blocks(int mode);  // blocks per SM for the element kernel
+  static int lanes();                    // G
+};
+
+cudaError_t upload_limtab(const LimTab& t, cudaStream_t s);
+cudaError_t launch_limit(int grid, const Geo& g, const LimArgs& a, cudaStream_t s);
+int limit_resident_blocks();
+
+}  // namespace dgbk

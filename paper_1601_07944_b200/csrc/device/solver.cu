@@ -1,0 +1,1300 @@
+// Device context and C ABI of the solver half (include/dg2d_b200/dg2d_b200.h).
+//
+// Owns the device-resident mesh (SoA, class-renumbered element order), the
+// coefficient slots, the per-run scalars and the step drivers that replace the
+// reference's rk_step_ws / run_* loops (proj/src/solver.cpp:506-613) with a
+// device step loop: dt, stop rules and residuals stay on the GPU and the host
+// synchronises once per batch of steps.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../../include/dg2d_b200/dg2d_b200.h"
+#include "../host/capi_common.hpp"
+#include "dg_kernels.cuh"
+#include "launch.hpp"
+
+using dgbk::Geo;
+using dgbk::LimArgs;
+using dgbk::Scalars;
+using dgbk::StageArgs;
+
+namespace {
+
+constexpr int kWindow = 256;  // renumbering window (elements), multiple of 32
+constexpr int kBatch = 64;    // steps per host synchronisation in open-ended drivers
+
+struct Fail {
+  int code;
+  std::string msg;
+};
+
+#define CU(call)                                                                   \
+  do {                                                                             \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess) throw Fail{DGB_ERR_CUDA, std::string("CUDA: ") + cudaGetErrorString(e_) + " at " #call}; \
+  } while (0)
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  void alloc(size_t count) {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = count;
+    if (count) CU(cudaMalloc(&p, count * sizeof(T)));
+  }
+  void upload(const T* h, size_t count, cudaStream_t s) {
+    alloc(count);
+    if (count) CU(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+};
+
+// ------------------------------------------------------------------ small kernels
+__global__ void k_permute_in(double* __restrict__ dst, const double* __restrict__ src, const int* __restrict__ ref_of,
+                             int n, int ld, int rows) {
+  const long long total = static_cast<long long>(rows) * ld;
+  for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(t / ld), d = static_cast<int>(t % ld);
+    dst[t] = d < n ? src[static_cast<long long>(r) * n + ref_of[d]] : 0.0;
+  }
+}
+
+__global__ void k_permute_out(double* __restrict__ dst, const double* __restrict__ src, const int* __restrict__ ref_of,
+                              int n, int ld, int rows) {
+  const long long total = static_cast<long long>(rows) * ld;
+  for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(t / ld), d = static_cast<int>(t % ld);
+    if (d < n) dst[static_cast<long long>(r) * n + ref_of[d]] = src[t];
+  }
+}
+
+// eval_rhs_pass (solver.cpp:253-277): (volume + slot_0 + slot_1 + slot_2) * (1/det)
+__global__ void k_gather(double* __restrict__ deriv, const double* __restrict__ vol, const double* __restrict__ slots,
+                         const double* __restrict__ inv_det, int n, int ld, int rows) {
+  const long long total = static_cast<long long>(rows) * ld;
+  const long long qs = static_cast<long long>(rows) * ld;
+  for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int d = static_cast<int>(t % ld);
+    if (d >= n) continue;
+    double acc = vol[t];
+    acc += slots[t];
+    acc += slots[qs + t];
+    acc += slots[2 * qs + t];
+    deriv[t] = acc * inv_det[d];
+  }
+}
+
+__global__ void k_max_abs_diff(const double* __restrict__ a, const double* __restrict__ b, int n, int ld, int rows,
+                               unsigned long long* out) {
+  const long long total = static_cast<long long>(rows) * ld;
+  double m = 0.0;
+  for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<long long>(gridDim.x) * blockDim.x) {
+    if (static_cast<int>(t % ld) < n) m = fmax(m, fabs(a[t] - b[t]));
+  }
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, static_cast<unsigned long long>(__double_as_longlong(m)));
+}
+
+int small_grid(long long work) {
+  long long g = (work + 255) / 256;
+  if (g > 148 * 16) g = 148 * 16;
+  if (g < 1) g = 1;
+  return static_cast<int>(g);
+}
+
+double pressure_ref(const double* u, double gamma) {
+  return (gamma - 1.0) * (u[3] - 0.5 * (u[1] * u[1] + u[2] * u[2]) / u[0]);
+}
+
+struct StageSpec {
+  double alpha, beta, gcoef, tcoef;
+  int kmode;
+};
+
+bool scheme_stages(int scheme, std::vector<StageSpec>& st) {
+  switch (scheme) {
+    case DGB_RK2_MIDPOINT:  // solver.cpp:513-519
+      st = {{0.0, 1.0, 0.5, 0.0, 0}, {1.0, 0.0, 1.0, 0.5, 0}};
+      return true;
+    case DGB_RK4_CLASSIC:  // solver.cpp:520-531
+      st = {{0.0, 1.0, 0.5, 0.0, 1}, {1.0, 0.0, 0.5, 0.5, 2}, {1.0, 0.0, 1.0, 0.5, 2}, {0.0, 0.0, 0.0, 1.0, 3}};
+      return true;
+    case DGB_SSP_RK2:  // Heun / SSP(2,2)
+      st = {{0.0, 1.0, 1.0, 0.0, 0}, {0.5, 0.5, 0.5, 1.0, 0}};
+      return true;
+    case DGB_SSP_RK3:  // Shu-Osher SSP(3,3)
+      st = {{0.0, 1.0, 1.0, 0.0, 0}, {0.75, 0.25, 0.25, 1.0, 0}, {1.0 / 3.0, 2.0 / 3.0, 2.0 / 3.0, 0.5, 0}};
+      return true;
+    default:
+      return false;
+  }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ context
+struct dgb_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int p = 1, np = 3, nq = 3, K = 2;
+  int N = 0, ld = 0, n_edges = 0, n_bnd = 0;
+  double gamma = 1.4;
+
+  // host copies needed for diagnostics and reference-layout conversions
+  std::vector<double> vx, vy, det;
+  std::vector<int32_t> elem_v, elem_edge, eleft, eright, esl, esr, ev0, ev1;
+  std::vector<double> enx, eny;
+  std::vector<double> bc_dir, bc_wn;
+  dgb_bc_view bc{};
+  std::vector<double> t_phi, t_phe, t_phm, t_xi;
+  std::vector<int> ref_of, dev_of;
+  std::string bc_error;  // deferred boundary-condition failure (reference throws in the surface pass)
+
+  // device geometry
+  DevBuf<double> d_tau, d_inv_det, d_inradius, d_enx, d_eny, d_eh, d_bstate, d_bwn, d_bx;
+  DevBuf<int> d_nbr, d_eid, d_info, d_ref_id;
+  Geo geo{};
+
+  // coefficient buffers (device order [4][np][ld])
+  DevBuf<double> state[2], input, volume, deriv, stage[2], kacc, slots, staging, hist;
+  int cur = 0;
+  Scalars* d_sc = nullptr;
+  Scalars* h_sc = nullptr;  // pinned mirror
+  unsigned long long* d_red = nullptr;
+  unsigned long long* h_red = nullptr;
+
+  double t = 0.0;
+  int64_t step_count = 0;
+  dgb_abort_info last_abort{};
+
+  // timers
+  bool timing = false;
+  dgb_pass_timers timers{};
+  struct Pending {
+    int cat;
+    cudaEvent_t a, b;
+  };
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> event_pool;
+  int64_t launches = 0;
+  double stage_ms = 0.0;
+  int64_t stage_launches = 0;
+
+  dgbk::Tab<1> tab1;
+  dgbk::Tab<2> tab2;
+  dgbk::Tab<3> tab3;
+  dgbk::Tab<4> tab4;
+  dgbk::Tab<5> tab5;
+  dgbk::LimTab lim{};
+
+  size_t coeff_count() const { return static_cast<size_t>(4) * np * ld; }
+};
+
+namespace {
+
+// Which context's tables currently sit in each degree's constant bank, per device.
+std::map<std::pair<int, int>, const dgb_ctx*> g_bank_owner;
+
+void set_device(dgb_ctx* c) { CU(cudaSetDevice(c->device)); }
+
+cudaEvent_t take_event(dgb_ctx* c) {
+  if (!c->event_pool.empty()) {
+    cudaEvent_t e = c->event_pool.back();
+    c->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  CU(cudaEventCreate(&e));
+  return e;
+}
+
+// category: 0 volume, 1 surface, 2 rhs, 3 limiter, 4 other, 5 stage
+struct Timed {
+  dgb_ctx* c;
+  int cat;
+  cudaEvent_t a = nullptr, b = nullptr;
+  Timed(dgb_ctx* ctx, int category) : c(ctx), cat(category) {
+    if (c->timing) {
+      a = take_event(c);
+      b = take_event(c);
+      CU(cudaEventRecord(a, c->stream));
+    }
+  }
+  ~Timed() {
+    if (c->timing && a) {
+      cudaEventRecord(b, c->stream);
+      c->pending.push_back({cat, a, b});
+    }
+  }
+};
+
+void settle_timers(dgb_ctx* c) {
+  for (auto& pd : c->pending) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, pd.a, pd.b) == cudaSuccess) {
+      const double s = ms * 1e-3;
+      switch (pd.cat) {
+        case 0: c->timers.volume += s; break;
+        case 1: c->timers.surface += s; break;
+        case 2: c->timers.rhs += s; break;
+        case 3: c->timers.limiter += s; break;
+        case 4: c->timers.other += s; break;
+        default:
+          c->timers.stage += s;
+          c->stage_ms += ms;
+          break;
+      }
+    }
+    c->event_pool.push_back(pd.a);
+    c->event_pool.push_back(pd.b);
+  }
+  c->pending.clear();
+}
+
+void sync(dgb_ctx* c) {
+  CU(cudaStreamSynchronize(c->stream));
+  settle_timers(c);
+}
+
+template <int P>
+void upload_tab(dgb_ctx* c, dgbk::Tab<P>& tab) {
+  auto key = std::make_pair(c->device, P);
+  if (g_bank_owner[key] != c) {
+    CU(dgbk::Launch<P>::upload(tab, c->stream));
+    g_bank_owner[key] = c;
+  }
+}
+
+void ensure_tables(dgb_ctx* c) {
+  switch (c->p) {
+    case 1:
+      upload_tab<1>(c, c->tab1);
+      {
+        auto key = std::make_pair(c->device, 100);
+        if (g_bank_owner[key] != c) {
+          CU(dgbk::upload_limtab(c->lim, c->stream));
+          g_bank_owner[key] = c;
+        }
+      }
+      break;
+    case 2: upload_tab<2>(c, c->tab2); break;
+    case 3: upload_tab<3>(c, c->tab3); break;
+    case 4: upload_tab<4>(c, c->tab4); break;
+    default: upload_tab<5>(c, c->tab5); break;
+  }
+}
+
+template <int P>
+void fill_tab(dgbk::Tab<P>& T, const dgb_tables_view* t) {
+  constexpr int NP = dgbk::Dim<P>::NP, NQ = dgbk::Dim<P>::NQ, K = dgbk::Dim<P>::K;
+  for (int k = 0; k < NQ; ++k)
+    for (int j = 0; j < NP; ++j) {
+      T.phi[k][j] = t->phi_interior[k * NP + j];
+      T.drw[k][j] = t->w_interior[k] * t->dphi_dr_interior[k * NP + j];
+      T.dsw[k][j] = t->w_interior[k] * t->dphi_ds_interior[k * NP + j];
+    }
+  for (int q = 0; q < 3; ++q)
+    for (int k = 0; k < K; ++k)
+      for (int j = 0; j < NP; ++j) T.phe[q][k][j] = t->phi_edge[(q * K + k) * NP + j];
+  for (int k = 0; k < K; ++k) T.we[k] = t->w_edge[k];
+  for (int q = 0; q < 3; ++q)
+    for (int j = 0; j < NP; ++j) T.phm[q][j] = t->phi_edge_mid[q * NP + j];
+}
+
+cudaError_t launch_element(dgb_ctx* c, int mode, const StageArgs& a) {
+  switch (c->p) {
+    case 1: return dgbk::Launch<1>::element(mode, 0, c->geo, a, c->stream);
+    case 2: return dgbk::Launch<2>::element(mode, 0, c->geo, a, c->stream);
+    case 3: return dgbk::Launch<3>::element(mode, 0, c->geo, a, c->stream);
+    case 4: return dgbk::Launch<4>::element(mode, 0, c->geo, a, c->stream);
+    default: return dgbk::Launch<5>::element(mode, 0, c->geo, a, c->stream);
+  }
+}
+
+cudaError_t launch_dt(dgb_ctx* c, const double* coeffs, int slot, unsigned long long seq) {
+  switch (c->p) {
+    case 1: return dgbk::Launch<1>::dt(0, c->geo, coeffs, c->d_sc, slot, seq, c->stream);
+    case 2: return dgbk::Launch<2>::dt(0, c->geo, coeffs, c->d_sc, slot, seq, c->stream);
+    case 3: return dgbk::Launch<3>::dt(0, c->geo, coeffs, c->d_sc, slot, seq, c->stream);
+    case 4: return dgbk::Launch<4>::dt(0, c->geo, coeffs, c->d_sc, slot, seq, c->stream);
+    default: return dgbk::Launch<5>::dt(0, c->geo, coeffs, c->d_sc, slot, seq, c->stream);
+  }
+}
+
+double* slot_ptr(dgb_ctx* c, int slot) {
+  switch (slot) {
+    case DGB_SLOT_STATE: return c->state[c->cur].p;
+    case DGB_SLOT_INPUT:
+      if (!c->input.p) {
+        c->input.alloc(c->coeff_count());
+        CU(cudaMemsetAsync(c->input.p, 0, c->coeff_count() * 8, c->stream));
+      }
+      return c->input.p;
+    case DGB_SLOT_VOLUME:
+      if (!c->volume.p) {
+        c->volume.alloc(c->coeff_count());
+        CU(cudaMemsetAsync(c->volume.p, 0, c->coeff_count() * 8, c->stream));
+      }
+      return c->volume.p;
+    case DGB_SLOT_DERIV:
+      if (!c->deriv.p) {
+        c->deriv.alloc(c->coeff_count());
+        CU(cudaMemsetAsync(c->deriv.p, 0, c->coeff_count() * 8, c->stream));
+      }
+      return c->deriv.p;
+    default:
+      throw Fail{DGB_ERR_ARG, "unknown coefficient slot " + std::to_string(slot)};
+  }
+}
+
+void reset_scalars(dgb_ctx* c, double t0) {
+  Scalars& s = *c->h_sc;
+  s.err_key = dgbk::kNoError;
+  s.halt = 0;
+  s.halt_step = 0;
+  s.t[0] = t0;
+  s.t[1] = t0;
+  s.dtmin[0] = s.dtmin[1] = 0x7ff0000000000000ull;
+  s.resid[0] = s.resid[1] = 0ull;
+  s.dt_used[0] = s.dt_used[1] = 0.0;
+  CU(cudaMemcpyAsync(c->d_sc, c->h_sc, sizeof(Scalars), cudaMemcpyHostToDevice, c->stream));
+}
+
+void read_scalars(dgb_ctx* c) {
+  CU(cudaMemcpyAsync(c->h_sc, c->d_sc, sizeof(Scalars), cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+}
+
+void download_dev(dgb_ctx* c, const double* dev, int rows, double* host) {
+  if (c->staging.n < static_cast<size_t>(rows) * c->N) c->staging.alloc(static_cast<size_t>(rows) * c->N);
+  k_permute_out<<<small_grid(static_cast<long long>(rows) * c->ld), 256, 0, c->stream>>>(
+      c->staging.p, dev, c->d_ref_id.p, c->N, c->ld, rows);
+  CU(cudaGetLastError());
+  ++c->launches;
+  CU(cudaMemcpyAsync(host, c->staging.p, sizeof(double) * rows * c->N, cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+}
+
+void upload_dev(dgb_ctx* c, double* dev, int rows, const double* host) {
+  if (c->staging.n < static_cast<size_t>(rows) * c->N) c->staging.alloc(static_cast<size_t>(rows) * c->N);
+  CU(cudaMemcpyAsync(c->staging.p, host, sizeof(double) * rows * c->N, cudaMemcpyHostToDevice, c->stream));
+  k_permute_in<<<small_grid(static_cast<long long>(rows) * c->ld), 256, 0, c->stream>>>(
+      dev, c->staging.p, c->d_ref_id.p, c->N, c->ld, rows);
+  CU(cudaGetLastError());
+  ++c->launches;
+}
+
+// Host recomputation of the failing state for the SolverAbort message
+// (solver.cpp:57-62); only runs after a device error.  Ghost states follow
+// euler.hpp:118-140.
+void ghost_host(const dgb_ctx* c, const double* ul, int code, int e, int k, double t, double* ur) {
+  auto reflect = [&](double nx, double ny) {
+    const double mn = 2.0 * (ul[1] * nx + ul[2] * ny);
+    ur[0] = ul[0];
+    ur[1] = ul[1] - mn * nx;
+    ur[2] = ul[2] - mn * ny;
+    ur[3] = ul[3];
+  };
+  const size_t pk = static_cast<size_t>(e) * c->K + k;
+  switch (code) {
+    case -1: reflect(c->enx[e], c->eny[e]); break;
+    case -2: reflect(c->bc_wn[2 * pk], c->bc_wn[2 * pk + 1]); break;
+    case -3:
+      std::memcpy(ur, c->bc_dir.empty() ? c->bc.inflow_state : &c->bc_dir[4 * pk], 4 * sizeof(double));
+      break;
+    case -5: {
+      const double xi = c->t_xi[k];
+      const double wa = 0.5 * (1.0 - xi), wb = 0.5 * (1.0 + xi);
+      const double x = wa * c->vx[c->ev0[e]] + wb * c->vx[c->ev1[e]];
+      const double y = wa * c->vy[c->ev0[e]] + wb * c->vy[c->ev1[e]];
+      const double front = c->geo.sh_x0 + (y * c->geo.sh_cos + c->geo.sh_speed * t) / c->geo.sh_sin;
+      std::memcpy(ur, x < front ? c->bc.shock_post : c->bc.shock_pre, 4 * sizeof(double));
+      break;
+    }
+    default: std::memcpy(ur, ul, 4 * sizeof(double)); break;
+  }
+}
+
+std::string failure_message(dgb_ctx* c, unsigned long long key, const double* dev_in, double t_stage) {
+  const int pass = static_cast<int>((key >> 35) & 7);
+  const long long id = static_cast<long long>((key >> 5) & 0x3fffffff);
+  const int point = static_cast<int>(key & 31);
+  std::vector<double> h(static_cast<size_t>(4) * c->np * c->N);
+  download_dev(c, dev_in, 4 * c->np, h.data());
+  auto coef = [&](int m, int j, int i) { return h[(static_cast<size_t>(m) * c->np + j) * c->N + i]; };
+  double u[4] = {0, 0, 0, 0};
+  const char* where = "eval_volume";
+  if (pass == dgbk::kPassVolume) {
+    for (int m = 0; m < 4; ++m) {
+      double s = 0.0;
+      for (int j = 0; j < c->np; ++j) s += coef(m, j, static_cast<int>(id)) * c->t_phi[point * c->np + j];
+      u[m] = s;
+    }
+  } else if (pass == dgbk::kPassDt) {
+    where = "stable_dt";
+    for (int m = 0; m < 4; ++m) {
+      double s = 0.0;
+      for (int j = 0; j < c->np; ++j) s += coef(m, j, static_cast<int>(id)) * c->t_phm[(point - 1) * c->np + j];
+      u[m] = s;
+    }
+  } else {
+    where = "eval_surface";
+    const int e = static_cast<int>(id);
+    const int L = c->eleft[e], R = c->eright[e];
+    double ul[4], ur[4];
+    for (int m = 0; m < 4; ++m) {
+      double s = 0.0;
+      for (int j = 0; j < c->np; ++j) s += coef(m, j, L) * c->t_phe[((c->esl[e] - 1) * c->K + point) * c->np + j];
+      ul[m] = s;
+    }
+    if (R >= 0) {
+      for (int m = 0; m < 4; ++m) {
+        double s = 0.0;
+        for (int j = 0; j < c->np; ++j)
+          s += coef(m, j, R) * c->t_phe[((c->esr[e] - 1) * c->K + (c->K - 1 - point)) * c->np + j];
+        ur[m] = s;
+      }
+    } else {
+      ghost_host(c, ul, R, e, point, t_stage, ur);
+    }
+    const bool okl = ul[0] > 0.0 && pressure_ref(ul, c->gamma) > 0.0;
+    std::memcpy(u, okl ? ur : ul, sizeof u);
+  }
+  const double pr = pressure_ref(u, c->gamma);
+  std::snprintf(c->last_abort.where, sizeof c->last_abort.where, "%s", where);
+  c->last_abort.id = id;
+  c->last_abort.point = point;
+  c->last_abort.rho = u[0];
+  c->last_abort.p = pr;
+  return std::string(where) + ": inadmissible state at id " + std::to_string(id) + ", point " +
+         std::to_string(point) + " (rho=" + std::to_string(u[0]) + ", p=" + std::to_string(pr) + ")";
+}
+
+void check_bc(dgb_ctx* c) {
+  if (!c->bc_error.empty()) throw Fail{DGB_ERR_BC, "eval_surface: " + c->bc_error};
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    return f();
+  } catch (const Fail& e) {
+    dgb::set_message(e.msg);
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    dgb::set_message("out of host memory");
+    return DGB_ERR_ARG;
+  } catch (const std::exception& e) {
+    dgb::set_message(e.what());
+    return DGB_ERR_ARG;
+  }
+}
+
+// Pass-level launch with an immediate error check.
+void run_pass(dgb_ctx* c, int mode, const double* in, double* out, double t, int cat) {
+  ensure_tables(c);
+  reset_scalars(c, t);
+  StageArgs a{};
+  a.in = in;
+  a.u = in;
+  a.out = out;
+  a.kacc = nullptr;
+  a.t_host = t;
+  a.use_t_host = 1;
+  a.seq = 1;
+  a.seq_next = 2;
+  a.sc = c->d_sc;
+  {
+    Timed tm(c, cat);
+    CU(launch_element(c, mode, a));
+    ++c->launches;
+  }
+  read_scalars(c);
+  if (c->h_sc->err_key != dgbk::kNoError) throw Fail{DGB_ERR_INADMISSIBLE, failure_message(c, c->h_sc->err_key, in, t)};
+}
+
+// ------------------------------------------------------------------ the device step loop
+struct RunSpec {
+  int scheme;
+  int dt_mode;  // 0 host dt, 1 stable dt
+  double dt_host = 0.0, cfl = 0.3;
+  bool limiting = false;
+  int64_t max_steps = 1;
+  bool clip = false, stop_t = false, stop_steady = false;
+  double t_end = 0.0, tol = 0.0;
+  double* hist = nullptr;  // host history
+  int64_t hist_cap = 0;
+};
+
+struct RunOut {
+  int64_t steps = 0;
+  double residual = 0.0;
+  bool halted = false;
+};
+
+RunOut run_steps(dgb_ctx* c, const RunSpec& r) {
+  std::vector<StageSpec> st;
+  if (!scheme_stages(r.scheme, st)) throw Fail{DGB_ERR_ARG, "rk_order must be 2 or 4"};
+  if (r.limiting && c->p != 1) throw Fail{DGB_ERR_ARG, "slope limiting is only supported for p = 1"};
+  check_bc(c);
+  ensure_tables(c);
+  const int S = static_cast<int>(st.size());
+  if (!c->stage[0].p) c->stage[0].alloc(c->coeff_count());
+  if (!c->stage[1].p) c->stage[1].alloc(c->coeff_count());
+  if (r.scheme == DGB_RK4_CLASSIC && !c->kacc.p) c->kacc.alloc(c->coeff_count());
+  if (!c->state[1 - c->cur].p) c->state[1 - c->cur].alloc(c->coeff_count());
+  double* d_hist = nullptr;
+  if (r.hist && r.hist_cap > 0) {
+    if (c->hist.n < static_cast<size_t>(r.hist_cap)) c->hist.alloc(r.hist_cap);
+    d_hist = c->hist.p;
+  }
+
+  const int cur0 = c->cur;
+  reset_scalars(c, c->t);
+  if (r.dt_mode == 1) {
+    Timed tm(c, 4);
+    CU(launch_dt(c, c->state[cur0].p, 0, 0));
+    ++c->launches;
+  }
+  RunOut out;
+  int64_t launched = 0;
+  bool stop = false;
+  while (!stop && launched < r.max_steps) {
+    const int64_t batch = std::min<int64_t>(r.max_steps - launched,
+                                             (r.stop_t || r.stop_steady) ? kBatch : r.max_steps);
+    for (int64_t b = 0; b < batch; ++b) {
+      const int64_t s = launched + b;
+      double* u = c->state[(cur0 + s) & 1].p;
+      double* unext = c->state[(cur0 + s + 1) & 1].p;
+      for (int k = 0; k < S; ++k) {
+        const bool last = k == S - 1;
+        StageArgs a{};
+        a.in = k == 0 ? u : c->stage[(k - 1) & 1].p;
+        a.u = u;
+        a.out = last ? unext : c->stage[k & 1].p;
+        a.kacc = c->kacc.p;
+        a.alpha = st[k].alpha;
+        a.beta = st[k].beta;
+        a.gcoef = st[k].gcoef;
+        a.tcoef = st[k].tcoef;
+        a.kmode = st[k].kmode;
+        a.dt_mode = r.dt_mode;
+        a.dt_host = r.dt_host;
+        a.cfl = r.cfl;
+        a.t_end = r.t_end;
+        a.clip_t_end = r.clip;
+        a.stop_at_t_end = r.stop_t;
+        a.stop_steady = r.stop_steady;
+        a.tol = r.tol;
+        a.step = static_cast<int>(s);
+        a.first = k == 0;
+        a.last = last;
+        a.want_lambda = last && !r.limiting && r.dt_mode == 1;
+        a.want_resid = last && !r.limiting;
+        a.seq = static_cast<unsigned long long>(s) * 8 + k + 1;
+        a.seq_next = static_cast<unsigned long long>(s + 1) * 8;
+        a.sc = c->d_sc;
+        a.hist = d_hist && s <= r.hist_cap ? d_hist : nullptr;
+        {
+          Timed tm(c, 5);
+          CU(launch_element(c, dgbk::kModeStage, a));
+          ++c->launches;
+          ++c->stage_launches;
+        }
+        if (r.limiting) {
+          LimArgs la{};
+          la.c = a.out;
+          la.u = u;
+          la.step = static_cast<int>(s);
+          la.want_lambda = last && r.dt_mode == 1;
+          la.want_resid = last;
+          la.seq = static_cast<unsigned long long>(s + 1) * 8;
+          la.sc = c->d_sc;
+          Timed tm(c, 3);
+          CU(dgbk::launch_limit(0, c->geo, la, c->stream));
+          ++c->launches;
+        }
+      }
+    }
+    launched += batch;
+    read_scalars(c);
+    const Scalars& h = *c->h_sc;
+    if (h.err_key != dgbk::kNoError) {
+      const unsigned long long seq = h.err_key >> 38;
+      const int64_t s_fail = static_cast<int64_t>(seq >> 3);
+      const int kst = static_cast<int>(seq & 7);
+      const double* in = (kst <= 1) ? c->state[(cur0 + s_fail) & 1].p : c->stage[(kst - 2) & 1].p;
+      // the failed step leaves the state untouched (rk_step_ws throws before the swap)
+      c->cur = static_cast<int>((cur0 + s_fail) & 1);
+      c->t = h.t[s_fail & 1];
+      c->step_count += s_fail;
+      if (d_hist && s_fail > 0) {
+        const int64_t n = std::min<int64_t>(s_fail, r.hist_cap);
+        CU(cudaMemcpyAsync(r.hist, d_hist, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+      }
+      const double tst = h.t[s_fail & 1];
+      throw Fail{DGB_ERR_INADMISSIBLE, failure_message(c, h.err_key, in, tst)};
+    }
+    if (h.halt) {
+      stop = true;
+      out.halted = true;
+      out.steps = h.halt_step;
+    }
+  }
+  if (!out.halted) out.steps = launched;
+  const Scalars& h = *c->h_sc;
+  if (out.steps > 0) out.residual = __builtin_bit_cast(double, h.resid[(out.steps - 1) & 1]);
+  if (d_hist && out.steps > 0) {
+    const int64_t n = std::min<int64_t>(out.steps, r.hist_cap);
+    // the last step's residual is only in the scalars (hist[s-1] is written by step s)
+    if (n > 1) CU(cudaMemcpyAsync(r.hist, d_hist, sizeof(double) * (n - 1), cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    if (out.steps <= r.hist_cap) r.hist[out.steps - 1] = out.residual;
+  }
+  c->cur = static_cast<int>((cur0 + out.steps) & 1);
+  c->t = h.t[out.steps & 1];
+  c->step_count += out.steps;
+  return out;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ C ABI
+extern "C" {
+
+int dgb_create(const dgb_mesh_view* m, const dgb_tables_view* t, const dgb_bc_view* bc, double gamma, int device,
+               dgb_ctx** out) {
+  return guarded([&] {
+    if (!m || !t || !out) throw Fail{DGB_ERR_ARG, "null argument"};
+    if (t->p < 1 || t->p > 5) throw Fail{DGB_ERR_ARG, "polynomial degree must be in [1,5]"};
+    const int np = (t->p + 1) * (t->p + 2) / 2;
+    const int nq_expect[5] = {3, 6, 12, 16, 25};
+    if (t->n_p != np || t->n_quad != nq_expect[t->p - 1] || t->n_edge_pts != t->p + 1)
+      throw Fail{DGB_ERR_ARG, "tables do not match the expected sizes for p = " + std::to_string(t->p)};
+    if (m->n_elements <= 0) throw Fail{DGB_ERR_ARG, "empty mesh"};
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+      throw Fail{DGB_ERR_CUDA, "no CUDA device available (the B200 path has no CPU fallback)"};
+    if (device < 0 || device >= ndev) throw Fail{DGB_ERR_ARG, "bad device ordinal"};
+    std::unique_ptr<dgb_ctx> c(new dgb_ctx);
+    c->device = device;
+    set_device(c.get());
+    CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    c->own_stream = true;
+    c->p = t->p;
+    c->np = np;
+    c->nq = t->n_quad;
+    c->K = t->n_edge_pts;
+    c->gamma = gamma;
+    const int N = m->n_elements;
+    c->N = N;
+    c->ld = (N + 31) / 32 * 32;
+    c->n_edges = m->n_edges;
+    c->n_bnd = m->n_boundary_edges;
+    const int ld = c->ld;
+
+    c->vx.assign(m->vx, m->vx + m->n_vertices);
+    c->vy.assign(m->vy, m->vy + m->n_vertices);
+    c->det.assign(m->det_jac, m->det_jac + N);
+    c->elem_v.assign(m->elem_v, m->elem_v + 3 * static_cast<size_t>(N));
+    c->elem_edge.assign(m->elem_edge, m->elem_edge + 3 * static_cast<size_t>(N));
+    c->eleft.assign(m->edge_left, m->edge_left + m->n_edges);
+    c->eright.assign(m->edge_right, m->edge_right + m->n_edges);
+    c->esl.assign(m->edge_side_left, m->edge_side_left + m->n_edges);
+    c->esr.assign(m->edge_side_right, m->edge_side_right + m->n_edges);
+    c->ev0.assign(m->edge_v0, m->edge_v0 + m->n_edges);
+    c->ev1.assign(m->edge_v1, m->edge_v1 + m->n_edges);
+    c->enx.assign(m->edge_nx, m->edge_nx + m->n_edges);
+    c->eny.assign(m->edge_ny, m->edge_ny + m->n_edges);
+    c->t_phi.assign(t->phi_interior, t->phi_interior + c->nq * np);
+    c->t_phe.assign(t->phi_edge, t->phi_edge + 3 * c->K * np);
+    c->t_phm.assign(t->phi_edge_mid, t->phi_edge_mid + 3 * np);
+    c->t_xi.assign(t->xi_edge, t->xi_edge + c->K);
+
+    // --- element classes: the neighbour's side label per side; windowed stable
+    // sort so every warp sees one class (warp-uniform neighbour-trace switch)
+    std::vector<int> cls(N);
+    std::vector<int> nb_side(3 * static_cast<size_t>(N)), nb_id(3 * static_cast<size_t>(N)), left_bits(N, 0);
+    for (int i = 0; i < N; ++i) {
+      int key = 0;
+      for (int q = 0; q < 3; ++q) {
+        const int e = m->elem_edge[3 * i + q];
+        if (e < 0 || e >= m->n_edges) throw Fail{DGB_ERR_MESH, "element edge id out of range"};
+        const bool left = m->edge_left[e] == i;
+        int s = 0, nb;
+        if (m->edge_right[e] < 0) {
+          nb = m->edge_right[e];
+          if (!left) throw Fail{DGB_ERR_MESH, "boundary edge whose left element is not its owner"};
+        } else {
+          nb = left ? m->edge_right[e] : m->edge_left[e];
+          s = left ? m->edge_side_right[e] : m->edge_side_left[e];
+        }
+        nb_side[3 * i + q] = s;
+        nb_id[3 * i + q] = nb;
+        if (left) left_bits[i] |= 1 << q;
+        key |= s << (2 * q);
+      }
+      cls[i] = key;
+    }
+    c->ref_of.resize(N);
+    for (int i = 0; i < N; ++i) c->ref_of[i] = i;
+    for (int w0 = 0; w0 < N; w0 += kWindow) {
+      const int w1 = std::min(N, w0 + kWindow);
+      std::stable_sort(c->ref_of.begin() + w0, c->ref_of.begin() + w1,
+                       [&](int a, int b) { return cls[a] < cls[b]; });
+    }
+    c->dev_of.resize(N);
+    for (int d = 0; d < N; ++d) c->dev_of[c->ref_of[d]] = d;
+
+    std::vector<double> tau(4 * static_cast<size_t>(ld), 0.0), inv_det(ld, 1.0), inr(ld, 1.0);
+    std::vector<int> nbr(3 * static_cast<size_t>(ld), -4), eid(3 * static_cast<size_t>(ld), 0), info(ld, 0),
+        ref_id(ld, 0);
+    for (int d = 0; d < N; ++d) {
+      const int i = c->ref_of[d];
+      for (int k = 0; k < 4; ++k) tau[static_cast<size_t>(k) * ld + d] = m->tau[4 * static_cast<size_t>(i) + k];
+      inv_det[d] = 1.0 / m->det_jac[i];
+      inr[d] = m->inradius[i];
+      int bits = 0;
+      for (int q = 0; q < 3; ++q) {
+        const int nb = nb_id[3 * i + q];
+        nbr[static_cast<size_t>(q) * ld + d] = nb >= 0 ? c->dev_of[nb] : nb;
+        eid[static_cast<size_t>(q) * ld + d] = m->elem_edge[3 * i + q];
+        bits |= nb_side[3 * i + q] << (2 * q);
+        if (left_bits[i] & (1 << q)) bits |= 1 << (6 + q);
+      }
+      info[d] = bits;
+      ref_id[d] = i;
+    }
+    c->d_tau.upload(tau.data(), tau.size(), c->stream);
+    c->d_inv_det.upload(inv_det.data(), ld, c->stream);
+    c->d_inradius.upload(inr.data(), ld, c->stream);
+    c->d_nbr.upload(nbr.data(), nbr.size(), c->stream);
+    c->d_eid.upload(eid.data(), eid.size(), c->stream);
+    c->d_info.upload(info.data(), ld, c->stream);
+    c->d_ref_id.upload(ref_id.data(), ld, c->stream);
+    c->d_enx.upload(m->edge_nx, m->n_edges, c->stream);
+    c->d_eny.upload(m->edge_ny, m->n_edges, c->stream);
+    c->d_eh.upload(m->edge_half_length, m->n_edges, c->stream);
+
+    // --- boundary data (closures evaluated by the caller at the Gauss points)
+    const int K = c->K, nb = c->n_bnd;
+    dgb_bc_view bcv{};
+    if (bc) bcv = *bc;
+    c->bc = bcv;
+    std::vector<double> bx(2 * static_cast<size_t>(std::max(nb, 1)) * K, 0.0);
+    for (int e = 0; e < nb; ++e) {
+      const double ax = m->vx[m->edge_v0[e]], ay = m->vy[m->edge_v0[e]];
+      const double bxx = m->vx[m->edge_v1[e]], byy = m->vy[m->edge_v1[e]];
+      for (int k = 0; k < K; ++k) {
+        const double xi = t->xi_edge[k];
+        const double wa = 0.5 * (1.0 - xi), wb = 0.5 * (1.0 + xi);
+        bx[2 * (static_cast<size_t>(e) * K + k)] = wa * ax + wb * bxx;
+        bx[2 * (static_cast<size_t>(e) * K + k) + 1] = wa * ay + wb * byy;
+      }
+    }
+    c->d_bx.upload(bx.data(), bx.size(), c->stream);
+    bool has_curved = false, has_shock = false;
+    for (int e = 0; e < nb; ++e) {
+      const int code = m->edge_right[e];
+      if (code == -2) has_curved = true;
+      if (code == -5) has_shock = true;
+      if (code < -5 && c->bc_error.empty()) c->bc_error = "unknown boundary code " + std::to_string(code);
+    }
+    if (bcv.dirichlet_state) {
+      c->bc_dir.assign(bcv.dirichlet_state, bcv.dirichlet_state + 4 * static_cast<size_t>(nb) * K);
+      c->d_bstate.upload(c->bc_dir.data(), c->bc_dir.size(), c->stream);
+    } else {
+      double z[4] = {0, 0, 0, 0};
+      c->d_bstate.upload(z, 4, c->stream);
+    }
+    if (bcv.wall_normal) {
+      c->bc_wn.assign(bcv.wall_normal, bcv.wall_normal + 2 * static_cast<size_t>(nb) * K);
+      c->d_bwn.upload(c->bc_wn.data(), c->bc_wn.size(), c->stream);
+    } else {
+      double z[2] = {0, 0};
+      c->d_bwn.upload(z, 2, c->stream);
+      if (has_curved && c->bc_error.empty()) c->bc_error = "curved reflecting boundary needs a wall-normal function";
+    }
+    if (has_shock && !bcv.has_shock && c->bc_error.empty())
+      c->bc_error = "moving-shock boundary needs shock parameters";
+
+    Geo& g = c->geo;
+    g.N = N;
+    g.ld = ld;
+    g.tau = c->d_tau.p;
+    g.inv_det = c->d_inv_det.p;
+    g.inradius = c->d_inradius.p;
+    g.nbr = c->d_nbr.p;
+    g.eid = c->d_eid.p;
+    g.info = c->d_info.p;
+    g.ref_id = c->d_ref_id.p;
+    g.enx = c->d_enx.p;
+    g.eny = c->d_eny.p;
+    g.eh = c->d_eh.p;
+    g.bstate = c->d_bstate.p;
+    g.bwn = c->d_bwn.p;
+    g.bx = c->d_bx.p;
+    g.has_dir = bcv.dirichlet_state ? 1 : 0;
+    g.has_wn = bcv.wall_normal ? 1 : 0;
+    g.has_shock = bcv.has_shock;
+    for (int k = 0; k < 4; ++k) {
+      g.inflow[k] = bcv.inflow_state[k];
+      g.sh_post[k] = bcv.shock_post[k];
+      g.sh_pre[k] = bcv.shock_pre[k];
+    }
+    const double rad = bcv.shock_angle_deg * M_PI / 180.0;
+    g.sh_x0 = bcv.shock_x0;
+    g.sh_cos = std::cos(rad);
+    g.sh_sin = std::sin(rad);
+    g.sh_speed = bcv.shock_speed;
+    g.gamma = gamma;
+
+    // --- tables
+    switch (c->p) {
+      case 1: fill_tab<1>(c->tab1, t); break;
+      case 2: fill_tab<2>(c->tab2, t); break;
+      case 3: fill_tab<3>(c->tab3, t); break;
+      case 4: fill_tab<4>(c->tab4, t); break;
+      default: fill_tab<5>(c->tab5, t); break;
+    }
+    if (c->p == 1) {  // limiter evaluation points (solver.cpp:296-321)
+      dgbk::LimTab& L = c->lim;
+      int idx = 0;
+      for (int k = 0; k < c->nq; ++k, ++idx) {
+        L.phi1[idx] = t->phi_interior[k * np + 1];
+        L.phi2[idx] = t->phi_interior[k * np + 2];
+      }
+      for (int q = 0; q < 3; ++q)
+        for (int k = 0; k < K; ++k, ++idx) {
+          L.phi1[idx] = t->phi_edge[(q * K + k) * np + 1];
+          L.phi2[idx] = t->phi_edge[(q * K + k) * np + 2];
+        }
+      for (int q = 0; q < 3; ++q, ++idx) {
+        L.phi1[idx] = t->phi_edge_mid[q * np + 1];
+        L.phi2[idx] = t->phi_edge_mid[q * np + 2];
+      }
+      L.n_pts = idx;
+      L.edge_begin = c->nq;
+      L.n_edge = 3 * K;
+      L.max_phi1 = 0.0;
+      L.max_phi2 = 0.0;
+      for (int k = 0; k < idx; ++k) {
+        L.max_phi1 = std::max(L.max_phi1, std::abs(L.phi1[k]));
+        L.max_phi2 = std::max(L.max_phi2, std::abs(L.phi2[k]));
+      }
+    }
+
+    // --- scalars and state
+    CU(cudaMalloc(&c->d_sc, sizeof(Scalars)));
+    CU(cudaMallocHost(&c->h_sc, sizeof(Scalars)));
+    CU(cudaMalloc(&c->d_red, sizeof(unsigned long long)));
+    CU(cudaMallocHost(&c->h_red, sizeof(unsigned long long)));
+    c->state[0].alloc(c->coeff_count());
+    CU(cudaMemsetAsync(c->state[0].p, 0, c->coeff_count() * sizeof(double), c->stream));
+    reset_scalars(c.get(), 0.0);
+    sync(c.get());
+    *out = c.release();
+    return DGB_OK;
+  });
+}
+
+int dgb_destroy(dgb_ctx* c) {
+  if (!c) return DGB_OK;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (auto& pd : c->pending) {
+    cudaEventDestroy(pd.a);
+    cudaEventDestroy(pd.b);
+  }
+  for (auto e : c->event_pool) cudaEventDestroy(e);
+  for (auto it = g_bank_owner.begin(); it != g_bank_owner.end();)
+    it = it->second == c ? g_bank_owner.erase(it) : std::next(it);
+  if (c->d_sc) cudaFree(c->d_sc);
+  if (c->h_sc) cudaFreeHost(c->h_sc);
+  if (c->d_red) cudaFree(c->d_red);
+  if (c->h_red) cudaFreeHost(c->h_red);
+  const bool own = c->own_stream;
+  cudaStream_t s = c->stream;
+  delete c;
+  if (own && s) cudaStreamDestroy(s);
+  return DGB_OK;
+}
+
+int dgb_set_stream(dgb_ctx* c, void* stream) {
+  return guarded([&] {
+    set_device(c);
+    sync(c);
+    if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+    if (stream) {
+      c->stream = static_cast<cudaStream_t>(stream);
+      c->own_stream = false;
+    } else {
+      CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      c->own_stream = true;
+    }
+    // constant banks are device state; nothing to re-upload
+    return DGB_OK;
+  });
+}
+
+int dgb_set_dirichlet(dgb_ctx* c, const double* states) {
+  return guarded([&] {
+    set_device(c);
+    if (!states) throw Fail{DGB_ERR_ARG, "null Dirichlet table"};
+    c->bc_dir.assign(states, states + 4 * static_cast<size_t>(c->n_bnd) * c->K);
+    c->d_bstate.upload(c->bc_dir.data(), c->bc_dir.size(), c->stream);
+    c->geo.bstate = c->d_bstate.p;
+    c->geo.has_dir = 1;
+    sync(c);
+    return DGB_OK;
+  });
+}
+
+int dgb_upload(dgb_ctx* c, int slot, const double* host) {
+  return guarded([&] {
+    set_device(c);
+    upload_dev(c, slot_ptr(c, slot), 4 * c->np, host);
+    sync(c);
+    return DGB_OK;
+  });
+}
+
+int dgb_download(dgb_ctx* c, int slot, double* host) {
+  return guarded([&] {
+    set_device(c);
+    download_dev(c, slot_ptr(c, slot), 4 * c->np, host);
+    return DGB_OK;
+  });
+}
+
+int dgb_copy_slot(dgb_ctx* c, int dst, int src) {
+  return guarded([&] {
+    set_device(c);
+    double* d = slot_ptr(c, dst);
+    const double* s = slot_ptr(c, src);
+    if (d != s) CU(cudaMemcpyAsync(d, s, c->coeff_count() * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    sync(c);
+    return DGB_OK;
+  });
+}
+
+int dgb_eval_volume_pass(dgb_ctx* c, int in_slot) {
+  return guarded([&] {
+    set_device(c);
+    run_pass(c, dgbk::kModeVolume, slot_ptr(c, in_slot), slot_ptr(c, DGB_SLOT_VOLUME), 0.0, 0);
+    return DGB_OK;
+  });
+}
+
+int dgb_eval_surface_pass(dgb_ctx* c, int in_slot, double t) {
+  return guarded([&] {
+    set_device(c);
+    check_bc(c);
+    if (!c->slots.p) {
+      c->slots.alloc(3 * c->coeff_count());
+      CU(cudaMemsetAsync(c->slots.p, 0, 3 * c->coeff_count() * sizeof(double), c->stream));
+    }
+    run_pass(c, dgbk::kModeSurface, slot_ptr(c, in_slot), c->slots.p, t, 1);
+    return DGB_OK;
+  });
+}
+
+int dgb_download_surface(dgb_ctx* c, double* left, double* right) {
+  return guarded([&] {
+    set_device(c);
+    const size_t per = static_cast<size_t>(4) * c->np * c->N;
+    std::vector<double> all(3 * per);
+    if (!c->slots.p) throw Fail{DGB_ERR_ARG, "no surface pass has been evaluated"};
+    download_dev(c, c->slots.p, 12 * c->np, all.data());
+    const int N = c->N, np = c->np;
+    std::memset(left, 0, sizeof(double) * 3 * per);
+    std::memset(right, 0, sizeof(double) * 3 * per);
+    for (int q = 0; q < 3; ++q)
+      for (int i = 0; i < N; ++i) {
+        const bool from_left = c->eleft[c->elem_edge[3 * i + q]] == i;
+        double* dst = from_left ? left : right;
+        for (int mm = 0; mm < 4; ++mm)
+          for (int j = 0; j < np; ++j) {
+            const size_t idx = ((static_cast<size_t>(q) * 4 + mm) * np + j) * N + i;
+            dst[idx] = all[idx];
+          }
+      }
+    return DGB_OK;
+  });
+}
+
+int dgb_upload_surface(dgb_ctx* c, const double* left, const double* right) {
+  return guarded([&] {
+    set_device(c);
+    const size_t per = static_cast<size_t>(4) * c->np * c->N;
+    std::vector<double> all(3 * per);
+    const int N = c->N, np = c->np;
+    for (int q = 0; q < 3; ++q)
+      for (int i = 0; i < N; ++i) {
+        const bool from_left = c->eleft[c->elem_edge[3 * i + q]] == i;
+        const double* src = from_left ? left : right;
+        for (int mm = 0; mm < 4; ++mm)
+          for (int j = 0; j < np; ++j) {
+            const size_t idx = ((static_cast<size_t>(q) * 4 + mm) * np + j) * N + i;
+            all[idx] = src[idx];
+          }
+      }
+    if (!c->slots.p) c->slots.alloc(3 * c->coeff_count());
+    upload_dev(c, c->slots.p, 12 * c->np, all.data());
+    sync(c);
+    return DGB_OK;
+  });
+}
+
+int dgb_eval_rhs_pass(dgb_ctx* c) {
+  return guarded([&] {
+    set_device(c);
+    if (!c->slots.p) throw Fail{DGB_ERR_ARG, "no surface pass has been evaluated"};
+    double* vol = slot_ptr(c, DGB_SLOT_VOLUME);
+    double* der = slot_ptr(c, DGB_SLOT_DERIV);
+    Timed tm(c, 2);
+    k_gather<<<small_grid(static_cast<long long>(4) * c->np * c->ld), 256, 0, c->stream>>>(
+        der, vol, c->slots.p, c->d_inv_det.p, c->N, c->ld, 4 * c->np);
+    CU(cudaGetLastError());
+    ++c->launches;
+    return DGB_OK;
+  });
+}
+
+int dgb_compute_rhs(dgb_ctx* c, int in_slot, double t, int out_slot) {
+  return guarded([&] {
+    set_device(c);
+    check_bc(c);
+    if (in_slot == out_slot) throw Fail{DGB_ERR_ARG, "compute_rhs needs distinct input and output slots"};
+    run_pass(c, dgbk::kModeRhs, slot_ptr(c, in_slot), slot_ptr(c, out_slot), t, 2);
+    return DGB_OK;
+  });
+}
+
+int dgb_limit(dgb_ctx* c, int slot) {
+  return guarded([&] {
+    set_device(c);
+    if (c->p != 1) throw Fail{DGB_ERR_ARG, "slope limiting is only supported for p = 1"};
+    ensure_tables(c);
+    reset_scalars(c, c->t);
+    LimArgs la{};
+    la.c = slot_ptr(c, slot);
+    la.u = la.c;
+    la.sc = c->d_sc;
+    {
+      Timed tm(c, 3);
+      CU(dgbk::launch_limit(0, c->geo, la, c->stream));
+      ++c->launches;
+    }
+    sync(c);
+    return DGB_OK;
+  });
+}
+
+int dgb_stable_dt(dgb_ctx* c, int slot, double cfl, double* dt) {
+  return guarded([&] {
+    set_device(c);
+    ensure_tables(c);
+    reset_scalars(c, c->t);
+    {
+      Timed tm(c, 4);
+      CU(launch_dt(c, slot_ptr(c, slot), 0, 0));
+      ++c->launches;
+    }
+    read_scalars(c);
+    if (c->h_sc->err_key != dgbk::kNoError)
+      throw Fail{DGB_ERR_INADMISSIBLE, failure_message(c, c->h_sc->err_key, slot_ptr(c, slot), c->t)};
+    *dt = cfl * __builtin_bit_cast(double, c->h_sc->dtmin[0]);
+    return DGB_OK;
+  });
+}
+
+int dgb_set_time(dgb_ctx* c, double t, int64_t step) {
+  c->t = t;
+  c->step_count = step;
+  return DGB_OK;
+}
+
+int dgb_get_time(dgb_ctx* c, double* t, int64_t* step) {
+  if (t) *t = c->t;
+  if (step) *step = c->step_count;
+  return DGB_OK;
+}
+
+int dgb_rk_step(dgb_ctx* c, int scheme, double dt, int limiting, double* residual) {
+  return guarded([&] {
+    set_device(c);
+    RunSpec r;
+    r.scheme = scheme;
+    r.dt_mode = 0;
+    r.dt_host = dt;
+    r.limiting = limiting != 0;
+    r.max_steps = 1;
+    RunOut o = run_steps(c, r);
+    if (residual) *residual = o.residual;
+    return DGB_OK;
+  });
+}
+
+int dgb_run_fixed_steps(dgb_ctx* c, int scheme, double cfl, int limiting, int64_t n, double* residual, double* hist) {
+  return guarded([&] {
+    set_device(c);
+    if (n <= 0) {
+      if (residual) *residual = 0.0;
+      return DGB_OK;
+    }
+    RunSpec r;
+    r.scheme = scheme;
+    r.dt_mode = 1;
+    r.cfl = cfl;
+    r.limiting = limiting != 0;
+    r.max_steps = n;
+    r.hist = hist;
+    r.hist_cap = hist ? n : 0;
+    RunOut o = run_steps(c, r);
+    if (residual) *residual = o.residual;
+    return DGB_OK;
+  });
+}
+
+int dgb_run_to_time(dgb_ctx* c, int scheme, double cfl, int limiting, double t_end, int64_t max_steps,
+                    double* residual, int64_t* steps_taken, double* hist, int64_t hist_cap) {
+  return guarded([&] {
+    set_device(c);
+    RunSpec r;
+    r.scheme = scheme;
+    r.dt_mode = 1;
+    r.cfl = cfl;
+    r.limiting = limiting != 0;
+    r.max_steps = max_steps;
+    r.clip = true;
+    r.stop_t = true;
+    r.t_end = t_end;
+    r.hist = hist;
+    r.hist_cap = hist ? hist_cap : 0;
+    if (!(c->t < t_end)) {
+      if (residual) *residual = 0.0;
+      if (steps_taken) *steps_taken = 0;
+      return DGB_OK;
+    }
+    RunOut o = max_steps > 0 ? run_steps(c, r) : RunOut{};
+    if (steps_taken) *steps_taken = o.steps;
+    if (residual) *residual = o.residual;
+    if (!o.halted && c->t < t_end)
+      throw Fail{DGB_ERR_NOT_REACHED, "t_end not reached within " + std::to_string(max_steps) + " steps"};
+    return DGB_OK;
+  });
+}
+
+int dgb_run_to_steady(dgb_ctx* c, int scheme, double cfl, int limiting, double tol, int64_t max_steps, int64_t* steps,
+                      double* residual, int* converged, double* hist, int64_t hist_cap) {
+  return guarded([&] {
+    set_device(c);
+    RunSpec r;
+    r.scheme = scheme;
+    r.dt_mode = 1;
+    r.cfl = cfl;
+    r.limiting = limiting != 0;
+    r.max_steps = max_steps;
+    r.stop_steady = true;
+    r.tol = tol;
+    r.hist = hist;
+    r.hist_cap = hist ? hist_cap : 0;
+    RunOut o = max_steps > 0 ? run_steps(c, r) : RunOut{};
+    if (steps) *steps = o.steps;
+    if (residual) *residual = o.residual;
+    if (converged) *converged = (o.steps > 0 && o.residual <= tol) ? 1 : 0;
+    return DGB_OK;
+  });
+}
+
+int dgb_total_mass(dgb_ctx* c, int slot, double* mass) {
+  return guarded([&] {
+    set_device(c);
+    std::vector<double> row(c->N);
+    download_dev(c, slot_ptr(c, slot), 1, row.data());
+    const double inv_sqrt2 = 1.0 / std::sqrt(2.0);
+    double s = 0.0;
+    for (int i = 0; i < c->N; ++i) s += c->det[i] * row[i] * inv_sqrt2;
+    *mass = s;
+    return DGB_OK;
+  });
+}
+
+int dgb_max_abs_diff(dgb_ctx* c, int sa, int sb, double* diff) {
+  return guarded([&] {
+    set_device(c);
+    const double* a = slot_ptr(c, sa);
+    const double* b = slot_ptr(c, sb);
+    CU(cudaMemsetAsync(c->d_red, 0, sizeof(unsigned long long), c->stream));
+    k_max_abs_diff<<<small_grid(static_cast<long long>(4) * c->np * c->ld), 256, 0, c->stream>>>(
+        a, b, c->N, c->ld, 4 * c->np, c->d_red);
+    CU(cudaGetLastError());
+    ++c->launches;
+    CU(cudaMemcpyAsync(c->h_red, c->d_red, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    *diff = __builtin_bit_cast(double, *c->h_red);
+    return DGB_OK;
+  });
+}
+
+int dgb_timers(dgb_ctx* c, dgb_pass_timers* out) {
+  return guarded([&] {
+    set_device(c);
+    sync(c);
+    *out = c->timers;
+    return DGB_OK;
+  });
+}
+
+int dgb_reset_timers(dgb_ctx* c) {
+  return guarded([&] {
+    set_device(c);
+    sync(c);
+    c->timers = dgb_pass_timers{};
+    c->stage_ms = 0.0;
+    c->stage_launches = 0;
+    return DGB_OK;
+  });
+}
+
+int dgb_enable_timers(dgb_ctx* c, int enable) {
+  c->timing = enable != 0;
+  return DGB_OK;
+}
+
+int dgb_last_abort(dgb_ctx* c, dgb_abort_info* out) {
+  *out = c->last_abort;
+  return DGB_OK;
+}
+
+int64_t dgb_launch_count(dgb_ctx* c) { return c->launches; }
+
+int dgb_stage_kernel_ms(dgb_ctx* c, double* ms, int64_t* launches) {
+  return guarded([&] {
+    set_device(c);
+    sync(c);
+    if (ms) *ms = c->stage_ms;
+    if (launches) *launches = c->stage_launches;
+    return DGB_OK;
+  });
+}
+
+}  // extern "C"
