@@ -1,0 +1,377 @@
+#!/usr/bin/env python
+"""Benchmark: FP64 DOF-updates/s per RK stage of the B200 modal-DG Euler path.
+
+Workload (BASELINE.json configs[1], at the >=1M-triangle size the metric names):
+periodic isentropic vortex on a 708x708 box split into 1,002,528 triangles,
+orders p = 1..5 swept, SSP-RK3 (3 stages per step), CFL 0.3, random-free
+synthetic initial data.  A bench "step" is one full RK time step at every
+order of the sweep; `value` = sum over orders of 4*Np*N*stages*K / sum of the
+device time of the timed regions (CUDA events on the solver stream).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Multi-GPU (torchrun): every rank runs its own copy of the workload (weak
+scaling; the halo-exchange partition is not wired into the benchmark yet) and
+the max over ranks of the device time is used.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+SCHEMES = {"ssp3": (103, 3), "ssp2": (102, 2), "rk2": (2, 2), "rk4": (4, 4)}
+NQ = {1: 3, 2: 6, 3: 12, 4: 16, 5: 25}
+METRIC = "FP64 DOF-updates/sec per RK stage (Euler, p=1-5)"
+
+
+def np_(p):
+    return (p + 1) * (p + 2) // 2
+
+
+def alg_bytes(p, e):
+    """bytes per element per stage (read stage, read u^n, write; geometry)."""
+    return 24 * 4 * np_(p) + 40 + 34 * e
+
+
+def alg_flops(p, e):
+    """minimal FLOPs per element per stage (FMA = 2)."""
+    n = np_(p)
+    return NQ[p] * (24 * n + 52) + e * (p + 1) * (32 * n + 115) + 24 * n
+
+
+def measured_peaks():
+    path = os.path.join(HERE, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured copy)"
+    except Exception:
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi-equivalent clock / throttle sampling during the timed region (pynvml)."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, index=0, period=0.1):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.period, self._stop, self._t = period, threading.Event(), None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons)}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def dist_setup(n_gpus):
+    rank, world, local = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), \
+        int(os.environ.get("LOCAL_RANK", 0))
+    pg = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        pg = dist
+    return rank, world, local, pg
+
+
+def max_over_ranks(x, pg, local):
+    if pg is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+    pg.all_reduce(t, op=pg.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(pg):
+    if pg is not None:
+        pg.barrier()
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_b200(args, rank, world, local, pg):
+    import torch
+    from paper_1601_07944_b200 import _lib as L
+    from paper_1601_07944_b200 import dg2d
+
+    torch.cuda.set_device(local)
+    scheme, stages = SCHEMES[args.scheme]
+    orders = [int(x) for x in args.orders.split(",")]
+    n = args.n
+    mesh = dg2d.generate_mesh(L.MESH_PERIODIC_BOX, n, n, 10.0, 10.0)
+    N = mesh.n_elements()
+    e_ratio = mesh.n_edges() / N
+    iv = dg2d.IsentropicVortex()
+    hbm_gbs, hbm_src = measured_peaks()
+    fp64 = C.c_double()
+    dg2d._check(L.lib.dgb_fp64_peak(local, C.byref(fp64)))
+    fp64_tf = fp64.value
+
+    per_order, tot_dof_upd, tot_ms, tot_launch = [], 0.0, 0.0, 0
+    e2e_dof, e2e_ms, h2d, d2h = 0.0, 0.0, 0, 0
+    stream = torch.cuda.Stream(device=local)
+    sampler = ClockSampler(local)
+    with sampler:
+        for p in orders:
+            tb = dg2d.build_tables(p)
+            c0 = dg2d.project_initial(lambda xy: iv(xy), mesh, tb)
+            ctx = dg2d.SolverContext(mesh, tb, options=dg2d.SolverOptions(scheme=scheme, cfl=args.cfl), device=local)
+            h = ctx.handle
+            dg2d._check(L.lib.dgb_set_stream(h, C.c_void_p(stream.cuda_stream)))
+            L.lib.dgb_enable_timers(h, 1)
+            ctx.upload(L.SLOT_STATE, c0)
+            res = C.c_double()
+            dg2d._check(L.lib.dgb_run_fixed_steps(h, scheme, args.cfl, 0, args.warmup, C.byref(res), None))
+            L.lib.dgb_reset_timers(h)
+            l0 = L.lib.dgb_launch_count(h)
+            barrier(pg)
+            torch.cuda.synchronize()
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record(stream)
+            dg2d._check(L.lib.dgb_run_fixed_steps(h, scheme, args.cfl, 0, args.steps, C.byref(res), None))
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            barrier(pg)
+            ms = ev0.elapsed_time(ev1)
+            ms = max_over_ranks(ms, pg, local)
+            launches = L.lib.dgb_launch_count(h) - l0
+            kms, kn = C.c_double(), C.c_int64()
+            L.lib.dgb_stage_kernel_ms(h, C.byref(kms), C.byref(kn))
+            k_avg = kms.value / max(kn.value, 1)
+            dof = 4 * np_(p) * N
+            upd = dof * stages * args.steps * world
+            b, f = alg_bytes(p, e_ratio) * N, alg_flops(p, e_ratio) * N
+            ach_bw, ach_fl = b / (k_avg * 1e-3) / 1e9, f / (k_avg * 1e-3) / 1e12
+            bound = "hbm" if b / (hbm_gbs * 1e9) >= f / (fp64_tf * 1e12) else "fp64"
+            roof = {"bound": bound,
+                    "achieved": ach_bw if bound == "hbm" else ach_fl,
+                    "peak": hbm_gbs if bound == "hbm" else fp64_tf,
+                    "unit": "GB/s" if bound == "hbm" else "TFLOP/s",
+                    "traffic": None}
+            roof["frac"] = roof["achieved"] / roof["peak"]
+            roof["kernel_ms"] = k_avg
+            roof["alg_bytes_per_launch"] = b
+            roof["alg_flops_per_launch"] = f
+            per_order.append({"p": p, "value": upd / (ms * 1e-3), "ms_per_step": ms / args.steps,
+                              "stage_kernel_ms": k_avg, "kernel_share": kms.value / ms if ms else None,
+                              "dof": dof, "roofline": roof, "launches_per_step": launches / args.steps})
+            tot_dof_upd += upd
+            tot_ms += ms
+            tot_launch += launches
+
+            # end to end through the public C ABI with host buffers: per step the
+            # state goes host->device (pinned), one RK step runs, and the new
+            # state comes back device->host.
+            if args.e2e_steps > 0:
+                pin = torch.empty(c0.size, dtype=torch.float64, pin_memory=True)
+                hbuf = pin.numpy().reshape(c0.shape)
+                hbuf[...] = c0
+                hp = hbuf.ctypes.data_as(L.c_double_p)
+                for _ in range(2):  # warm-up
+                    dg2d._check(L.lib.dgb_upload(h, L.SLOT_STATE, hp))
+                    dg2d._check(L.lib.dgb_run_fixed_steps(h, scheme, args.cfl, 0, 1, C.byref(res), None))
+                    dg2d._check(L.lib.dgb_download(h, L.SLOT_STATE, hp))
+                barrier(pg)
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                ev0.record(stream)
+                for _ in range(args.e2e_steps):
+                    dg2d._check(L.lib.dgb_upload(h, L.SLOT_STATE, hp))
+                    dg2d._check(L.lib.dgb_run_fixed_steps(h, scheme, args.cfl, 0, 1, C.byref(res), None))
+                    dg2d._check(L.lib.dgb_download(h, L.SLOT_STATE, hp))
+                ev1.record(stream)
+                torch.cuda.synchronize()
+                wall = (time.perf_counter() - t0) * 1e3
+                ms_e = max_over_ranks(max(ev0.elapsed_time(ev1), wall), pg, local)
+                e2e_dof += dof * stages * args.e2e_steps * world
+                e2e_ms += ms_e
+                h2d += c0.nbytes
+                d2h += c0.nbytes
+                per_order[-1]["e2e_value"] = dof * stages * args.e2e_steps * world / (ms_e * 1e-3)
+            ctx.close()
+
+    dom = max(per_order, key=lambda r: r["stage_kernel_ms"] * stages)
+    line = {
+        "metric": METRIC, "value": tot_dof_upd / (tot_ms * 1e-3), "unit": "DOF-updates/s/stage",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": tot_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: periodic isentropic vortex initial data (projected), no dataset",
+        "config": {"workload": f"isentropic vortex, periodic {n}x{n} box ({N} triangles), "
+                               f"p={','.join(map(str, orders))} sweep, {args.scheme.upper()}, cfl {args.cfl}",
+                   "triangles_per_gpu": N, "edges_per_gpu": mesh.n_edges(), "orders": orders,
+                   "scheme": args.scheme, "stages_per_step": stages,
+                   "l2": "inputs larger than L2 (>=288 MB of coefficients per stage)",
+                   "parallelism": f"replica x{world}" if world > 1 else "single GPU"},
+        "roofline": dict(dom["roofline"], p=dom["p"],
+                         note=f"dominant kernel = fused stage kernel at p={dom['p']}; "
+                              f"HBM peak {hbm_src}; FP64 peak measured in-run (DFMA loop) {fp64_tf:.1f} TF/s"),
+        "per_order": per_order,
+        "gpu_launches": tot_launch,
+        "clocks": sampler.summary(),
+        "fp64_peak_tflops_measured": fp64_tf,
+    }
+    if e2e_ms > 0:
+        line["e2e"] = {"value": e2e_dof / (e2e_ms * 1e-3), "unit": "DOF-updates/s/stage",
+                       "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                       "note": "per step: pinned host state -> dgb_upload -> one RK step -> dgb_download"}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(mesh, orders, args)
+    return line
+
+
+# ----------------------------------------------------------------------------- CPU reference
+def cpu_sample(mesh, orders, sample_n, steps=2):
+    """Time the reference solver's run_fixed_steps (RK2, its own driver with its
+    workspace reused across the steps of a call, all host threads) for `steps`
+    steps per order on the same mesh; returns DOF-updates/s/stage."""
+    from oracle import bind
+    from paper_1601_07944_b200 import _lib as L
+    from paper_1601_07944_b200 import dg2d
+    if mesh is None or mesh.n_elements() != 2 * sample_n * sample_n:
+        mesh = dg2d.generate_mesh(L.MESH_PERIODIC_BOX, sample_n, sample_n, 10.0, 10.0)
+    N = mesh.n_elements()
+    iv = dg2d.IsentropicVortex()
+    kind = "reference" if bind.ref_available() else "port"
+    upd, secs = 0.0, 0.0
+    if kind == "reference":
+        rm = bind.RefMesh.from_mesh(mesh)
+        cores = bind.ref_lib().ref_num_threads()
+    else:
+        cores = 1
+    for p in orders:
+        tb = dg2d.build_tables(p)
+        c0 = dg2d.project_initial(lambda xy: iv(xy), mesh, tb)
+        if kind == "reference":
+            rt = bind.RefTables(p)
+            rs = bind.RefSolver(rm, rt, rk_order=2, cfl=0.3)
+            t0 = time.perf_counter()
+            rs.run_fixed_steps(c0, 0.0, steps)
+            dt = time.perf_counter() - t0
+        else:
+            orc = bind.Oracle(mesh, tb)
+            t0 = time.perf_counter()
+            orc.run_fixed_steps(c0, 0.0, steps, 2, 0.3)
+            dt = time.perf_counter() - t0
+        upd += 4 * np_(p) * N * 2 * steps
+        secs += dt
+    return {"value": upd / secs, "unit": "DOF-updates/s/stage", "cores": cores, "kind": kind,
+            "seconds": secs,
+            "sample": f"{steps} RK2 (midpoint) steps per order p={','.join(map(str, orders))} on the "
+                      f"periodic {int(round(math.sqrt(N / 2)))}^2 box ({N} triangles), "
+                      f"reference run_fixed_steps with OpenMP over {cores} threads"}
+
+
+def cpu_baseline(mesh, orders, args):
+    try:
+        return cpu_sample(mesh if args.cpu_n == args.n else None, orders, args.cpu_n)
+    except Exception as e:  # the CPU leg must never break the GPU number
+        return {"value": None, "unit": "DOF-updates/s/stage", "cores": None, "kind": None,
+                "sample": f"failed: {e}"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    orders = [int(x) for x in args.orders.split(",")]
+    for _ in range(args.warmup):
+        cpu_sample(None, orders, args.cpu_n)
+    t_tot, upd_tot, info = 0.0, 0.0, None
+    for _ in range(args.steps):
+        info = cpu_sample(None, orders, args.cpu_n)
+        t_tot += info["seconds"]
+        upd_tot += info["value"] * info["seconds"]
+    value = upd_tot / t_tot
+    N = 2 * args.cpu_n * args.cpu_n
+    return {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "DOF-updates/s/stage",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t_tot / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic: periodic isentropic vortex initial data",
+        "config": {"workload": f"isentropic vortex, periodic {args.cpu_n}x{args.cpu_n} box ({N} triangles), "
+                               f"p={args.orders} sweep; reference RK2 (SSP-RK3 is not in the reference; "
+                               "per-stage cost is the same RHS + stage combination)",
+                   "orders": orders},
+        "cpu_baseline": {"value": value, "unit": "DOF-updates/s/stage", "cores": info["cores"],
+                         "kind": info["kind"], "sample": info["sample"]},
+        "e2e": {"value": value, "unit": "DOF-updates/s/stage", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--n", type=int, default=708, help="box cells per side (2 n^2 triangles)")
+    ap.add_argument("--orders", default="1,2,3,4,5")
+    ap.add_argument("--scheme", default="ssp3", choices=list(SCHEMES))
+    ap.add_argument("--cfl", type=float, default=0.3)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-n", type=int, default=708, help="box size of the CPU sample")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    rank, world, local, pg = dist_setup(args.gpus)
+    if args.impl == "reference":
+        line = run_reference(args, rank, world)
+    else:
+        line = run_b200(args, rank, world, local, pg)
+    if rank == 0 and line is not None:
+        print(json.dumps(line), flush=True)
+    if pg is not None:
+        pg.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -194,6 +194,10 @@ int64_t dgb_launch_count(dgb_ctx* ctx);
  * stage kernels since the last reset (CUDA events on the context stream). */
 int dgb_stage_kernel_ms(dgb_ctx* ctx, double* ms, int64_t* launches);
 
+/* Measured FP64 FMA-pipe throughput of `device` (DFMA loop on every SM), TFLOP/s;
+ * the FP64 roofline denominator (MEASURED_PEAKS.json has no FP64 entry). */
+int dgb_fp64_peak(int device, double* tflops);
+
 /* ---------------------------------------------------------------- host setup (runs once) */
 /* Our own builders, bit-compatible with the reference's (not the hot path). */
 typedef struct dgb_mesh dgb_mesh;

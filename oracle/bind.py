@@ -61,6 +61,14 @@ def oracle_lib():
             f.restype = C.c_int
         lib.or_gather.argtypes = [P, dp, dp, dp, dp]
         lib.or_gather.restype = None
+        lib.or_pressure.argtypes = [dp, C.c_double]
+        lib.or_pressure.restype = C.c_double
+        lib.or_euler_flux.argtypes = [dp, C.c_double, dp, dp]
+        lib.or_euler_flux.restype = None
+        lib.or_llf.argtypes = [dp, dp, C.c_double, C.c_double, C.c_double, dp]
+        lib.or_llf.restype = None
+        lib.or_wave_speed.argtypes = [dp, C.c_double, C.c_double, C.c_double]
+        lib.or_wave_speed.restype = C.c_double
         _olib = lib
     return _olib
 

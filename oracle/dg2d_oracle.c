@@ -491,3 +491,11 @@ int or_run_fixed_steps(const or_problem* P, double* c, double* t, int64_t n, int
   }
   return 0;
 }
+
+/* KAT hooks for tests/test_oracle.py: the physics primitives on their own. */
+double or_pressure(const double* u, double gamma) { return pressure(u, gamma); }
+void or_euler_flux(const double* u, double gamma, double* f1, double* f2) { euler_flux(u, gamma, f1, f2); }
+void or_llf(const double* ul, const double* ur, double nx, double ny, double gamma, double* f) {
+  llf(ul, ur, nx, ny, gamma, f);
+}
+double or_wave_speed(const double* u, double nx, double ny, double gamma) { return wave_speed(u, nx, ny, gamma); }

@@ -51,6 +51,12 @@ int or_step(const or_problem* P, double* c, double* t, double dt, int scheme, in
 int or_run_fixed_steps(const or_problem* P, double* c, double* t, int64_t n, int scheme, double cfl, int limiting,
                        double* resid, double* hist, or_fail* f);
 
+/* physics primitives (KAT hooks) */
+double or_pressure(const double* u, double gamma);
+void or_euler_flux(const double* u, double gamma, double* f1, double* f2);
+void or_llf(const double* ul, const double* ur, double nx, double ny, double gamma, double* f);
+double or_wave_speed(const double* u, double nx, double ny, double gamma);
+
 #ifdef __cplusplus
 }
 #endif

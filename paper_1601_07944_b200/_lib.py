@@ -112,6 +112,7 @@ _sig("dgb_enable_timers", C.c_int, _vp, C.c_int)
 _sig("dgb_last_abort", C.c_int, _vp, C.POINTER(AbortInfo))
 _sig("dgb_launch_count", C.c_int64, _vp)
 _sig("dgb_stage_kernel_ms", C.c_int, _vp, c_double_p, c_int64_p)
+_sig("dgb_fp64_peak", C.c_int, C.c_int, c_double_p)
 _sig("dgb_mesh_from_msh", C.c_int, C.c_char_p, C.c_size_t, C.POINTER(_vp))
 _sig("dgb_mesh_generate", C.c_int, C.c_int, C.c_int, C.c_int, c_double_p, C.c_int, C.POINTER(_vp))
 _sig("dgb_mesh_generate_text", C.c_int, C.c_int, C.c_int, C.c_int, c_double_p, C.c_int,

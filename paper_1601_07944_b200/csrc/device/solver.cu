@@ -111,6 +111,22 @@ __global__ void k_max_abs_diff(const double* __restrict__ a, const double* __res
   if ((threadIdx.x & 31) == 0) atomicMax(out, static_cast<unsigned long long>(__double_as_longlong(m)));
 }
 
+// FP64 FMA-pipe peak probe: 8 independent DFMA chains per thread, all SMs.
+__global__ void k_fp64_peak(double* out, int iters) {
+  double a[8];
+  const double m = 1.0000001, c = 1e-9;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = threadIdx.x * 1e-3 + k;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = fma(a[k], m, c);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += a[k];
+  if (s == 12345.678) out[0] = s;  // keep the chains alive
+}
+
 int small_grid(long long work) {
   long long g = (work + 255) / 256;
   if (g > 148 * 16) g = 148 * 16;
@@ -1286,6 +1302,36 @@ int dgb_last_abort(dgb_ctx* c, dgb_abort_info* out) {
 }
 
 int64_t dgb_launch_count(dgb_ctx* c) { return c->launches; }
+
+int dgb_fp64_peak(int device, double* tflops) {
+  return guarded([&] {
+    CU(cudaSetDevice(device));
+    int sms = 0;
+    CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    double* d = nullptr;
+    CU(cudaMalloc(&d, sizeof(double)));
+    cudaEvent_t a, b;
+    CU(cudaEventCreate(&a));
+    CU(cudaEventCreate(&b));
+    const int blocks = sms * 8, threads = 256, iters = 4096;
+    k_fp64_peak<<<blocks, threads>>>(d, 64);  // warm up
+    float best = 1e30f;
+    for (int r = 0; r < 5; ++r) {
+      CU(cudaEventRecord(a));
+      k_fp64_peak<<<blocks, threads>>>(d, iters);
+      CU(cudaEventRecord(b));
+      CU(cudaEventSynchronize(b));
+      float ms = 0.f;
+      CU(cudaEventElapsedTime(&ms, a, b));
+      best = std::min(best, ms);
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(d);
+    *tflops = 2.0 * 8.0 * iters * static_cast<double>(blocks) * threads / (best * 1e-3) / 1e12;
+    return DGB_OK;
+  });
+}
 
 int dgb_stage_kernel_ms(dgb_ctx* c, double* ms, int64_t* launches) {
   return guarded([&] {

@@ -1,0 +1,308 @@
+"""GPU parity: the sm_100a kernels through the C ABI against the CPU oracle and
+the real reference (oracle/_ref travels to the GPU box as a built library).
+
+Tolerances (BASELINE.json north star):
+  * per RHS:  ||d_gpu - d_ref||_inf,m / ||(|vol| + sum_q |slot_q|)/detJ||_inf,m <= 1e-12
+  * per run:  ||c_gpu - c_ref||_inf,m / ||c_ref||_inf,m <= 1e-9
+"""
+import math
+import os
+import tempfile
+
+import numpy as np
+import pytest
+
+from oracle import bind
+from paper_1601_07944_b200 import _lib as L
+from paper_1601_07944_b200 import dg2d
+
+from helpers import cases, owned_left, rel_per_eq, smooth_field, term_rel, term_scale
+
+pytestmark = pytest.mark.gpu
+
+RHS_TOL = 1e-12
+RUN_TOL = 1e-9
+CASES = cases()
+
+
+def build(case, p, options=None):
+    name, kind, nx, ny, prm, bcf, u0 = case
+    mesh = dg2d.generate_mesh(kind, nx, ny, *prm)
+    tb = dg2d.build_tables(p)
+    bc = bcf()
+    c = dg2d.project_initial(u0, mesh, tb)
+    ctx = dg2d.SolverContext(mesh, tb, bc=bc, options=options or dg2d.SolverOptions())
+    return mesh, tb, bc, c, ctx, bind.Oracle(mesh, tb, bc)
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("ci", range(len(CASES)), ids=[c[0] for c in CASES])
+def test_passes_match_oracle(ci, p):
+    mesh, tb, bc, c, ctx, orc = build(CASES[ci], p)
+    t = 0.05
+    vol = orc.volume(c)
+    sl, sr = orc.surface(c, t)
+    scale = term_scale(vol, sl, sr, mesh.det_jac)
+    assert rel_per_eq(dg2d.eval_volume_pass(ctx, c), vol) <= RHS_TOL
+    bufs = dg2d.eval_surface_pass(ctx, c, t)
+    own = owned_left(mesh)
+    for q in range(3):
+        for m in range(4):
+            a = np.where(own[q], bufs.surface_left[q, m] - sl[q, m], bufs.surface_right[q, m] - sr[q, m])
+            assert np.max(np.abs(a)) <= RHS_TOL * max(float(np.max(scale[m] * mesh.det_jac)), 1e-300)
+    deriv = orc.rhs(c, t)
+    assert term_rel(dg2d.compute_rhs(ctx, c, t), deriv, scale) <= RHS_TOL
+    bufs.volume[...] = dg2d.eval_volume_pass(ctx, c)
+    assert term_rel(dg2d.eval_rhs_pass(ctx, bufs), deriv, scale) <= RHS_TOL
+    ctx.close()
+
+
+@pytest.mark.skipif(not bind.ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("p", [1, 3, 5])
+def test_rhs_matches_live_reference_same_inputs(p):
+    """The reference's own mesh arrays and tables feed the GPU; its compute_rhs is the oracle."""
+    rm = bind.RefMesh.generate(L.MESH_VORTEX, 1, 0, 1.0, 1.384)
+    rt = bind.RefTables(p)
+    rbc = bind.RefBC()
+    bind.ref_lib().ref_bc_set_vortex(rbc.h, 1.0, 1.384, 2.25, 1.0, 1.0, 1.4)
+    rs = bind.RefSolver(rm, rt, rbc)
+    c = bind.ref_project(rm, rt, 2, (1.0, 1.384, 2.25, 1.0, 1.0))
+    mesh, tb = dg2d.ArrayMesh(rm.export(), rm.nb), rt.as_external()
+    ctx = dg2d.SolverContext(mesh, tb, bc=dg2d.vortex_boundary())
+    vol = rs.volume(c)
+    sl, sr = rs.surface(c, 0.0)
+    scale = term_scale(vol, sl, sr, mesh.det_jac)
+    assert term_rel(dg2d.compute_rhs(ctx, c, 0.0), rs.rhs(c, 0.0), scale) <= RHS_TOL
+    assert abs(dg2d.stable_dt(ctx, c) - rs.stable_dt(c)) <= 1e-14 * rs.stable_dt(c)
+    ctx.close()
+
+
+@pytest.mark.parametrize("scheme", [2, 4, 102, 103])
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5])
+def test_single_step_matches_oracle(scheme, p):
+    mesh, tb, bc, c, ctx, orc = build(CASES[0], p, dg2d.SolverOptions(scheme=scheme))
+    dt = dg2d.stable_dt(ctx, c)
+    assert abs(dt - orc.stable_dt(c, 0.3)) <= 1e-14 * dt
+    st = dg2d.SolverState(c.copy(), 0.25, 7)
+    res = dg2d.rk_step(ctx, st, dt)
+    co, to, ro = orc.step(c, 0.25, dt, scheme)
+    assert rel_per_eq(st.coeffs, co) <= RHS_TOL
+    assert st.t == to and st.step_count == 8
+    assert abs(res - ro) <= 1e-9 * ro
+    ctx.close()
+
+
+@pytest.mark.parametrize("p,scheme,steps", [(1, 2, 100), (2, 4, 50), (3, 103, 40), (5, 102, 20)])
+def test_run_fixed_steps_matches_oracle(p, scheme, steps):
+    mesh, tb, bc, c, ctx, orc = build(CASES[4], p, dg2d.SolverOptions(scheme=scheme))
+    st = dg2d.SolverState(c.copy())
+    hist = []
+    dg2d.run_fixed_steps(ctx, st, steps, lambda s, r: hist.append(r))
+    co, to, ro, ho = orc.run_fixed_steps(c, 0.0, steps, scheme, 0.3)
+    assert rel_per_eq(st.coeffs, co) <= RUN_TOL
+    assert abs(st.t - to) <= 1e-13 * to and st.step_count == steps
+    assert len(hist) == steps and np.allclose(hist, ho, rtol=1e-6, atol=1e-14)
+    ctx.close()
+
+
+@pytest.mark.parametrize("p", [1, 2, 4])
+def test_vortex_run_matches_reference(p):
+    """Curved walls, Dirichlet inflow, outflow: 60 RK4 steps vs the reference's run_fixed_steps."""
+    if not bind.ref_available():
+        pytest.skip("oracle/_ref not built")
+    rm = bind.RefMesh.generate(L.MESH_VORTEX, 1, 0, 1.0, 1.384)
+    rt = bind.RefTables(p)
+    rbc = bind.RefBC()
+    bind.ref_lib().ref_bc_set_vortex(rbc.h, 1.0, 1.384, 2.25, 1.0, 1.0, 1.4)
+    rs = bind.RefSolver(rm, rt, rbc, rk_order=4, cfl=0.9)
+    c = bind.ref_project(rm, rt, 2, (1.0, 1.384, 2.25, 1.0, 1.0))
+    cr, tr, rr, hr = rs.run_fixed_steps(c, 0.0, 60)
+    mesh, tb = dg2d.ArrayMesh(rm.export(), rm.nb), rt.as_external()
+    ctx = dg2d.SolverContext(mesh, tb, bc=dg2d.vortex_boundary(), options=dg2d.SolverOptions(rk_order=4, cfl=0.9))
+    st = dg2d.SolverState(c.copy())
+    res = dg2d.run_fixed_steps(ctx, st, 60)
+    assert rel_per_eq(st.coeffs, cr) <= RUN_TOL
+    assert abs(st.t - tr) <= 1e-12 * tr
+    assert abs(res - rr) <= 1e-6 * rr
+    ctx.close()
+
+
+def test_double_mach_with_limiter_matches_reference():
+    """C4 path at desk size: DMR 200x50, p=1, limiter, RK2, 100 steps vs the reference."""
+    if not bind.ref_available():
+        pytest.skip("oracle/_ref not built")
+    rm = bind.RefMesh.generate(L.MESH_DOUBLE_MACH, 200, 50, 1.0 / 6.0)
+    rt = bind.RefTables(1)
+    rbc = bind.RefBC()
+    bind.ref_lib().ref_bc_set_double_mach(rbc.h, 1.0 / 6.0, 10.0, 60.0, 1.4)
+    rs = bind.RefSolver(rm, rt, rbc, rk_order=2, cfl=0.3, limiting=True)
+    c = rs.limit(bind.ref_project(rm, rt, 3, (1.0 / 6.0, 10.0, 60.0)))
+    cr, tr, rr, _ = rs.run_fixed_steps(c, 0.0, 100)
+    mesh, tb = dg2d.ArrayMesh(rm.export(), rm.nb), rt.as_external()
+    bc = dg2d.double_mach_boundary(dg2d.DoubleMachSetup())
+    ctx = dg2d.SolverContext(mesh, tb, bc=bc, options=dg2d.SolverOptions(rk_order=2, cfl=0.3, limiting=True))
+    st = dg2d.SolverState(c.copy())
+    dg2d.run_fixed_steps(ctx, st, 100)
+    assert rel_per_eq(st.coeffs, cr) <= RUN_TOL
+    assert abs(st.t - tr) <= 1e-12 * tr
+    ctx.close()
+
+
+def test_run_to_time_and_steady_drivers():
+    mesh, tb, bc, c, ctx, orc = build(CASES[2], 2, dg2d.SolverOptions(rk_order=4, cfl=0.9))
+    st = dg2d.SolverState(c.copy())
+    dg2d.run_to_time(ctx, st, 0.01, 10000)
+    assert st.t == 0.01
+    if bind.ref_available():
+        rm = bind.RefMesh.generate(L.MESH_VORTEX, 0, 0, 1.0, 1.384)
+        rt = bind.RefTables(2)
+        rbc = bind.RefBC()
+        bind.ref_lib().ref_bc_set_vortex(rbc.h, 1.0, 1.384, 2.25, 1.0, 1.0, 1.4)
+        rs = bind.RefSolver(rm, rt, rbc, rk_order=4, cfl=0.9)
+        cr, tr, steps_r, _ = rs.run_to_time(c, 0.0, 0.01, 10000)
+        assert st.step_count == steps_r
+        assert rel_per_eq(st.coeffs, cr) <= RUN_TOL
+    with pytest.raises(dg2d.SolverAbort, match="t_end not reached within 3 steps"):
+        dg2d.run_to_time(ctx, dg2d.SolverState(c.copy()), 1.0, 3)
+    # steady driver terminates quickly on already-steady data (test_solver.cpp:493-502)
+    m2 = dg2d.generate_mesh(L.MESH_BOX, 3, 3, 1.0, 1.0, 4)
+    t1 = dg2d.build_tables(1)
+    u = dg2d.make_state(1.0, 0.4, 0.1, 1.0)
+    c2 = dg2d.project_initial(lambda xy: np.tile(u, (len(xy), 1)), m2, t1)
+    ctx2 = dg2d.SolverContext(m2, t1)
+    r = dg2d.run_to_steady(ctx2, dg2d.SolverState(c2), 1e-12, 1000)
+    assert r.converged and r.steps <= 2
+    ctx.close()
+    ctx2.close()
+
+
+def test_limiter_matches_oracle_bitwise_on_shocked_data():
+    m = dg2d.generate_mesh(L.MESH_BOX, 16, 4, 1.0, 0.25, 1)
+    t = dg2d.build_tables(1)
+    sod = lambda xy: np.where((xy[:, 0] < 0.5)[:, None], dg2d.make_state(1, 0, 0, 1)[None],
+                              dg2d.make_state(0.125, 0, 0, 0.1)[None])
+    c = dg2d.project_initial(sod, m, t)
+    ctx = dg2d.SolverContext(m, t)
+    lg = dg2d.limit(ctx, c.copy())
+    lo = bind.Oracle(m, t).limit(c)
+    assert np.max(np.abs(lg - lo)) <= 1e-15 * np.max(np.abs(lo))
+    assert np.array_equal(lg[:, 0], c[:, 0])  # means bit-identical (test_limiter.cpp:146-158)
+    with pytest.raises(ValueError, match="only supported for p = 1"):
+        dg2d.limit(dg2d.SolverContext(m, dg2d.build_tables(2)), np.zeros((4, 6, m.n_elements())))
+    ctx.close()
+
+
+def test_free_stream_preservation():  # test_solver.cpp:231-266, acceptance.cpp:148-209
+    u = dg2d.make_state(1.2, 0.8, -0.5, 1.5)
+    rest = dg2d.make_state(1.2, 0.0, 0.0, 1.5)
+    for p in range(1, 6):
+        m = dg2d.generate_mesh(L.MESH_BOX, 3, 2, 2.0, 1.0, 4)
+        t = dg2d.build_tables(p)
+        c = dg2d.project_initial(lambda xy: np.tile(u, (len(xy), 1)), m, t)
+        assert np.max(np.abs(dg2d.compute_rhs(dg2d.SolverContext(m, t), c, 0.0))) < 1e-11
+        mv = dg2d.generate_mesh(L.MESH_VORTEX, 0, 0, 1.0, 1.384)
+        bc = dg2d.BoundaryConditions(dirichlet=lambda xy, tt: np.tile(rest, (len(xy), 1)),
+                                     wall_normal=lambda xy: xy / np.hypot(xy[:, 0], xy[:, 1])[:, None])
+        c = dg2d.project_initial(lambda xy: np.tile(rest, (len(xy), 1)), mv, t)
+        assert np.max(np.abs(dg2d.compute_rhs(dg2d.SolverContext(mv, t, bc=bc), c, 0.0))) < 1e-11
+
+
+@pytest.mark.parametrize("limiting", [False, True])
+def test_conservation_closed_reflecting_box(limiting):  # acceptance.cpp:240-266
+    m = dg2d.generate_mesh(L.MESH_BOX, 6, 6, 1.0, 1.0, 1)
+    t = dg2d.build_tables(1)
+
+    def bump(xy):
+        r2 = (xy[:, 0] - 0.5) ** 2 + (xy[:, 1] - 0.5) ** 2
+        return np.stack([dg2d.make_state(1 + 0.3 * math.exp(-30 * a), 0, 0, 1 + 0.2 * math.exp(-30 * a)) for a in r2])
+    c = dg2d.project_initial(bump, m, t)
+    ctx = dg2d.SolverContext(m, t, options=dg2d.SolverOptions(rk_order=4, limiting=limiting))
+    if limiting:
+        c = dg2d.limit(ctx, c)
+    mass0 = dg2d.total_mass(m, c)
+    st = dg2d.SolverState(c)
+    dg2d.run_fixed_steps(ctx, st, 1000)
+    assert abs(dg2d.total_mass(m, st.coeffs) - mass0) / abs(mass0) < 1e-10
+    ctx.close()
+
+
+def test_determinism_and_bitwise_checkpoint_restart():  # test_solver.cpp:424-461
+    mesh, tb, bc, c, ctx, orc = build(CASES[2], 2, dg2d.SolverOptions(rk_order=4))
+    a, b = dg2d.SolverState(c.copy()), dg2d.SolverState(c.copy())
+    dg2d.run_fixed_steps(ctx, a, 10)
+    dg2d.run_fixed_steps(ctx, b, 10)
+    assert np.array_equal(a.coeffs, b.coeffs)
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "ck.bin")
+        dg2d.save_checkpoint(a, path)
+        ld = dg2d.load_checkpoint(path)
+        assert ld.t == a.t and ld.step_count == a.step_count and np.array_equal(ld.coeffs, a.coeffs)
+        dg2d.run_fixed_steps(ctx, ld, 5)
+        dg2d.run_fixed_steps(ctx, a, 5)
+        assert np.array_equal(ld.coeffs, a.coeffs)
+    ctx.close()
+
+
+def test_abort_diagnostics_match_reference_semantics():  # test_solver.cpp:413-422
+    m = dg2d.build_connectivity(dg2d.parse_msh(dg2d.two_triangle_square(1)))
+    t = dg2d.build_tables(1)
+    c = np.zeros((4, 3, 2))
+    c[0, 0, :] = -1.0
+    ctx = dg2d.SolverContext(m, t)
+    with pytest.raises(dg2d.SolverAbort, match=r"eval_volume: inadmissible state at id 0, point 0 \(rho=-1\.414214"):
+        dg2d.eval_volume_pass(ctx, c)
+    # a failing step leaves the state untouched and the step counter unchanged
+    good = dg2d.project_initial(smooth_field(3, 0.3), m, t)
+    st = dg2d.SolverState(good.copy(), 0.0, 0)
+    with pytest.raises(dg2d.SolverAbort, match="inadmissible"):
+        dg2d.rk_step(ctx, st, 50.0)
+    assert np.array_equal(st.coeffs, good) and st.step_count == 0 and st.t == 0.0
+    with pytest.raises(ValueError, match="rk_order must be 2 or 4"):
+        ctx.options.rk_order = 3
+        dg2d.rk_step(ctx, st, 1e-3)
+    ctx.close()
+
+
+def test_custom_rhs_operator_seam():  # test_solver.cpp:351-385
+    m = dg2d.build_connectivity(dg2d.parse_msh(dg2d.two_triangle_square(4)))
+    t = dg2d.build_tables(1)
+    for order in (2, 4):
+        ctx = dg2d.SolverContext(m, t, options=dg2d.SolverOptions(rk_order=order))
+        st = dg2d.SolverState(np.arange(24, dtype=float).reshape(4, 3, 2) * 0.01, 0.3)
+        init = st.coeffs.copy()
+        op = lambda cc, tt: 1.0 + 0.1 * np.arange(24).reshape(4, 3, 2)
+        dg2d.rk_step(ctx, st, 0.25, op, False)
+        assert np.allclose(st.coeffs, init + 0.25 * (1.0 + 0.1 * np.arange(24).reshape(4, 3, 2)), rtol=1e-13)
+        st = dg2d.SolverState(np.zeros((4, 3, 2)), 0.3)
+        dg2d.rk_step(ctx, st, 0.5, lambda cc, tt: np.full((4, 3, 2), 2.0 * tt), False)
+        assert np.allclose(st.coeffs, 0.8 ** 2 - 0.3 ** 2, rtol=1e-13)
+
+
+# ----------------------------------------------------------------------------- full-size properties
+@pytest.mark.parametrize("p", [1, 3])
+def test_full_size_free_stream_conservation_determinism(p):
+    """At the benchmark size (708^2 periodic box, 1,002,528 triangles): uniform flow
+    is a fixed point, mass is conserved over SSP-RK3 steps, runs are bitwise
+    reproducible, and one RHS matches the CPU oracle."""
+    m = dg2d.generate_mesh(L.MESH_PERIODIC_BOX, 708, 708, 10.0, 10.0)
+    t = dg2d.build_tables(p)
+    u = dg2d.make_state(1.0, 0.7, -0.3, 1.2)
+    c = dg2d.project_initial(lambda xy: np.tile(u, (len(xy), 1)), m, t)
+    ctx = dg2d.SolverContext(m, t, options=dg2d.SolverOptions(scheme=103))
+    st = dg2d.SolverState(c.copy())
+    dg2d.run_fixed_steps(ctx, st, 5)
+    assert np.max(np.abs(st.coeffs - c)) < 1e-12
+    iv = dg2d.IsentropicVortex()
+    c = dg2d.project_initial(lambda xy: iv(xy), m, t)
+    mass0 = dg2d.total_mass(m, c)
+    a, b = dg2d.SolverState(c.copy()), dg2d.SolverState(c.copy())
+    dg2d.run_fixed_steps(ctx, a, 5)
+    dg2d.run_fixed_steps(ctx, b, 5)
+    assert np.array_equal(a.coeffs, b.coeffs)
+    assert abs(dg2d.total_mass(m, a.coeffs) - mass0) <= 1e-13 * abs(mass0)
+    if p == 1:
+        orc = bind.Oracle(m, t)
+        vol = orc.volume(c)
+        sl, sr = orc.surface(c)
+        assert term_rel(dg2d.compute_rhs(ctx, c, 0.0), orc.rhs(c), term_scale(vol, sl, sr, m.det_jac)) <= RHS_TOL
+    ctx.close()
