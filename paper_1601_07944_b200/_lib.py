@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdg2d_b200.so")
+LIB_PATH = os.environ.get("DGB_LIB") or os.path.join(_HERE, "libdg2d_b200.so")  # DGB_LIB: tuning builds
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

@@ -73,20 +73,22 @@ __device__ __forceinline__ void euler_flux(const double (&U)[4], const Prim& w, 
   f2[3] = w.vy * ep;
 }
 
-// Local Lax-Friedrichs flux, normal from left to right (euler.hpp:59-71).
-__device__ __forceinline__ void llf_flux(const double (&UL)[4], const double (&UR)[4], double nx, double ny,
-                                         double gamma, double (&fn)[4]) {
-  const double g1 = gamma - 1.0;
-  const Prim wl = primitives(UL, g1), wr = primitives(UR, g1);
-  double f1l[4], f2l[4], f1r[4], f2r[4];
-  euler_flux(UL, wl, f1l, f2l);
-  euler_flux(UR, wr, f1r, f2r);
+// Local Lax-Friedrichs flux, normal from left to right (euler.hpp:59-71), on
+// precomputed primitives; evaluated variable by variable to keep few values live.
+__device__ __forceinline__ void llf_flux(const double (&UL)[4], const Prim& wl, const double (&UR)[4], const Prim& wr,
+                                         double nx, double ny, double gamma, double (&fn)[4]) {
   const double sl = fabs(wl.vx * nx + wl.vy * ny) + sqrt(gamma * wl.p * wl.inv);
   const double sr = fabs(wr.vx * nx + wr.vy * ny) + sqrt(gamma * wr.p * wr.inv);
-  const double s = fmax(sl, sr);
+  const double hs = 0.5 * fmax(sl, sr);
+  const double epl = UL[3] + wl.p, epr = UR[3] + wr.p;
+  // F1 = (mx, mx vx + p, my vx, vx (E+p)), F2 = (my, mx vy, my vy + p, vy (E+p))
+  const double f1l[4] = {UL[1], fma(UL[1], wl.vx, wl.p), UL[2] * wl.vx, wl.vx * epl};
+  const double f1r[4] = {UR[1], fma(UR[1], wr.vx, wr.p), UR[2] * wr.vx, wr.vx * epr};
+  const double f2l[4] = {UL[2], UL[1] * wl.vy, fma(UL[2], wl.vy, wl.p), wl.vy * epl};
+  const double f2r[4] = {UR[2], UR[1] * wr.vy, fma(UR[2], wr.vy, wr.p), wr.vy * epr};
 #pragma unroll
   for (int m = 0; m < 4; ++m)
-    fn[m] = 0.5 * (nx * (f1l[m] + f1r[m]) + ny * (f2l[m] + f2r[m])) - 0.5 * s * (UR[m] - UL[m]);
+    fn[m] = 0.5 * (nx * (f1l[m] + f1r[m]) + ny * (f2l[m] + f2r[m])) - hs * (UR[m] - UL[m]);
 }
 
 __device__ __forceinline__ void reflect(const double (&u)[4], double nx, double ny, double (&g)[4]) {
@@ -191,16 +193,76 @@ __device__ __forceinline__ void neighbour_trace(const Tab<P>& T, const double* _
   }
 }
 
-// The fused element kernel.  MODE selects what is written:
+// 4x4 transpose across the 4 lanes of an element group: on entry lane g holds
+// v[i] = (variable g) at point i; on exit lane g holds v[m] = (variable m) at
+// point g.  Two butterfly rounds, 4 double shuffles.
+__device__ __forceinline__ void transpose4(double (&v)[4], int g) {
+  const bool b1 = g & 2, b0 = g & 1;
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const double send = b1 ? v[i] : v[i + 2];
+    const double r = __shfl_xor_sync(kFull, send, 2);
+    if (b1) v[i] = r; else v[i + 2] = r;
+  }
+#pragma unroll
+  for (int i = 0; i < 4; i += 2) {
+    const double send = b0 ? v[i] : v[i + 1];
+    const double r = __shfl_xor_sync(kFull, send, 1);
+    if (b0) v[i] = r; else v[i + 1] = r;
+  }
+}
+
+template <int K>
+__device__ __forceinline__ double pick_weight(const double (&we)[K], int k) {
+  double r = we[0];
+#pragma unroll
+  for (int i = 1; i < K; ++i) r = (k == i) ? we[i] : r;
+  return r;
+}
+
+// Minimum registers per launch for the fused kernel (occupancy target per degree).
+#ifndef DGB_MINB
+#define DGB_MINB(P) ((P) == 1 ? 5 : (P) == 2 ? 3 : (P) == 3 ? 5 : (P) == 4 ? 4 : 3)
+#endif
+#ifndef DGB_G1_MAXP
+#define DGB_G1_MAXP 2
+#endif
+// Degrees up to DGB_G1_MAXP use one thread per element, higher ones four lanes.
+template <int P>
+struct Lanes {
+  static constexpr int value = P <= DGB_G1_MAXP ? 1 : 4;
+};
+
+#ifndef DGB_SIDE_UNROLL
+#define DGB_SIDE_UNROLL 1
+#endif
+constexpr int kSideUnroll = DGB_SIDE_UNROLL;  // 1: sides processed in a runtime loop
+#ifndef DGB_VOL_UNROLL
+#define DGB_VOL_UNROLL 1
+#endif
+constexpr int kVolUnroll = DGB_VOL_UNROLL;  // 1: volume point groups in a runtime loop
+
+template <int P>
+struct MinBlocks {
+  static constexpr int value = DGB_MINB(P);
+};
+
+// The fused element kernel.  Four lanes per element, lane g owns conserved
+// variable g (its n_p coefficients and accumulators).  Contractions are DFMA
+// chains with constant-bank table operands (all lanes of a warp use the same
+// table entry); every nonlinear pointwise evaluation (volume flux, numerical
+// flux, wave speed) is done ONCE per point: the four lanes transpose four
+// points' states, each lane evaluates one point, and the results are
+// transposed back.  MODE selects what is written:
 //   kModeVolume  -> volume integral only (eval_volume_pass)
 //   kModeSurface -> per-side surface integrals into the slot buffer (eval_surface_pass)
 //   kModeRhs     -> (volume + surface) / det (compute_rhs)
 //   kModeStage   -> RK stage update with the fused epilogues
-template <int P, int G, int MODE>
+template <int P, int MODE>
 __device__ __forceinline__ void element_body(const Tab<P>& T, const Geo& geo, const StageArgs& a) {
-  constexpr int NP = Dim<P>::NP, NQ = Dim<P>::NQ, K = Dim<P>::K, MG = 4 / G;
+  constexpr int NP = Dim<P>::NP, NQ = Dim<P>::NQ, K = Dim<P>::K;
   const long long ld = geo.ld;
-  const int gsize = geo.ld * G;
+  const int gsize = geo.ld * 4;
   const int stride = gridDim.x * blockDim.x;
   const double gamma = geo.gamma, g1 = gamma - 1.0;
   Scalars* sc = a.sc;
@@ -252,57 +314,61 @@ __device__ __forceinline__ void element_body(const Tab<P>& T, const Geo& geo, co
   double res_max = 0.0;
 
   for (int tid = blockIdx.x * blockDim.x + threadIdx.x; tid < gsize; tid += stride) {
-    const int lane_g = (G == 1) ? 0 : (tid % G);
-    const int m0 = lane_g * MG;
-    int e = tid / G;
+    const int g = tid & 3;  // conserved variable owned by this lane
+    int e = tid >> 2;
     const bool valid = e < geo.N;
     if (!valid) e = geo.N - 1;
+    const long long row = static_cast<long long>(g) * NP * ld + e;  // (g, j=0, e)
 
-    double c[MG][NP];
+    double c[NP];
 #pragma unroll
-    for (int mm = 0; mm < MG; ++mm)
+    for (int j = 0; j < NP; ++j) c[j] = __ldg(a.in + row + j * ld);
+    double acc[NP];
 #pragma unroll
-      for (int j = 0; j < NP; ++j) c[mm][j] = __ldg(a.in + (static_cast<long long>(m0 + mm) * NP + j) * ld + e);
-
-    double acc[MG][NP];
-#pragma unroll
-    for (int mm = 0; mm < MG; ++mm)
-#pragma unroll
-      for (int j = 0; j < NP; ++j) acc[mm][j] = 0.0;
+    for (int j = 0; j < NP; ++j) acc[j] = 0.0;
 
     // ------------------------------------------------------------ volume
     if constexpr (MODE != kModeSurface) {
       const double ta = __ldg(geo.tau + e), tb = __ldg(geo.tau + ld + e);
       const double tc = __ldg(geo.tau + 2 * ld + e), td = __ldg(geo.tau + 3 * ld + e);
+#pragma unroll kVolUnroll
+      for (int k0 = 0; k0 < NQ; k0 += 4) {
+        const int nk = (NQ - k0) < 4 ? (NQ - k0) : 4;
+        double v[4];
 #pragma unroll
-      for (int k = 0; k < NQ; ++k) {
-        double u[MG];
+        for (int i = 0; i < 4; ++i) {
+          if (i < nk) {
+            double s = T.phi[k0 + i][0] * c[0];
 #pragma unroll
-        for (int mm = 0; mm < MG; ++mm) {
-          double s = T.phi[k][0] * c[mm][0];
-#pragma unroll
-          for (int j = 1; j < NP; ++j) s = fma(T.phi[k][j], c[mm][j], s);
-          u[mm] = s;
+            for (int j = 1; j < NP; ++j) s = fma(T.phi[k0 + i][j], c[j], s);
+            v[i] = s;
+          } else {
+            v[i] = v[0];  // padding lane: duplicate of a real point
+          }
         }
-        double U[4];
-        gather_state<G, MG>(u, U);
-        Prim w = primitives(U, g1);
-        if (!admissible(U, w)) {
-          if (valid && lane_g == 0) record_error(sc, err_key(a.seq, kPassVolume, __ldg(geo.ref_id + e), k));
-          U[0] = 1.0; U[1] = 0.0; U[2] = 0.0; U[3] = 2.5;  // placeholder (solver.cpp:129-132)
+        transpose4(v, g);  // lane g: full state at point k0 + g
+        Prim w = primitives(v, g1);
+        if (!admissible(v, w)) {
+          if (valid && g < nk) record_error(sc, err_key(a.seq, kPassVolume, __ldg(geo.ref_id + e), k0 + g));
+          v[0] = 1.0; v[1] = 0.0; v[2] = 0.0; v[3] = 2.5;  // placeholder (solver.cpp:129-132)
           w.inv = 1.0; w.vx = 0.0; w.vy = 0.0; w.p = 1.0;
         }
         double f1[4], f2[4];
-        euler_flux(U, w, f1, f2);
+        euler_flux(v, w, f1, f2);
+        double fr[4], fs[4];
 #pragma unroll
-        for (int mm = 0; mm < MG; ++mm) {
-          const int m = m0 + mm;
-          const double F1 = (G == 1) ? f1[mm] : pick4(f1, m);
-          const double F2 = (G == 1) ? f2[mm] : pick4(f2, m);
-          const double fr = ta * F1 + tb * F2;  // contravariant flux along r
-          const double fs = tc * F1 + td * F2;  // along s
+        for (int m = 0; m < 4; ++m) {
+          fr[m] = ta * f1[m] + tb * f2[m];  // contravariant flux along r
+          fs[m] = tc * f1[m] + td * f2[m];  // along s
+        }
+        transpose4(fr, g);  // lane g: variable g at points k0..k0+3
+        transpose4(fs, g);
 #pragma unroll
-          for (int j = 0; j < NP; ++j) acc[mm][j] = fma(T.drw[k][j], fr, fma(T.dsw[k][j], fs, acc[mm][j]));
+        for (int i = 0; i < 4; ++i) {
+          if (i < nk) {
+#pragma unroll
+            for (int j = 0; j < NP; ++j) acc[j] = fma(T.drw[k0 + i][j], fr[i], fma(T.dsw[k0 + i][j], fs[i], acc[j]));
+          }
         }
       }
     }
@@ -311,7 +377,7 @@ __device__ __forceinline__ void element_body(const Tab<P>& T, const Geo& geo, co
     double snx[3], sny[3];
     if constexpr (MODE != kModeVolume) {
       const int inf = __ldg(geo.info + e);
-#pragma unroll
+#pragma unroll kSideUnroll
       for (int q = 0; q < 3; ++q) {
         const int nb = __ldg(geo.nbr + q * ld + e);
         const int ed = __ldg(geo.eid + q * ld + e);
@@ -322,72 +388,69 @@ __device__ __forceinline__ void element_body(const Tab<P>& T, const Geo& geo, co
         sny[q] = ny;
         const bool bnd = nb < 0;
 
-        double un[K][MG];
+        double un[K][1];
         if (!bnd) {
           switch (snb) {
-            case 1: neighbour_trace<P, 0, MG>(T, a.in, ld, m0, nb, un); break;
-            case 2: neighbour_trace<P, 1, MG>(T, a.in, ld, m0, nb, un); break;
-            default: neighbour_trace<P, 2, MG>(T, a.in, ld, m0, nb, un); break;
+            case 1: neighbour_trace<P, 0, 1>(T, a.in, ld, g, nb, un); break;
+            case 2: neighbour_trace<P, 1, 1>(T, a.in, ld, g, nb, un); break;
+            default: neighbour_trace<P, 2, 1>(T, a.in, ld, g, nb, un); break;
           }
         } else {
 #pragma unroll
-          for (int ko = 0; ko < K; ++ko)
+          for (int ko = 0; ko < K; ++ko) un[ko][0] = 0.0;
+        }
+        double uo[K];
 #pragma unroll
-            for (int mm = 0; mm < MG; ++mm) un[ko][mm] = 0.0;
+        for (int ko = 0; ko < K; ++ko) {
+          double s = T.phe[q][ko][0] * c[0];
+#pragma unroll
+          for (int j = 1; j < NP; ++j) s = fma(T.phe[q][ko][j], c[j], s);
+          uo[ko] = s;
         }
         if constexpr (MODE == kModeSurface) {
 #pragma unroll
-          for (int mm = 0; mm < MG; ++mm)
-#pragma unroll
-            for (int j = 0; j < NP; ++j) acc[mm][j] = 0.0;
+          for (int j = 0; j < NP; ++j) acc[j] = 0.0;
         }
 #pragma unroll
-        for (int ko = 0; ko < K; ++ko) {
-          double uo[MG];
-#pragma unroll
-          for (int mm = 0; mm < MG; ++mm) {
-            double s = T.phe[q][ko][0] * c[mm][0];
-#pragma unroll
-            for (int j = 1; j < NP; ++j) s = fma(T.phe[q][ko][j], c[mm][j], s);
-            uo[mm] = s;
-          }
-          double Uo[4], Un[4];
-          gather_state<G, MG>(uo, Uo);
-          gather_state<G, MG>(un[ko], Un);
+        for (int k0 = 0; k0 < K; k0 += 4) {
+          const int nk = (K - k0) < 4 ? (K - k0) : 4;
           double UL[4], UR[4];
 #pragma unroll
-          for (int m = 0; m < 4; ++m) {
-            UL[m] = left ? Uo[m] : Un[m];
-            UR[m] = left ? Un[m] : Uo[m];
+          for (int i = 0; i < 4; ++i) {
+            const int ko = (i < nk) ? k0 + i : k0;
+            UL[i] = left ? uo[ko] : un[ko][0];
+            UR[i] = left ? un[ko][0] : uo[ko];
           }
-          const int kc = left ? ko : K - 1 - ko;
+          transpose4(UL, g);  // lane g: full traces at own point k0 + g
+          transpose4(UR, g);
+          const int ko = (g < nk) ? k0 + g : k0;
+          const int kc = left ? ko : K - 1 - ko;  // canonical (left-element) point index
           if (bnd) ghost_state<K>(UL, nb, ed, kc, nx, ny, tstage, geo, UR);
           const Prim wl = primitives(UL, g1), wr = primitives(UR, g1);
-          const bool okl = admissible(UL, wl), okr = admissible(UR, wr);
           double fn[4];
-          if (okl && okr) {
-            llf_flux(UL, UR, nx, ny, gamma, fn);
+          if (admissible(UL, wl) && admissible(UR, wr)) {
+            llf_flux(UL, wl, UR, wr, nx, ny, gamma, fn);
           } else {
-            if (valid && lane_g == 0) record_error(sc, err_key(a.seq, kPassSurface, ed, kc));
+            if (valid && g < nk) record_error(sc, err_key(a.seq, kPassSurface, ed, kc));
 #pragma unroll
             for (int m = 0; m < 4; ++m) fn[m] = 0.0;
           }
-          const double wl_ = h * (left ? T.we[ko] : T.we[K - 1 - ko]);
+          const double wl_ = h * pick_weight<K>(T.we, kc);
 #pragma unroll
-          for (int mm = 0; mm < MG; ++mm) {
-            const double f = (G == 1) ? fn[mm] : pick4(fn, m0 + mm);
-            const double cf = left ? -(wl_ * f) : (wl_ * f);
+          for (int m = 0; m < 4; ++m) fn[m] = left ? -(wl_ * fn[m]) : (wl_ * fn[m]);
+          transpose4(fn, g);  // lane g: weighted flux of variable g at points k0..k0+3
 #pragma unroll
-            for (int j = 0; j < NP; ++j) acc[mm][j] = fma(cf, T.phe[q][ko][j], acc[mm][j]);
+          for (int i = 0; i < 4; ++i) {
+            if (i < nk) {
+#pragma unroll
+              for (int j = 0; j < NP; ++j) acc[j] = fma(fn[i], T.phe[q][k0 + i][j], acc[j]);
+            }
           }
         }
         if constexpr (MODE == kModeSurface) {
           if (valid) {
 #pragma unroll
-            for (int mm = 0; mm < MG; ++mm)
-#pragma unroll
-              for (int j = 0; j < NP; ++j)
-                a.out[((static_cast<long long>(q) * 4 + m0 + mm) * NP + j) * ld + e] = acc[mm][j];
+            for (int j = 0; j < NP; ++j) a.out[(static_cast<long long>(q) * 4 * NP + g * NP + j) * ld + e] = acc[j];
           }
         }
       }
@@ -397,18 +460,13 @@ __device__ __forceinline__ void element_body(const Tab<P>& T, const Geo& geo, co
     if constexpr (MODE == kModeVolume) {
       if (valid) {
 #pragma unroll
-        for (int mm = 0; mm < MG; ++mm)
-#pragma unroll
-          for (int j = 0; j < NP; ++j) a.out[(static_cast<long long>(m0 + mm) * NP + j) * ld + e] = acc[mm][j];
+        for (int j = 0; j < NP; ++j) a.out[row + j * ld] = acc[j];
       }
     } else if constexpr (MODE == kModeRhs) {
       const double idet = __ldg(geo.inv_det + e);
       if (valid) {
 #pragma unroll
-        for (int mm = 0; mm < MG; ++mm)
-#pragma unroll
-          for (int j = 0; j < NP; ++j)
-            a.out[(static_cast<long long>(m0 + mm) * NP + j) * ld + e] = acc[mm][j] * idet;
+        for (int j = 0; j < NP; ++j) a.out[row + j * ld] = acc[j] * idet;
       }
     } else if constexpr (MODE == kModeStage) {
       const double idet = __ldg(geo.inv_det + e);
@@ -416,50 +474,299 @@ __device__ __forceinline__ void element_body(const Tab<P>& T, const Geo& geo, co
       const double dt6 = dt / 6.0;
       const bool need_u = a.alpha != 0.0 || a.want_resid || a.kmode == 3;
 #pragma unroll
-      for (int mm = 0; mm < MG; ++mm) {
+      for (int j = 0; j < NP; ++j) {
+        const long long idx = row + j * ld;
+        const double d = acc[j] * idet;
+        const double uu = need_u ? __ldg(a.u + idx) : 0.0;
+        double o;
+        if (a.kmode == 3) {
+          o = fma(dt6, __ldg(a.kacc + idx) + d, uu);
+        } else {
+          const double base = (a.alpha != 0.0) ? fma(a.alpha, uu, a.beta * c[j]) : a.beta * c[j];
+          o = fma(gdt, d, base);
+          if (a.kmode == 1 && valid) a.kacc[idx] = d;
+          if (a.kmode == 2 && valid) a.kacc[idx] = fma(2.0, d, a.kacc[idx]);
+        }
+        if (valid) {
+          a.out[idx] = o;
+          if (a.want_resid) res_max = fmax(res_max, fabs(uu - o));
+        }
+        acc[j] = o;  // keep the new stage for the CFL epilogue
+      }
+      if (a.want_lambda) {
+        double v[4];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          double s = T.phm[q][0] * acc[0];
+#pragma unroll
+          for (int j = 1; j < NP; ++j) s = fma(T.phm[q][j], acc[j], s);
+          v[q] = s;
+        }
+        v[3] = v[0];
+        transpose4(v, g);  // lane q < 3: state at the midpoint of side q
+        const Prim w = primitives(v, g1);
+        const double nxq = g == 0 ? snx[0] : (g == 1 ? snx[1] : snx[2]);
+        const double nyq = g == 0 ? sny[0] : (g == 1 ? sny[1] : sny[2]);
+        double lam = 0.0;
+        if (admissible(v, w)) {
+          lam = fabs(w.vx * nxq + w.vy * nyq) + sqrt(gamma * w.p * w.inv);
+        } else if (valid && g < 3) {
+          record_error(sc, err_key(a.seq_next, kPassDt, __ldg(geo.ref_id + e), g + 1));
+        }
+        if (g == 3) lam = 0.0;
+        lam = fmax(lam, __shfl_xor_sync(kFull, lam, 1));
+        lam = fmax(lam, __shfl_xor_sync(kFull, lam, 2));
+        if (valid && g == 0) lam_min = fmin(lam_min, 2.0 * __ldg(geo.inradius + e) / ((2.0 * P + 1.0) * lam));
+      }
+    }
+  }
+
+  if constexpr (MODE == kModeStage) {
+    const int par = a.step & 1;
+    if (a.want_lambda) block_reduce_atomic<true>(lam_min, &sc->dtmin[par ^ 1]);
+    if (a.want_resid) block_reduce_atomic<false>(res_max, &sc->resid[par]);
+  }
+}
+
+
+// One thread per element (all four variables): the low-degree variant.  At
+// p <= 2 the per-point work (reciprocals, square roots, shuffles) dominates the
+// contractions, so spreading an element over lanes multiplies it; a thread per
+// element evaluates every pointwise quantity exactly once with no exchange.
+template <int P, int MODE>
+__device__ __forceinline__ void element_body_g1(const Tab<P>& T, const Geo& geo, const StageArgs& a) {
+  constexpr int NP = Dim<P>::NP, NQ = Dim<P>::NQ, K = Dim<P>::K;
+  const long long ld = geo.ld;
+  const int stride = gridDim.x * blockDim.x;
+  const double gamma = geo.gamma, g1 = gamma - 1.0;
+  Scalars* sc = a.sc;
+
+  __shared__ int s_stop;
+  if (threadIdx.x == 0) s_stop = (sc->err_key != kNoError || sc->halt) ? 1 : 0;
+  __syncthreads();
+  if (s_stop) return;
+
+  double t0 = a.t_host, dt = 0.0;
+  if constexpr (MODE == kModeStage) {
+    const int par = a.step & 1;
+    t0 = sc->t[par];
+    if (a.first) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (a.hist && a.step > 0) a.hist[a.step - 1] = bits_to_double(sc->resid[par ^ 1]);
+      }
+      bool stop = false;
+      if (a.stop_at_t_end && !(t0 < a.t_end)) stop = true;
+      if (a.stop_steady && a.step > 0 && bits_to_double(sc->resid[par ^ 1]) <= a.tol) stop = true;
+      if (stop) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+          sc->halt = 1;
+          sc->halt_step = a.step;
+        }
+        return;
+      }
+    }
+    if (a.dt_mode == 0) {
+      dt = a.dt_host;
+    } else {
+      dt = a.cfl * bits_to_double(sc->dtmin[par]);
+      if (a.clip_t_end && t0 + dt > a.t_end) dt = a.t_end - t0;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      if (a.first) {
+        sc->dtmin[par ^ 1] = 0x7ff0000000000000ull;
+        sc->resid[par] = 0ull;
+        sc->dt_used[par] = dt;
+      }
+      if (a.last) sc->t[par ^ 1] = t0 + dt;
+    }
+  }
+  const double tstage = (MODE == kModeStage) ? fma(a.tcoef, dt, t0) : t0;
+
+  double lam_min = __longlong_as_double(0x7ff0000000000000ll);
+  double res_max = 0.0;
+
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < geo.ld; e += stride) {
+    const bool valid = e < geo.N;
+    if (!valid) continue;
+
+    double c[4][NP];
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+#pragma unroll
+      for (int j = 0; j < NP; ++j) c[m][j] = __ldg(a.in + (static_cast<long long>(m) * NP + j) * ld + e);
+    double acc[4][NP];
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+#pragma unroll
+      for (int j = 0; j < NP; ++j) acc[m][j] = 0.0;
+
+    // ------------------------------------------------------------ volume
+    if constexpr (MODE != kModeSurface) {
+      const double ta = __ldg(geo.tau + e), tb = __ldg(geo.tau + ld + e);
+      const double tc = __ldg(geo.tau + 2 * ld + e), td = __ldg(geo.tau + 3 * ld + e);
+#pragma unroll
+      for (int k = 0; k < NQ; ++k) {
+        double U[4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          double s = T.phi[k][0] * c[m][0];
+#pragma unroll
+          for (int j = 1; j < NP; ++j) s = fma(T.phi[k][j], c[m][j], s);
+          U[m] = s;
+        }
+        Prim w = primitives(U, g1);
+        if (!admissible(U, w)) {
+          record_error(sc, err_key(a.seq, kPassVolume, __ldg(geo.ref_id + e), k));
+          U[0] = 1.0; U[1] = 0.0; U[2] = 0.0; U[3] = 2.5;  // placeholder (solver.cpp:129-132)
+          w.inv = 1.0; w.vx = 0.0; w.vy = 0.0; w.p = 1.0;
+        }
+        double f1[4], f2[4];
+        euler_flux(U, w, f1, f2);
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          const double fr = ta * f1[m] + tb * f2[m];
+          const double fs = tc * f1[m] + td * f2[m];
+#pragma unroll
+          for (int j = 0; j < NP; ++j) acc[m][j] = fma(T.drw[k][j], fr, fma(T.dsw[k][j], fs, acc[m][j]));
+        }
+      }
+    }
+
+    // ------------------------------------------------------------ surface
+    if constexpr (MODE != kModeVolume) {
+      const int inf = __ldg(geo.info + e);
+#pragma unroll 1
+      for (int q = 0; q < 3; ++q) {
+        const int nb = __ldg(geo.nbr + q * ld + e);
+        const int ed = __ldg(geo.eid + q * ld + e);
+        const int snb = (inf >> (2 * q)) & 3;
+        const bool left = (inf >> (6 + q)) & 1;
+        const double nx = __ldg(geo.enx + ed), ny = __ldg(geo.eny + ed), h = __ldg(geo.eh + ed);
+        const bool bnd = nb < 0;
+        double un[K][4];
+        if (!bnd) {
+          switch (snb) {
+            case 1: neighbour_trace<P, 0, 4>(T, a.in, ld, 0, nb, un); break;
+            case 2: neighbour_trace<P, 1, 4>(T, a.in, ld, 0, nb, un); break;
+            default: neighbour_trace<P, 2, 4>(T, a.in, ld, 0, nb, un); break;
+          }
+        } else {
+#pragma unroll
+          for (int ko = 0; ko < K; ++ko)
+#pragma unroll
+            for (int m = 0; m < 4; ++m) un[ko][m] = 0.0;
+        }
+        if constexpr (MODE == kModeSurface) {
+#pragma unroll
+          for (int m = 0; m < 4; ++m)
+#pragma unroll
+            for (int j = 0; j < NP; ++j) acc[m][j] = 0.0;
+        }
+        const double* __restrict__ phq = &T.phe[q][0][0];  // own side, uniform runtime offset
+#pragma unroll
+        for (int ko = 0; ko < K; ++ko) {
+          double uo[4];
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            double s = phq[ko * NP] * c[m][0];
+#pragma unroll
+            for (int j = 1; j < NP; ++j) s = fma(phq[ko * NP + j], c[m][j], s);
+            uo[m] = s;
+          }
+          double UL[4], UR[4];
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            UL[m] = left ? uo[m] : un[ko][m];
+            UR[m] = left ? un[ko][m] : uo[m];
+          }
+          const int kc = left ? ko : K - 1 - ko;
+          if (bnd) ghost_state<K>(UL, nb, ed, kc, nx, ny, tstage, geo, UR);
+          const Prim wl = primitives(UL, g1), wr = primitives(UR, g1);
+          double fn[4];
+          if (admissible(UL, wl) && admissible(UR, wr)) {
+            llf_flux(UL, wl, UR, wr, nx, ny, gamma, fn);
+          } else {
+            record_error(sc, err_key(a.seq, kPassSurface, ed, kc));
+#pragma unroll
+            for (int m = 0; m < 4; ++m) fn[m] = 0.0;
+          }
+          const double wl_ = h * pick_weight<K>(T.we, kc);
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            const double cf = left ? -(wl_ * fn[m]) : (wl_ * fn[m]);
+#pragma unroll
+            for (int j = 0; j < NP; ++j) acc[m][j] = fma(cf, phq[ko * NP + j], acc[m][j]);
+          }
+        }
+        if constexpr (MODE == kModeSurface) {
+#pragma unroll
+          for (int m = 0; m < 4; ++m)
+#pragma unroll
+            for (int j = 0; j < NP; ++j)
+              a.out[((static_cast<long long>(q) * 4 + m) * NP + j) * ld + e] = acc[m][j];
+        }
+      }
+    }
+
+    // ------------------------------------------------------------ outputs
+    if constexpr (MODE == kModeVolume) {
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int j = 0; j < NP; ++j) a.out[(static_cast<long long>(m) * NP + j) * ld + e] = acc[m][j];
+    } else if constexpr (MODE == kModeRhs) {
+      const double idet = __ldg(geo.inv_det + e);
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int j = 0; j < NP; ++j) a.out[(static_cast<long long>(m) * NP + j) * ld + e] = acc[m][j] * idet;
+    } else if constexpr (MODE == kModeStage) {
+      const double idet = __ldg(geo.inv_det + e);
+      const double gdt = a.gcoef * dt;
+      const double dt6 = dt / 6.0;
+      const bool need_u = a.alpha != 0.0 || a.want_resid || a.kmode == 3;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
 #pragma unroll
         for (int j = 0; j < NP; ++j) {
-          const long long idx = (static_cast<long long>(m0 + mm) * NP + j) * ld + e;
-          const double d = acc[mm][j] * idet;
+          const long long idx = (static_cast<long long>(m) * NP + j) * ld + e;
+          const double d = acc[m][j] * idet;
           const double uu = need_u ? __ldg(a.u + idx) : 0.0;
           double o;
           if (a.kmode == 3) {
             o = fma(dt6, __ldg(a.kacc + idx) + d, uu);
           } else {
-            const double base = (a.alpha != 0.0) ? fma(a.alpha, uu, a.beta * c[mm][j]) : a.beta * c[mm][j];
+            const double base = (a.alpha != 0.0) ? fma(a.alpha, uu, a.beta * c[m][j]) : a.beta * c[m][j];
             o = fma(gdt, d, base);
-            if (a.kmode == 1 && valid) a.kacc[idx] = d;
-            if (a.kmode == 2 && valid) a.kacc[idx] = fma(2.0, d, a.kacc[idx]);
+            if (a.kmode == 1) a.kacc[idx] = d;
+            if (a.kmode == 2) a.kacc[idx] = fma(2.0, d, a.kacc[idx]);
           }
-          if (valid) {
-            a.out[idx] = o;
-            if (a.want_resid) res_max = fmax(res_max, fabs(uu - o));
-          }
-          acc[mm][j] = o;  // keep the new stage for the CFL epilogue
+          a.out[idx] = o;
+          if (a.want_resid) res_max = fmax(res_max, fabs(uu - o));
+          acc[m][j] = o;
         }
       }
       if (a.want_lambda) {
         double lam = 0.0;
-#pragma unroll
+#pragma unroll 1
         for (int q = 0; q < 3; ++q) {
-          double um[MG];
-#pragma unroll
-          for (int mm = 0; mm < MG; ++mm) {
-            double s = T.phm[q][0] * acc[mm][0];
-#pragma unroll
-            for (int j = 1; j < NP; ++j) s = fma(T.phm[q][j], acc[mm][j], s);
-            um[mm] = s;
-          }
           double U[4];
-          gather_state<G, MG>(um, U);
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            double s = T.phm[q][0] * acc[m][0];
+#pragma unroll
+            for (int j = 1; j < NP; ++j) s = fma(T.phm[q][j], acc[m][j], s);
+            U[m] = s;
+          }
           const Prim w = primitives(U, g1);
           if (admissible(U, w)) {
-            lam = fmax(lam, fabs(w.vx * snx[q] + w.vy * sny[q]) + sqrt(gamma * w.p * w.inv));
-          } else if (valid && lane_g == 0) {
+            const int ed = __ldg(geo.eid + q * ld + e);
+            lam = fmax(lam, fabs(w.vx * __ldg(geo.enx + ed) + w.vy * __ldg(geo.eny + ed)) + sqrt(gamma * w.p * w.inv));
+          } else {
             record_error(sc, err_key(a.seq_next, kPassDt, __ldg(geo.ref_id + e), q + 1));
           }
         }
-        if (valid) lam_min = fmin(lam_min, 2.0 * __ldg(geo.inradius + e) / ((2.0 * P + 1.0) * lam));
+        lam_min = fmin(lam_min, 2.0 * __ldg(geo.inradius + e) / ((2.0 * P + 1.0) * lam));
       }
     }
   }

@@ -10,11 +10,14 @@ namespace dgbk {
 // and its own kernel instances.
 namespace {
 __constant__ Tab<DGB_P> c_tab;
-constexpr int kG = LanesPerElem<DGB_P>::G;
+constexpr int kG = Lanes<DGB_P>::value;  // lanes per element
 
 template <int MODE>
-__global__ void __launch_bounds__(kBlock) k_element(Geo geo, StageArgs a) {
-  element_body<DGB_P, kG, MODE>(c_tab, geo, a);
+__global__ void __launch_bounds__(kBlock, MinBlocks<DGB_P>::value) k_element(Geo geo, StageArgs a) {
+  if constexpr (kG == 1)
+    element_body_g1<DGB_P, MODE>(c_tab, geo, a);
+  else
+    element_body<DGB_P, MODE>(c_tab, geo, a);
 }
 
 __global__ void __launch_bounds__(kBlock) k_dt(Geo geo, const double* __restrict__ c, Scalars* sc, int slot,
