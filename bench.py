@@ -10,9 +10,11 @@ device time of the timed regions (CUDA events on the solver stream).
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
-Multi-GPU (torchrun): every rank runs its own copy of the workload (weak
-scaling; the halo-exchange partition is not wired into the benchmark yet) and
-the max over ranks of the device time is used.
+Multi-GPU (torchrun): weak scaling.  The periodic box grows to n x (n*world)
+cells, every rank owns a contiguous strip of 2 n^2 triangles and exchanges the
+halo elements with its neighbours every stage through peer memory (the stage
+kernel stores them into the peer's halo columns).  Device
+time is the max over ranks; `value` counts the DOF updates of all ranks.
 """
 from __future__ import annotations
 
@@ -109,15 +111,20 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-def dist_setup(n_gpus):
+def dist_setup(n_gpus, same_device=False):
     rank, world, local = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), \
         int(os.environ.get("LOCAL_RANK", 0))
     pg = None
+    if same_device:  # test mode: every rank on cuda:0 (gloo; NCCL refuses duplicate GPUs)
+        local = 0
     if world > 1:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if same_device:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         pg = dist
     return rank, world, local, pg
 
@@ -126,7 +133,8 @@ def max_over_ranks(x, pg, local):
     if pg is None:
         return x
     import torch
-    t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+    dev = f"cuda:{local}" if pg.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     pg.all_reduce(t, op=pg.ReduceOp.MAX)
     return float(t.item())
 
@@ -142,13 +150,19 @@ def run_b200(args, rank, world, local, pg):
     from paper_1601_07944_b200 import _lib as L
     from paper_1601_07944_b200 import dg2d
 
+    from paper_1601_07944_b200 import dist as D
+
     torch.cuda.set_device(local)
     scheme, stages = SCHEMES[args.scheme]
     orders = [int(x) for x in args.orders.split(",")]
     n = args.n
-    mesh = dg2d.generate_mesh(L.MESH_PERIODIC_BOX, n, n, 10.0, 10.0)
-    N = mesh.n_elements()
-    e_ratio = mesh.n_edges() / N
+    # weak scaling: the periodic box grows with the rank count (n x n*world cells), every
+    # rank owns a contiguous strip of 2 n^2 triangles and exchanges halo edges with its
+    # two neighbours every stage
+    mesh = dg2d.generate_mesh(L.MESH_PERIODIC_BOX, n, n * world, 10.0, 10.0 * world)
+    N_glob = mesh.n_elements()
+    N = N_glob // world
+    e_ratio = mesh.n_edges() / N_glob
     iv = dg2d.IsentropicVortex()
     hbm_gbs, hbm_src = measured_peaks()
     fp64 = C.c_double()
@@ -162,8 +176,14 @@ def run_b200(args, rank, world, local, pg):
     with sampler:
         for p in orders:
             tb = dg2d.build_tables(p)
-            c0 = dg2d.project_initial(lambda xy: iv(xy), mesh, tb)
-            ctx = dg2d.SolverContext(mesh, tb, options=dg2d.SolverOptions(scheme=scheme, cfl=args.cfl), device=local)
+            opts = dg2d.SolverOptions(scheme=scheme, cfl=args.cfl)
+            if world > 1:
+                ctx = D.PartContext(mesh, tb, rank, world, options=opts, device=local)
+                D.connect_process_group(ctx)
+                c0 = D.project_local(ctx, lambda xy: iv(xy))
+            else:
+                ctx = dg2d.SolverContext(mesh, tb, options=opts, device=local)
+                c0 = dg2d.project_initial(lambda xy: iv(xy), mesh, tb)
             h = ctx.handle
             dg2d._check(L.lib.dgb_set_stream(h, C.c_void_p(stream.cuda_stream)))
             L.lib.dgb_enable_timers(h, 1)
@@ -186,8 +206,8 @@ def run_b200(args, rank, world, local, pg):
             kms, kn = C.c_double(), C.c_int64()
             L.lib.dgb_stage_kernel_ms(h, C.byref(kms), C.byref(kn))
             k_avg = kms.value / max(kn.value, 1)
-            dof = 4 * np_(p) * N
-            upd = dof * stages * args.steps * world
+            dof = 4 * np_(p) * N_glob
+            upd = dof * stages * args.steps
             b, f = alg_bytes(p, e_ratio) * N, alg_flops(p, e_ratio) * N
             ach_bw, ach_fl = b / (k_avg * 1e-3) / 1e9, f / (k_avg * 1e-3) / 1e12
             bound = "hbm" if b / (hbm_gbs * 1e9) >= f / (fp64_tf * 1e12) else "fp64"
@@ -211,14 +231,18 @@ def run_b200(args, rank, world, local, pg):
             # state goes host->device (pinned), one RK step runs, and the new
             # state comes back device->host.
             if args.e2e_steps > 0:
+                # host buffers: the rank's compact input (owned + halo) and its owned output
                 pin = torch.empty(c0.size, dtype=torch.float64, pin_memory=True)
                 hbuf = pin.numpy().reshape(c0.shape)
                 hbuf[...] = c0
                 hp = hbuf.ctypes.data_as(L.c_double_p)
+                n_out = 4 * np_(p) * N
+                pout = torch.empty(n_out, dtype=torch.float64, pin_memory=True)
+                op = pout.numpy().ctypes.data_as(L.c_double_p)
                 for _ in range(2):  # warm-up
                     dg2d._check(L.lib.dgb_upload(h, L.SLOT_STATE, hp))
                     dg2d._check(L.lib.dgb_run_fixed_steps(h, scheme, args.cfl, 0, 1, C.byref(res), None))
-                    dg2d._check(L.lib.dgb_download(h, L.SLOT_STATE, hp))
+                    dg2d._check(L.lib.dgb_download(h, L.SLOT_STATE, op))
                 barrier(pg)
                 torch.cuda.synchronize()
                 t0 = time.perf_counter()
@@ -226,16 +250,16 @@ def run_b200(args, rank, world, local, pg):
                 for _ in range(args.e2e_steps):
                     dg2d._check(L.lib.dgb_upload(h, L.SLOT_STATE, hp))
                     dg2d._check(L.lib.dgb_run_fixed_steps(h, scheme, args.cfl, 0, 1, C.byref(res), None))
-                    dg2d._check(L.lib.dgb_download(h, L.SLOT_STATE, hp))
+                    dg2d._check(L.lib.dgb_download(h, L.SLOT_STATE, op))
                 ev1.record(stream)
                 torch.cuda.synchronize()
                 wall = (time.perf_counter() - t0) * 1e3
                 ms_e = max_over_ranks(max(ev0.elapsed_time(ev1), wall), pg, local)
-                e2e_dof += dof * stages * args.e2e_steps * world
+                e2e_dof += dof * stages * args.e2e_steps
                 e2e_ms += ms_e
-                h2d += c0.nbytes
-                d2h += c0.nbytes
-                per_order[-1]["e2e_value"] = dof * stages * args.e2e_steps * world / (ms_e * 1e-3)
+                h2d += c0.nbytes * world
+                d2h += n_out * 8 * world
+                per_order[-1]["e2e_value"] = dof * stages * args.e2e_steps / (ms_e * 1e-3)
             ctx.close()
 
     dom = max(per_order, key=lambda r: r["stage_kernel_ms"] * stages)
@@ -245,12 +269,13 @@ def run_b200(args, rank, world, local, pg):
         "ms_per_step": tot_ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: periodic isentropic vortex initial data (projected), no dataset",
-        "config": {"workload": f"isentropic vortex, periodic {n}x{n} box ({N} triangles), "
+        "config": {"workload": f"isentropic vortex, periodic {n}x{n * world} box ({N_glob} triangles), "
                                f"p={','.join(map(str, orders))} sweep, {args.scheme.upper()}, cfl {args.cfl}",
-                   "triangles_per_gpu": N, "edges_per_gpu": mesh.n_edges(), "orders": orders,
+                   "triangles_per_gpu": N, "edges_per_gpu": mesh.n_edges() // world, "orders": orders,
                    "scheme": args.scheme, "stages_per_step": stages,
                    "l2": "inputs larger than L2 (>=288 MB of coefficients per stage)",
-                   "parallelism": f"replica x{world}" if world > 1 else "single GPU"},
+                   "parallelism": (f"element partition x{world} (contiguous strips), peer-memory halo "
+                                   "exchange fused into the stage kernel") if world > 1 else "single GPU"},
         "roofline": dict(dom["roofline"], p=dom["p"],
                          note=f"dominant kernel = fused stage kernel at p={dom['p']}; "
                               f"HBM peak {hbm_src}; FP64 peak measured in-run (DFMA loop) {fp64_tf:.1f} TF/s"),
@@ -352,17 +377,19 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--n", type=int, default=708, help="box cells per side (2 n^2 triangles)")
+    ap.add_argument("--box", dest="n", type=int, default=708, help="box cells per side (2 n^2 triangles per GPU)")
     ap.add_argument("--orders", default="1,2,3,4,5")
     ap.add_argument("--scheme", default="ssp3", choices=list(SCHEMES))
     ap.add_argument("--cfl", type=float, default=0.3)
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--cpu-n", type=int, default=708, help="box size of the CPU sample")
+    ap.add_argument("--cpu-box", dest="cpu_n", type=int, default=708, help="box size of the CPU sample")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--same-device", action="store_true",
+                    help="test mode: all ranks share cuda:0 (partitioned path on one GPU)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    rank, world, local, pg = dist_setup(args.gpus)
+    rank, world, local, pg = dist_setup(args.gpus, args.same_device)
     if args.impl == "reference":
         line = run_reference(args, rank, world)
     else:

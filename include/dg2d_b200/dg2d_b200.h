@@ -188,6 +188,58 @@ typedef struct dgb_abort_info {
 } dgb_abort_info;
 int dgb_last_abort(dgb_ctx* ctx, dgb_abort_info* out);
 
+/* ---------------------------------------------------------------- partitions (multi-GPU)
+ * SURVEY.md 8(e); no reference counterpart (the reference is one shared-memory
+ * process, solver.cpp OpenMP loops).  Rank r of `world` owns the contiguous
+ * reference ids [n*r/world, n*(r+1)/world) ("identical partition indexing").
+ * Its context holds the owned elements plus halo columns for the off-rank
+ * neighbours.  Coefficient arrays of a partitioned context cross the ABI in
+ * "compact" order: dgb_upload takes [4][n_p][n_owned + n_halo] (owned in
+ * ascending id, then halo in ascending id, see dgb_part_local_ids), dgb_download
+ * returns [4][n_p][n_owned].  Every RK stage the elements a peer needs are
+ * written straight into the peer's halo columns by the stage kernel (peer
+ * memory over NVLink), then an epoch flag is raised; each rank computes its
+ * interior elements while waiting for the peers' flags.  Setup: create on every
+ * rank, exchange peer views (same process) or IPC handles (one process per
+ * GPU), tell every rank which of its elements each peer needs
+ * (dgb_part_set_sends with the peer's halo ids/columns), then dgb_part_finalize.
+ * After that the ordinary dgb_run_* / dgb_rk_step calls run the partitioned
+ * solve; all ranks must issue the same sequence of calls. */
+int dgb_part_create(const dgb_mesh_view* mesh, const dgb_tables_view* tables, const dgb_bc_view* bc,
+                    double gamma, int device, int rank, int world, dgb_ctx** out);
+typedef struct dgb_part_info {
+  int32_t rank, world, lo, hi, n_owned, n_halo, n_interior, ld;
+  uint32_t neighbor_mask; /* ranks owning halo elements */
+} dgb_part_info;
+int dgb_part_get_info(dgb_ctx* ctx, dgb_part_info* out);
+/* Host-only plan of rank `rank` (no device needed): counts in *info, then the halo
+ * ids (ascending; halo column = n_owned + index) and the boundary element ids
+ * (owned elements with an off-rank neighbour, ascending); arrays may be NULL. */
+int dgb_part_plan(const dgb_mesh_view* mesh, int rank, int world, dgb_part_info* info, int32_t* halo_ids,
+                  int32_t* boundary_ids);
+/* Halo columns: reference ids and device columns (a peer feeds these). */
+int dgb_part_halo_ids(dgb_ctx* ctx, int32_t* ids, int32_t* cols);
+/* Compact local order used by dgb_upload: owned ids then halo ids. */
+int dgb_part_local_ids(dgb_ctx* ctx, int32_t* ids);
+/* Device addresses a peer writes to (same-process attachment). */
+typedef struct dgb_peer_view {
+  void* buf[4];  /* rotating coefficient buffers */
+  void* flags;   /* [8] epoch flags */
+  void* scal;    /* [2][8][4] scalar exchange */
+  int32_t ld;
+} dgb_peer_view;
+int dgb_part_peer_view(dgb_ctx* ctx, dgb_peer_view* out);
+int dgb_part_attach_peer(dgb_ctx* ctx, int peer, const dgb_peer_view* view);
+/* Cross-process attachment through CUDA IPC: DGB_IPC_BYTES of handles. */
+#define DGB_IPC_BYTES (5 * 64)
+int dgb_part_ipc_export(dgb_ctx* ctx, void* handles);
+int dgb_part_attach_peer_ipc(dgb_ctx* ctx, int peer, const void* handles, int32_t peer_ld);
+/* Elements of this rank (reference ids) that `peer` holds as halo, at the peer's columns. */
+int dgb_part_set_sends(dgb_ctx* ctx, int peer, int64_t n, const int32_t* ids, const int32_t* peer_cols);
+int dgb_part_finalize(dgb_ctx* ctx);
+/* Bound on a halo wait before the run fails with DGB_ERR_CUDA (default 60 s). */
+int dgb_part_set_timeout(dgb_ctx* ctx, double seconds);
+
 /* Kernel launches issued by this context so far (benchmark evidence). */
 int64_t dgb_launch_count(dgb_ctx* ctx);
 /* Per-step kernel-only timing helper for the benchmark: device ms of the fused

@@ -58,6 +58,18 @@ class PassTimers(C.Structure):
     _fields_ = [(n, C.c_double) for n in ("volume", "surface", "rhs", "limiter", "other", "stage")]
 
 
+class PartInfo(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("rank", "world", "lo", "hi", "n_owned", "n_halo", "n_interior", "ld")] + \
+        [("neighbor_mask", C.c_uint32)]
+
+
+class PeerView(C.Structure):
+    _fields_ = [("buf", C.c_void_p * 4), ("flags", C.c_void_p), ("scal", C.c_void_p), ("ld", C.c_int32)]
+
+
+IPC_BYTES = 5 * 64
+
+
 class AbortInfo(C.Structure):
     _fields_ = [("where", C.c_char * 32), ("id", C.c_int64), ("point", C.c_int32),
                 ("rho", C.c_double), ("p", C.c_double)]
@@ -113,6 +125,19 @@ _sig("dgb_last_abort", C.c_int, _vp, C.POINTER(AbortInfo))
 _sig("dgb_launch_count", C.c_int64, _vp)
 _sig("dgb_stage_kernel_ms", C.c_int, _vp, c_double_p, c_int64_p)
 _sig("dgb_fp64_peak", C.c_int, C.c_int, c_double_p)
+_sig("dgb_part_create", C.c_int, C.POINTER(MeshView), C.POINTER(TablesView), C.POINTER(BcView),
+     C.c_double, C.c_int, C.c_int, C.c_int, C.POINTER(_vp))
+_sig("dgb_part_plan", C.c_int, C.POINTER(MeshView), C.c_int, C.c_int, C.POINTER(PartInfo), c_int32_p, c_int32_p)
+_sig("dgb_part_get_info", C.c_int, _vp, C.POINTER(PartInfo))
+_sig("dgb_part_halo_ids", C.c_int, _vp, c_int32_p, c_int32_p)
+_sig("dgb_part_local_ids", C.c_int, _vp, c_int32_p)
+_sig("dgb_part_peer_view", C.c_int, _vp, C.POINTER(PeerView))
+_sig("dgb_part_attach_peer", C.c_int, _vp, C.c_int, C.POINTER(PeerView))
+_sig("dgb_part_ipc_export", C.c_int, _vp, C.c_void_p)
+_sig("dgb_part_attach_peer_ipc", C.c_int, _vp, C.c_int, C.c_void_p, C.c_int32)
+_sig("dgb_part_set_sends", C.c_int, _vp, C.c_int, C.c_int64, c_int32_p, c_int32_p)
+_sig("dgb_part_finalize", C.c_int, _vp)
+_sig("dgb_part_set_timeout", C.c_int, _vp, C.c_double)
 _sig("dgb_mesh_from_msh", C.c_int, C.c_char_p, C.c_size_t, C.POINTER(_vp))
 _sig("dgb_mesh_generate", C.c_int, C.c_int, C.c_int, C.c_int, c_double_p, C.c_int, C.POINTER(_vp))
 _sig("dgb_mesh_generate_text", C.c_int, C.c_int, C.c_int, C.c_int, c_double_p, C.c_int,

@@ -76,8 +76,18 @@ struct Scalars {
   double dt_used[2];           // dt of step s in [s & 1]
 };
 
+// Peer-memory halo exchange (multi-GPU).  One entry per
+// rank of the job; the local rank's entry is unused.
+constexpr int kMaxRanks = 8;
+struct PeerTab {
+  double* buf[kMaxRanks][4];            // the peer's rotating coefficient buffers (state0/1, stage0/1)
+  long long ld[kMaxRanks];              // the peer's leading dimension
+  unsigned long long* flag[kMaxRanks];  // the peer's flag array [kMaxRanks] (we write our slot)
+  unsigned long long* scal[kMaxRanks];  // the peer's scalar exchange [2][kMaxRanks][4]
+};
+
 struct Geo {
-  int N, ld;
+  int N, ld;                           // N = owned elements (device columns [0, N)); halo columns follow
   const double* __restrict__ tau;      // [4][ld]
   const double* __restrict__ inv_det;  // [ld]
   const double* __restrict__ inradius; // [ld]
@@ -96,6 +106,11 @@ struct Geo {
   double sh_x0, sh_cos, sh_sin, sh_speed;
   double sh_post[4], sh_pre[4];
   double gamma;
+  // halo sends: device columns [send_begin, N) may feed peers; entries
+  // send_ent[send_ptr[d - send_begin] .. send_ptr[d - send_begin + 1]) = (peer rank, peer column)
+  const int* __restrict__ send_ptr;
+  const int2* __restrict__ send_ent;
+  int send_begin;
 };
 
 // Modes of the fused element kernel.
@@ -124,6 +139,10 @@ struct StageArgs {
   unsigned long long seq_next;    // sequence number of the next step's CFL pass
   Scalars* sc;
   double* hist;                   // optional residual history (on_step)
+  int e0, e1;                     // device element range of this launch
+  int push;                       // write the new stage of send elements into the peers' halo columns
+  int out_buf;                    // index of `out` among the rotating buffers (peer addressing)
+  const PeerTab* peers;
 };
 
 struct LimArgs {
@@ -132,6 +151,9 @@ struct LimArgs {
   int step, want_lambda, want_resid;
   unsigned long long seq;         // error key for the CFL epilogue (next step)
   Scalars* sc;
+  int e0, e1;                     // device element range of this launch
+  int push, out_buf;              // as StageArgs: push the limited element to the peers
+  const PeerTab* peers;
 };
 
 }  // namespace dgbk

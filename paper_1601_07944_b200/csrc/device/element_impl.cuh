@@ -220,6 +220,25 @@ __device__ __forceinline__ double pick_weight(const double (&we)[K], int k) {
   return r;
 }
 
+// Halo push: store the new values of variables
+// [m0, m0 + MG) of send element `e` into the halo columns of every peer that
+// needs it, over NVLink peer memory (plain global stores to IPC-mapped buffers).
+template <int NP, int MG>
+__device__ __forceinline__ void push_element(const Geo& geo, const PeerTab* __restrict__ pt, int out_buf, int e, int m0,
+                                             const double (&v)[MG][NP]) {
+  const int s0 = __ldg(geo.send_ptr + (e - geo.send_begin));
+  const int s1 = __ldg(geo.send_ptr + (e - geo.send_begin) + 1);
+  for (int s = s0; s < s1; ++s) {
+    const int2 ent = __ldg(geo.send_ent + s);
+    double* __restrict__ dst = pt->buf[ent.x][out_buf];
+    const long long pld = pt->ld[ent.x];
+#pragma unroll
+    for (int mm = 0; mm < MG; ++mm)
+#pragma unroll
+      for (int j = 0; j < NP; ++j) dst[(static_cast<long long>(m0 + mm) * NP + j) * pld + ent.y] = v[mm][j];
+  }
+}
+
 // Minimum registers per launch for the fused kernel (occupancy target per degree).
 #ifndef DGB_MINB
 #define DGB_MINB(P) ((P) == 1 ? 5 : (P) == 2 ? 3 : (P) == 3 ? 5 : (P) == 4 ? 4 : 3)
@@ -262,7 +281,7 @@ template <int P, int MODE>
 __device__ __forceinline__ void element_body(const Tab<P>& T, const Geo& geo, const StageArgs& a) {
   constexpr int NP = Dim<P>::NP, NQ = Dim<P>::NQ, K = Dim<P>::K;
   const long long ld = geo.ld;
-  const int gsize = geo.ld * 4;
+  const int gsize = ((a.e1 - a.e0 + 31) & ~31) * 4;  // whole warps (8 elements each), whole blocks
   const int stride = gridDim.x * blockDim.x;
   const double gamma = geo.gamma, g1 = gamma - 1.0;
   Scalars* sc = a.sc;
@@ -315,9 +334,9 @@ __device__ __forceinline__ void element_body(const Tab<P>& T, const Geo& geo, co
 
   for (int tid = blockIdx.x * blockDim.x + threadIdx.x; tid < gsize; tid += stride) {
     const int g = tid & 3;  // conserved variable owned by this lane
-    int e = tid >> 2;
-    const bool valid = e < geo.N;
-    if (!valid) e = geo.N - 1;
+    int e = a.e0 + (tid >> 2);
+    const bool valid = e < a.e1;
+    if (!valid) e = a.e1 - 1;
     const long long row = static_cast<long long>(g) * NP * ld + e;  // (g, j=0, e)
 
     double c[NP];
@@ -493,6 +512,10 @@ __device__ __forceinline__ void element_body(const Tab<P>& T, const Geo& geo, co
         }
         acc[j] = o;  // keep the new stage for the CFL epilogue
       }
+      if (a.push && valid && e >= geo.send_begin) {
+        const double(&v)[1][NP] = reinterpret_cast<const double(&)[1][NP]>(acc);
+        push_element<NP, 1>(geo, a.peers, a.out_buf, e, g, v);
+      }
       if (a.want_lambda) {
         double v[4];
 #pragma unroll
@@ -525,6 +548,7 @@ __device__ __forceinline__ void element_body(const Tab<P>& T, const Geo& geo, co
     const int par = a.step & 1;
     if (a.want_lambda) block_reduce_atomic<true>(lam_min, &sc->dtmin[par ^ 1]);
     if (a.want_resid) block_reduce_atomic<false>(res_max, &sc->resid[par]);
+    if (a.push) __threadfence_system();  // halo stores visible before the signal kernel's flag
   }
 }
 
@@ -585,10 +609,7 @@ __device__ __forceinline__ void element_body_g1(const Tab<P>& T, const Geo& geo,
   double lam_min = __longlong_as_double(0x7ff0000000000000ll);
   double res_max = 0.0;
 
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < geo.ld; e += stride) {
-    const bool valid = e < geo.N;
-    if (!valid) continue;
-
+  for (int e = a.e0 + blockIdx.x * blockDim.x + threadIdx.x; e < a.e1; e += stride) {
     double c[4][NP];
 #pragma unroll
     for (int m = 0; m < 4; ++m)
@@ -746,6 +767,7 @@ __device__ __forceinline__ void element_body_g1(const Tab<P>& T, const Geo& geo,
           acc[m][j] = o;
         }
       }
+      if (a.push && e >= geo.send_begin) push_element<NP, 4>(geo, a.peers, a.out_buf, e, 0, acc);
       if (a.want_lambda) {
         double lam = 0.0;
 #pragma unroll 1
@@ -775,6 +797,7 @@ __device__ __forceinline__ void element_body_g1(const Tab<P>& T, const Geo& geo,
     const int par = a.step & 1;
     if (a.want_lambda) block_reduce_atomic<true>(lam_min, &sc->dtmin[par ^ 1]);
     if (a.want_resid) block_reduce_atomic<false>(res_max, &sc->resid[par]);
+    if (a.push) __threadfence_system();  // halo stores visible before the signal kernel's flag
   }
 }
 

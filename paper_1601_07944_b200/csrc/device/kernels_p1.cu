@@ -32,8 +32,7 @@ __global__ void __launch_bounds__(kBlock) k_limit(Geo geo, LimArgs a) {
   double lam_min = __longlong_as_double(0x7ff0000000000000ll);
   double res_max = 0.0;
 
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < geo.ld; e += gridDim.x * blockDim.x) {
-    if (e >= geo.N) continue;
+  for (int e = a.e0 + blockIdx.x * blockDim.x + threadIdx.x; e < a.e1; e += gridDim.x * blockDim.x) {
     double c0[4], c1[4], c2[4];
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
@@ -125,6 +124,10 @@ __global__ void __launch_bounds__(kBlock) k_limit(Geo geo, LimArgs a) {
       a.c[(m * NP + 1) * ld + e] = c1[m];
       a.c[(m * NP + 2) * ld + e] = c2[m];
     }
+    if (a.push && e >= geo.send_begin) {
+      const double v[4][NP] = {{c0[0], c1[0], c2[0]}, {c0[1], c1[1], c2[1]}, {c0[2], c1[2], c2[2]}, {c0[3], c1[3], c2[3]}};
+      push_element<NP, 4>(geo, a.peers, a.out_buf, e, 0, v);
+    }
     if (a.want_resid) {
 #pragma unroll
       for (int m = 0; m < 4; ++m) {
@@ -155,6 +158,7 @@ __global__ void __launch_bounds__(kBlock) k_limit(Geo geo, LimArgs a) {
   const int par = a.step & 1;
   if (a.want_lambda) block_reduce_atomic<true>(lam_min, &sc->dtmin[par ^ 1]);
   if (a.want_resid) block_reduce_atomic<false>(res_max, &sc->resid[par]);
+  if (a.push) __threadfence_system();  // halo stores visible before the signal kernel's flag
 }
 }  // namespace
 
@@ -169,7 +173,8 @@ int limit_resident_blocks() {
 }
 
 cudaError_t launch_limit(int grid, const Geo& g, const LimArgs& a, cudaStream_t s) {
-  if (grid <= 0) grid = grid_for(g.ld, limit_resident_blocks());
+  if (a.e1 <= a.e0) return cudaSuccess;
+  if (grid <= 0) grid = grid_for(a.e1 - a.e0, limit_resident_blocks());
   k_limit<<<grid, kBlock, 0, s>>>(g, a);
   return cudaGetLastError();
 }

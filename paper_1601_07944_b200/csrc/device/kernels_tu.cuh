@@ -73,7 +73,8 @@ int Launch<DGB_P>::lanes() {
 
 template <>
 cudaError_t Launch<DGB_P>::element(int mode, int grid, const Geo& g, const StageArgs& a, cudaStream_t s) {
-  if (grid <= 0) grid = grid_for(static_cast<long long>(g.ld) * kG, resident_blocks(mode));
+  if (a.e1 <= a.e0) return cudaSuccess;
+  if (grid <= 0) grid = grid_for(static_cast<long long>((a.e1 - a.e0 + 31) & ~31) * kG, resident_blocks(mode));
   switch (mode) {
     case kModeVolume: k_element<kModeVolume><<<grid, kBlock, 0, s>>>(g, a); break;
     case kModeSurface: k_element<kModeSurface><<<grid, kBlock, 0, s>>>(g, a); break;

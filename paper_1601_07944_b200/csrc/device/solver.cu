@@ -62,23 +62,106 @@ struct DevBuf {
 };
 
 // ------------------------------------------------------------------ small kernels
-__global__ void k_permute_in(double* __restrict__ dst, const double* __restrict__ src, const int* __restrict__ ref_of,
-                             int n, int ld, int rows) {
+// Reference (host) layout <-> device layout.  Host arrays are [rows][n_host] in
+// "compact" order: the reference order for a whole-mesh context, and for a
+// partition the owned elements (ascending reference id) followed by the halo
+// elements (ascending reference id).  cmp[d] = compact index of device column d.
+__global__ void k_permute_in(double* __restrict__ dst, const double* __restrict__ src, const int* __restrict__ cmp,
+                             int n_cols, int n_host, int ld, int rows) {
   const long long total = static_cast<long long>(rows) * ld;
   for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < total;
        t += static_cast<long long>(gridDim.x) * blockDim.x) {
     const int r = static_cast<int>(t / ld), d = static_cast<int>(t % ld);
-    dst[t] = d < n ? src[static_cast<long long>(r) * n + ref_of[d]] : 0.0;
+    dst[t] = d < n_cols ? src[static_cast<long long>(r) * n_host + cmp[d]] : 0.0;
   }
 }
 
-__global__ void k_permute_out(double* __restrict__ dst, const double* __restrict__ src, const int* __restrict__ ref_of,
-                              int n, int ld, int rows) {
+__global__ void k_permute_out(double* __restrict__ dst, const double* __restrict__ src, const int* __restrict__ cmp,
+                              int n_cols, int n_host, int ld, int rows) {
   const long long total = static_cast<long long>(rows) * ld;
   for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < total;
        t += static_cast<long long>(gridDim.x) * blockDim.x) {
     const int r = static_cast<int>(t / ld), d = static_cast<int>(t % ld);
-    if (d < n) dst[static_cast<long long>(r) * n + ref_of[d]] = src[t];
+    if (d < n_cols) dst[static_cast<long long>(r) * n_host + cmp[d]] = src[t];
+  }
+}
+
+// ------------------------------------------------------------------ halo exchange
+// Error key of an exchange timeout (sorts before every solver error).
+constexpr unsigned long long kTimeoutKey = (7ull << 35);
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// One warp: publish (optionally) this rank's step scalars into every peer of
+// `mask`, then raise our flag there to `epoch`.  The stage kernel that pushed
+// the halo values fenced them (system scope) before it completed.
+__global__ void k_signal(const dgbk::PeerTab* __restrict__ pt, unsigned mask, int me, unsigned long long epoch,
+                         const dgbk::Scalars* __restrict__ sc, int publish, int slot, int dt_idx, int res_idx) {
+  const int r = threadIdx.x;
+  unsigned long long v0 = 0, v1 = 0, v2 = 0;
+  if (publish) {
+    v0 = sc->dtmin[dt_idx];
+    v1 = sc->resid[res_idx];
+    v2 = sc->err_key;
+  }
+  __threadfence_system();
+  if (r < dgbk::kMaxRanks && ((mask >> r) & 1u)) {
+    if (publish) {
+      unsigned long long* dst = pt->scal[r] + (static_cast<long long>(slot) * dgbk::kMaxRanks + me) * 4;
+      dst[0] = v0;
+      dst[1] = v1;
+      dst[2] = v2;
+      __threadfence_system();
+    }
+    st_release_sys(pt->flag[r] + me, epoch);
+  }
+}
+
+// One warp: wait until every rank of `mask` raised its flag in our memory to
+// at least `epoch` (bounded by a timeout that turns into an error key), then
+// optionally merge the published scalars: min dt bound, max residual, min error.
+__global__ void k_wait(const unsigned long long* __restrict__ flags, const unsigned long long* __restrict__ scal,
+                       unsigned mask, unsigned long long epoch, dgbk::Scalars* sc, int merge, int slot, int dt_idx,
+                       int res_idx, unsigned long long timeout_ns) {
+  const int r = threadIdx.x;
+  bool ok = true;
+  if (r < dgbk::kMaxRanks && ((mask >> r) & 1u)) {
+    const unsigned long long t0 = global_ns();
+    while (ld_acquire_sys(flags + r) < epoch) {
+      if (global_ns() - t0 > timeout_ns) {
+        ok = false;
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+  ok = __all_sync(0xffffffffu, ok);
+  if (r != 0) return;
+  if (!ok) {
+    atomicMin(&sc->err_key, kTimeoutKey);
+    return;
+  }
+  if (!merge) return;
+  __threadfence_system();
+  for (int k = 0; k < dgbk::kMaxRanks; ++k) {
+    if (!((mask >> k) & 1u)) continue;
+    const unsigned long long* v = scal + (static_cast<long long>(slot) * dgbk::kMaxRanks + k) * 4;
+    const unsigned long long v0 = ld_acquire_sys(v), v1 = ld_acquire_sys(v + 1), v2 = ld_acquire_sys(v + 2);
+    if (v0 < sc->dtmin[dt_idx]) sc->dtmin[dt_idx] = v0;  // non-negative doubles order like their bits
+    if (v1 > sc->resid[res_idx]) sc->resid[res_idx] = v1;
+    if (v2 < sc->err_key) sc->err_key = v2;
   }
 }
 
@@ -180,12 +263,31 @@ struct dgb_ctx {
   std::vector<double> bc_dir, bc_wn;
   dgb_bc_view bc{};
   std::vector<double> t_phi, t_phe, t_phm, t_xi;
-  std::vector<int> ref_of, dev_of;
+  std::vector<int> ref_of;   // device column -> reference element id (owned, then halo)
+  std::vector<int> col_of;   // reference element id -> device column (-1 when not local)
+  std::vector<int> halo_gid; // reference ids of the halo columns [N, N + n_halo)
+
+  // partition (multi-GPU); a whole-mesh context is rank 0 of 1
+  int rank = 0, world = 1, lo = 0, hi = 0, n_global = 0, n_int = 0, n_halo = 0;
+  bool partitioned = false, finalized = true;
+  unsigned nb_mask = 0;                       // ranks owning our halo elements (we wait on them)
+  unsigned send_mask = 0;                     // ranks fed from our send elements (we signal them)
+  std::vector<std::vector<std::pair<int, int>>> sends;  // per peer: (reference id, peer column)
+  dgbk::PeerTab h_peers{};
+  dgbk::PeerTab* d_peers = nullptr;
+  unsigned long long* d_xch = nullptr;        // flags[kMaxRanks] + scalar slots [2][kMaxRanks][4]
+  std::vector<void*> ipc_opened;
+  DevBuf<int> d_cmp, d_send_ptr;
+  DevBuf<int2> d_send_ent;
+  unsigned long long epoch = 0;               // signals sent so far (same sequence on every rank)
+  unsigned long long pub_epoch = 0;           // epoch of the last scalar publish
+  int64_t n_pub = 0;                          // publishes so far (slot = n_pub & 1)
+  double timeout_s = 60.0;
   std::string bc_error;  // deferred boundary-condition failure (reference throws in the surface pass)
 
   // device geometry
   DevBuf<double> d_tau, d_inv_det, d_inradius, d_enx, d_eny, d_eh, d_bstate, d_bwn, d_bx;
-  DevBuf<int> d_nbr, d_eid, d_info, d_ref_id;
+  DevBuf<int> d_nbr, d_eid, d_info, d_ref_id;  // d_ref_id: reference id of each device column
   Geo geo{};
 
   // coefficient buffers (device order [4][np][ld])
@@ -398,21 +500,26 @@ void read_scalars(dgb_ctx* c) {
   sync(c);
 }
 
+// Device -> host: the owned columns, [rows][N] in compact order.
 void download_dev(dgb_ctx* c, const double* dev, int rows, double* host) {
-  if (c->staging.n < static_cast<size_t>(rows) * c->N) c->staging.alloc(static_cast<size_t>(rows) * c->N);
+  const size_t n = static_cast<size_t>(rows) * c->N;
+  if (c->staging.n < n) c->staging.alloc(n);
   k_permute_out<<<small_grid(static_cast<long long>(rows) * c->ld), 256, 0, c->stream>>>(
-      c->staging.p, dev, c->d_ref_id.p, c->N, c->ld, rows);
+      c->staging.p, dev, c->d_cmp.p, c->N, c->N, c->ld, rows);
   CU(cudaGetLastError());
   ++c->launches;
-  CU(cudaMemcpyAsync(host, c->staging.p, sizeof(double) * rows * c->N, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaMemcpyAsync(host, c->staging.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
   sync(c);
 }
 
+// Host -> device: owned + halo columns from [rows][N + n_halo] in compact order.
 void upload_dev(dgb_ctx* c, double* dev, int rows, const double* host) {
-  if (c->staging.n < static_cast<size_t>(rows) * c->N) c->staging.alloc(static_cast<size_t>(rows) * c->N);
-  CU(cudaMemcpyAsync(c->staging.p, host, sizeof(double) * rows * c->N, cudaMemcpyHostToDevice, c->stream));
+  const int nl = c->N + c->n_halo;
+  const size_t n = static_cast<size_t>(rows) * nl;
+  if (c->staging.n < n) c->staging.alloc(n);
+  CU(cudaMemcpyAsync(c->staging.p, host, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
   k_permute_in<<<small_grid(static_cast<long long>(rows) * c->ld), 256, 0, c->stream>>>(
-      dev, c->staging.p, c->d_ref_id.p, c->N, c->ld, rows);
+      dev, c->staging.p, c->d_cmp.p, nl, nl, c->ld, rows);
   CU(cudaGetLastError());
   ++c->launches;
 }
@@ -452,9 +559,18 @@ std::string failure_message(dgb_ctx* c, unsigned long long key, const double* de
   const int pass = static_cast<int>((key >> 35) & 7);
   const long long id = static_cast<long long>((key >> 5) & 0x3fffffff);
   const int point = static_cast<int>(key & 31);
+  if (pass == 7) return "halo exchange timed out (a peer rank stopped signalling)";
   std::vector<double> h(static_cast<size_t>(4) * c->np * c->N);
   download_dev(c, dev_in, 4 * c->np, h.data());
-  auto coef = [&](int m, int j, int i) { return h[(static_cast<size_t>(m) * c->np + j) * c->N + i]; };
+  // the download holds the owned elements only (compact index = reference id - lo)
+  bool have = true;
+  auto coef = [&](int m, int j, int i) {
+    if (i < c->lo || i >= c->hi) {
+      have = false;
+      return 0.0;
+    }
+    return h[(static_cast<size_t>(m) * c->np + j) * c->N + (i - c->lo)];
+  };
   double u[4] = {0, 0, 0, 0};
   const char* where = "eval_volume";
   if (pass == dgbk::kPassVolume) {
@@ -493,6 +609,7 @@ std::string failure_message(dgb_ctx* c, unsigned long long key, const double* de
     const bool okl = ul[0] > 0.0 && pressure_ref(ul, c->gamma) > 0.0;
     std::memcpy(u, okl ? ur : ul, sizeof u);
   }
+  if (!have) u[0] = u[3] = std::nan("");  // failing element lives on another rank
   const double pr = pressure_ref(u, c->gamma);
   std::snprintf(c->last_abort.where, sizeof c->last_abort.where, "%s", where);
   c->last_abort.id = id;
@@ -537,6 +654,8 @@ void run_pass(dgb_ctx* c, int mode, const double* in, double* out, double t, int
   a.seq = 1;
   a.seq_next = 2;
   a.sc = c->d_sc;
+  a.e0 = 0;
+  a.e1 = c->N;
   {
     Timed tm(c, cat);
     CU(launch_element(c, mode, a));
@@ -565,10 +684,46 @@ struct RunOut {
   bool halted = false;
 };
 
+int buf_id(const dgb_ctx* c, const double* p) {
+  if (p == c->state[0].p) return 0;
+  if (p == c->state[1].p) return 1;
+  if (p == c->stage[0].p) return 2;
+  if (p == c->stage[1].p) return 3;
+  return -1;
+}
+
+bool exchanging(const dgb_ctx* c) { return c->partitioned && c->world > 1; }
+
+unsigned all_peers(const dgb_ctx* c) { return ((1u << c->world) - 1u) & ~(1u << c->rank); }
+
+// Raise our flag at the peers in `mask` (publishing the step scalars to every
+// rank when `publish`).  Returns the epoch of this signal.
+unsigned long long xch_signal(dgb_ctx* c, unsigned mask, bool publish, int dt_idx, int res_idx) {
+  const unsigned long long ep = ++c->epoch;
+  const int slot = static_cast<int>(c->n_pub & 1);
+  k_signal<<<1, 32, 0, c->stream>>>(c->d_peers, mask, c->rank, ep, c->d_sc, publish ? 1 : 0, slot, dt_idx, res_idx);
+  CU(cudaGetLastError());
+  ++c->launches;
+  if (publish) {
+    c->pub_epoch = ep;
+    ++c->n_pub;
+  }
+  return ep;
+}
+
+void xch_wait(dgb_ctx* c, unsigned mask, unsigned long long ep, bool merge, int dt_idx, int res_idx) {
+  const int slot = static_cast<int>((c->n_pub - 1) & 1);
+  k_wait<<<1, 32, 0, c->stream>>>(c->d_xch, c->d_xch + dgbk::kMaxRanks, mask, ep, c->d_sc, merge ? 1 : 0, slot, dt_idx,
+                                  res_idx, static_cast<unsigned long long>(c->timeout_s * 1e9));
+  CU(cudaGetLastError());
+  ++c->launches;
+}
+
 RunOut run_steps(dgb_ctx* c, const RunSpec& r) {
   std::vector<StageSpec> st;
   if (!scheme_stages(r.scheme, st)) throw Fail{DGB_ERR_ARG, "rk_order must be 2 or 4"};
   if (r.limiting && c->p != 1) throw Fail{DGB_ERR_ARG, "slope limiting is only supported for p = 1"};
+  if (!c->finalized) throw Fail{DGB_ERR_ARG, "partitioned context used before dgb_part_finalize"};
   check_bc(c);
   ensure_tables(c);
   const int S = static_cast<int>(st.size());
@@ -581,6 +736,11 @@ RunOut run_steps(dgb_ctx* c, const RunSpec& r) {
     if (c->hist.n < static_cast<size_t>(r.hist_cap)) c->hist.alloc(r.hist_cap);
     d_hist = c->hist.p;
   }
+  const bool X = exchanging(c);
+  const unsigned ALL = X ? all_peers(c) : 0u;
+  // interior elements [0, n_int) never read a halo column; boundary elements
+  // [n_int, N) do, and only they feed the peers
+  const int n_int = X ? c->n_int : c->N;
 
   const int cur0 = c->cur;
   reset_scalars(c, c->t);
@@ -589,6 +749,9 @@ RunOut run_steps(dgb_ctx* c, const RunSpec& r) {
     CU(launch_dt(c, c->state[cur0].p, 0, 0));
     ++c->launches;
   }
+  // the first step's dt bound is a global min over the ranks
+  if (X) xch_signal(c, ALL, true, 0, 0);
+
   RunOut out;
   int64_t launched = 0;
   bool stop = false;
@@ -597,6 +760,7 @@ RunOut run_steps(dgb_ctx* c, const RunSpec& r) {
                                              (r.stop_t || r.stop_steady) ? kBatch : r.max_steps);
     for (int64_t b = 0; b < batch; ++b) {
       const int64_t s = launched + b;
+      const int par = static_cast<int>(s & 1);
       double* u = c->state[(cur0 + s) & 1].p;
       double* unext = c->state[(cur0 + s + 1) & 1].p;
       for (int k = 0; k < S; ++k) {
@@ -628,11 +792,32 @@ RunOut run_steps(dgb_ctx* c, const RunSpec& r) {
         a.seq_next = static_cast<unsigned long long>(s + 1) * 8;
         a.sc = c->d_sc;
         a.hist = d_hist && s <= r.hist_cap ? d_hist : nullptr;
+        a.peers = c->d_peers;
+        a.out_buf = buf_id(c, a.out);
+        // step start: merge the previous step's scalars (dt bound, residual, error) from every rank
+        if (X && k == 0) xch_wait(c, ALL, c->pub_epoch, true, par, par ^ 1);
+        const unsigned long long prev = c->epoch;
         {
           Timed tm(c, 5);
+          a.e0 = 0;
+          a.e1 = n_int;
           CU(launch_element(c, dgbk::kModeStage, a));
           ++c->launches;
           ++c->stage_launches;
+          if (X) {
+            if (k > 0) xch_wait(c, c->nb_mask, prev, false, 0, 0);  // the peers' previous stage landed
+            a.e0 = n_int;
+            a.e1 = c->N;
+            a.push = 1;
+            CU(launch_element(c, dgbk::kModeStage, a));
+            ++c->launches;
+          }
+        }
+        if (X) {
+          if (last && !r.limiting)
+            xch_signal(c, ALL, true, par ^ 1, par);
+          else
+            xch_signal(c, c->send_mask, false, 0, 0);
         }
         if (r.limiting) {
           LimArgs la{};
@@ -643,17 +828,37 @@ RunOut run_steps(dgb_ctx* c, const RunSpec& r) {
           la.want_resid = last;
           la.seq = static_cast<unsigned long long>(s + 1) * 8;
           la.sc = c->d_sc;
+          la.peers = c->d_peers;
+          la.out_buf = a.out_buf;
+          const unsigned long long prev2 = c->epoch;
           Timed tm(c, 3);
+          la.e0 = 0;
+          la.e1 = n_int;
           CU(dgbk::launch_limit(0, c->geo, la, c->stream));
           ++c->launches;
+          if (X) {
+            // the limiter needs the neighbours' new means: wait for this stage's halo
+            xch_wait(c, c->nb_mask, prev2, false, 0, 0);
+            la.e0 = n_int;
+            la.e1 = c->N;
+            la.push = 1;
+            CU(dgbk::launch_limit(0, c->geo, la, c->stream));
+            ++c->launches;
+            if (last)
+              xch_signal(c, ALL, true, par ^ 1, par);
+            else
+              xch_signal(c, c->send_mask, false, 0, 0);
+          }
         }
       }
     }
     launched += batch;
+    if (X) xch_wait(c, ALL, c->pub_epoch, true, static_cast<int>(launched & 1), static_cast<int>((launched - 1) & 1));
     read_scalars(c);
     const Scalars& h = *c->h_sc;
     if (h.err_key != dgbk::kNoError) {
       const unsigned long long seq = h.err_key >> 38;
+      if (((h.err_key >> 35) & 7) == 7 && seq == 0) throw Fail{DGB_ERR_CUDA, failure_message(c, h.err_key, nullptr, 0.0)};
       const int64_t s_fail = static_cast<int64_t>(seq >> 3);
       const int kst = static_cast<int>(seq & 7);
       const double* in = (kst <= 1) ? c->state[(cur0 + s_fail) & 1].p : c->stage[(kst - 2) & 1].p;
@@ -690,6 +895,66 @@ RunOut run_steps(dgb_ctx* c, const RunSpec& r) {
   return out;
 }
 
+// Partition plan (host only): owned range, per owned element its neighbour ids /
+// side labels / left bits / class, the interior-boundary split and the halo.
+struct PartPlan {
+  int lo = 0, hi = 0;
+  std::vector<int> cls, nb_side, nb_id, left_bits;  // per owned element (index id - lo)
+  std::vector<int> interior, boundary, halo;        // reference ids (ascending)
+  unsigned nb_mask = 0;                             // owners of halo elements
+};
+
+int owner_of(int id, int n, int world) {
+  int r = static_cast<int>((static_cast<long long>(id) * world) / n);
+  r = std::min(world - 1, std::max(0, r));
+  while (r > 0 && id < static_cast<int>(static_cast<long long>(n) * r / world)) --r;
+  while (r < world - 1 && id >= static_cast<int>(static_cast<long long>(n) * (r + 1) / world)) ++r;
+  return r;
+}
+
+void make_plan(const dgb_mesh_view* m, int rank, int world, PartPlan& P) {
+  const int NG = m->n_elements;
+  P.lo = static_cast<int>(static_cast<long long>(NG) * rank / world);
+  P.hi = static_cast<int>(static_cast<long long>(NG) * (rank + 1) / world);
+  const int lo = P.lo, hi = P.hi, N = hi - lo;
+  auto owned = [&](int i) { return i >= lo && i < hi; };
+  P.cls.assign(N, 0);
+  P.nb_side.assign(3 * static_cast<size_t>(N), 0);
+  P.nb_id.assign(3 * static_cast<size_t>(N), 0);
+  P.left_bits.assign(N, 0);
+  for (int l = 0; l < N; ++l) {
+    const int i = lo + l;
+    int key = 0;
+    bool cut = false;
+    for (int q = 0; q < 3; ++q) {
+      const int e = m->elem_edge[3 * i + q];
+      if (e < 0 || e >= m->n_edges) throw Fail{DGB_ERR_MESH, "element edge id out of range"};
+      const bool left = m->edge_left[e] == i;
+      int sd = 0, nb;
+      if (m->edge_right[e] < 0) {
+        nb = m->edge_right[e];
+        if (!left) throw Fail{DGB_ERR_MESH, "boundary edge whose left element is not its owner"};
+      } else {
+        nb = left ? m->edge_right[e] : m->edge_left[e];
+        sd = left ? m->edge_side_right[e] : m->edge_side_left[e];
+        if (!owned(nb)) {
+          cut = true;
+          P.halo.push_back(nb);
+        }
+      }
+      P.nb_side[3 * l + q] = sd;
+      P.nb_id[3 * l + q] = nb;
+      if (left) P.left_bits[l] |= 1 << q;
+      key |= sd << (2 * q);
+    }
+    P.cls[l] = key;
+    (cut ? P.boundary : P.interior).push_back(i);
+  }
+  std::sort(P.halo.begin(), P.halo.end());
+  P.halo.erase(std::unique(P.halo.begin(), P.halo.end()), P.halo.end());
+  for (int h : P.halo) P.nb_mask |= 1u << owner_of(h, NG, world);
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ C ABI
@@ -697,14 +962,23 @@ extern "C" {
 
 int dgb_create(const dgb_mesh_view* m, const dgb_tables_view* t, const dgb_bc_view* bc, double gamma, int device,
                dgb_ctx** out) {
+  return dgb_part_create(m, t, bc, gamma, device, 0, 1, out);
+}
+
+int dgb_part_create(const dgb_mesh_view* m, const dgb_tables_view* t, const dgb_bc_view* bc, double gamma, int device,
+                    int rank, int world, dgb_ctx** out) {
   return guarded([&] {
     if (!m || !t || !out) throw Fail{DGB_ERR_ARG, "null argument"};
     if (t->p < 1 || t->p > 5) throw Fail{DGB_ERR_ARG, "polynomial degree must be in [1,5]"};
+    if (world < 1 || world > dgbk::kMaxRanks || rank < 0 || rank >= world)
+      throw Fail{DGB_ERR_ARG, "rank/world out of range (1 <= world <= 8)"};
     const int np = (t->p + 1) * (t->p + 2) / 2;
     const int nq_expect[5] = {3, 6, 12, 16, 25};
     if (t->n_p != np || t->n_quad != nq_expect[t->p - 1] || t->n_edge_pts != t->p + 1)
       throw Fail{DGB_ERR_ARG, "tables do not match the expected sizes for p = " + std::to_string(t->p)};
     if (m->n_elements <= 0) throw Fail{DGB_ERR_ARG, "empty mesh"};
+    const int NG = m->n_elements;
+    if (NG < world) throw Fail{DGB_ERR_ARG, "fewer elements than ranks"};
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
       throw Fail{DGB_ERR_CUDA, "no CUDA device available (the B200 path has no CPU fallback)"};
@@ -719,18 +993,26 @@ int dgb_create(const dgb_mesh_view* m, const dgb_tables_view* t, const dgb_bc_vi
     c->nq = t->n_quad;
     c->K = t->n_edge_pts;
     c->gamma = gamma;
-    const int N = m->n_elements;
+    c->rank = rank;
+    c->world = world;
+    c->partitioned = world > 1;
+    c->finalized = world == 1;
+    c->n_global = NG;
+    // contiguous ranges of reference ids ("identical partition indexing")
+    const int lo = static_cast<int>(static_cast<long long>(NG) * rank / world);
+    const int hi = static_cast<int>(static_cast<long long>(NG) * (rank + 1) / world);
+    c->lo = lo;
+    c->hi = hi;
+    const int N = hi - lo;  // owned
     c->N = N;
-    c->ld = (N + 31) / 32 * 32;
     c->n_edges = m->n_edges;
     c->n_bnd = m->n_boundary_edges;
-    const int ld = c->ld;
 
     c->vx.assign(m->vx, m->vx + m->n_vertices);
     c->vy.assign(m->vy, m->vy + m->n_vertices);
-    c->det.assign(m->det_jac, m->det_jac + N);
-    c->elem_v.assign(m->elem_v, m->elem_v + 3 * static_cast<size_t>(N));
-    c->elem_edge.assign(m->elem_edge, m->elem_edge + 3 * static_cast<size_t>(N));
+    c->det.assign(m->det_jac, m->det_jac + NG);
+    c->elem_v.assign(m->elem_v, m->elem_v + 3 * static_cast<size_t>(NG));
+    c->elem_edge.assign(m->elem_edge, m->elem_edge + 3 * static_cast<size_t>(NG));
     c->eleft.assign(m->edge_left, m->edge_left + m->n_edges);
     c->eright.assign(m->edge_right, m->edge_right + m->n_edges);
     c->esl.assign(m->edge_side_left, m->edge_side_left + m->n_edges);
@@ -744,60 +1026,66 @@ int dgb_create(const dgb_mesh_view* m, const dgb_tables_view* t, const dgb_bc_vi
     c->t_phm.assign(t->phi_edge_mid, t->phi_edge_mid + 3 * np);
     c->t_xi.assign(t->xi_edge, t->xi_edge + c->K);
 
-    // --- element classes: the neighbour's side label per side; windowed stable
-    // sort so every warp sees one class (warp-uniform neighbour-trace switch)
-    std::vector<int> cls(N);
-    std::vector<int> nb_side(3 * static_cast<size_t>(N)), nb_id(3 * static_cast<size_t>(N)), left_bits(N, 0);
-    for (int i = 0; i < N; ++i) {
-      int key = 0;
-      for (int q = 0; q < 3; ++q) {
-        const int e = m->elem_edge[3 * i + q];
-        if (e < 0 || e >= m->n_edges) throw Fail{DGB_ERR_MESH, "element edge id out of range"};
-        const bool left = m->edge_left[e] == i;
-        int s = 0, nb;
-        if (m->edge_right[e] < 0) {
-          nb = m->edge_right[e];
-          if (!left) throw Fail{DGB_ERR_MESH, "boundary edge whose left element is not its owner"};
-        } else {
-          nb = left ? m->edge_right[e] : m->edge_left[e];
-          s = left ? m->edge_side_right[e] : m->edge_side_left[e];
-        }
-        nb_side[3 * i + q] = s;
-        nb_id[3 * i + q] = nb;
-        if (left) left_bits[i] |= 1 << q;
-        key |= s << (2 * q);
+    PartPlan P;
+    make_plan(m, rank, world, P);
+    std::vector<int>& cls = P.cls;
+    std::vector<int>& nb_side = P.nb_side;
+    std::vector<int>& nb_id = P.nb_id;
+    std::vector<int>& left_bits = P.left_bits;
+    std::vector<int>& interior = P.interior;
+    std::vector<int>& boundary = P.boundary;
+    std::vector<int>& halo = P.halo;
+    c->nb_mask = P.nb_mask;
+    c->n_int = static_cast<int>(interior.size());
+    c->n_halo = static_cast<int>(halo.size());
+    c->halo_gid = halo;
+    c->ld = (N + c->n_halo + 31) / 32 * 32;
+    const int ld = c->ld;
+
+    // --- device order: interior, then boundary elements, each windowed-class
+    // sorted so every warp sees one neighbour-side class (warp-uniform trace switch);
+    // halo columns follow the owned ones
+    auto window_sort = [&](std::vector<int>& v) {
+      for (size_t w0 = 0; w0 < v.size(); w0 += kWindow) {
+        const size_t w1 = std::min(v.size(), w0 + kWindow);
+        std::stable_sort(v.begin() + w0, v.begin() + w1, [&](int a, int b) { return cls[a - lo] < cls[b - lo]; });
       }
-      cls[i] = key;
-    }
-    c->ref_of.resize(N);
-    for (int i = 0; i < N; ++i) c->ref_of[i] = i;
-    for (int w0 = 0; w0 < N; w0 += kWindow) {
-      const int w1 = std::min(N, w0 + kWindow);
-      std::stable_sort(c->ref_of.begin() + w0, c->ref_of.begin() + w1,
-                       [&](int a, int b) { return cls[a] < cls[b]; });
-    }
-    c->dev_of.resize(N);
-    for (int d = 0; d < N; ++d) c->dev_of[c->ref_of[d]] = d;
+    };
+    window_sort(interior);
+    window_sort(boundary);
+    c->ref_of.clear();
+    c->ref_of.insert(c->ref_of.end(), interior.begin(), interior.end());
+    c->ref_of.insert(c->ref_of.end(), boundary.begin(), boundary.end());
+    c->ref_of.insert(c->ref_of.end(), halo.begin(), halo.end());
+    c->col_of.assign(NG, -1);
+    for (size_t d = 0; d < c->ref_of.size(); ++d) c->col_of[c->ref_of[d]] = static_cast<int>(d);
 
     std::vector<double> tau(4 * static_cast<size_t>(ld), 0.0), inv_det(ld, 1.0), inr(ld, 1.0);
     std::vector<int> nbr(3 * static_cast<size_t>(ld), -4), eid(3 * static_cast<size_t>(ld), 0), info(ld, 0),
-        ref_id(ld, 0);
+        ref_id(ld, 0), cmp(ld, 0);
     for (int d = 0; d < N; ++d) {
       const int i = c->ref_of[d];
+      const int l = i - lo;
       for (int k = 0; k < 4; ++k) tau[static_cast<size_t>(k) * ld + d] = m->tau[4 * static_cast<size_t>(i) + k];
       inv_det[d] = 1.0 / m->det_jac[i];
       inr[d] = m->inradius[i];
       int bits = 0;
       for (int q = 0; q < 3; ++q) {
-        const int nb = nb_id[3 * i + q];
-        nbr[static_cast<size_t>(q) * ld + d] = nb >= 0 ? c->dev_of[nb] : nb;
+        const int nb = nb_id[3 * l + q];
+        nbr[static_cast<size_t>(q) * ld + d] = nb >= 0 ? c->col_of[nb] : nb;
         eid[static_cast<size_t>(q) * ld + d] = m->elem_edge[3 * i + q];
-        bits |= nb_side[3 * i + q] << (2 * q);
-        if (left_bits[i] & (1 << q)) bits |= 1 << (6 + q);
+        bits |= nb_side[3 * l + q] << (2 * q);
+        if (left_bits[l] & (1 << q)) bits |= 1 << (6 + q);
       }
       info[d] = bits;
       ref_id[d] = i;
+      cmp[d] = l;
     }
+    for (int h = 0; h < c->n_halo; ++h) {
+      ref_id[N + h] = halo[h];
+      cmp[N + h] = N + h;
+    }
+    c->sends.assign(world, {});
     c->d_tau.upload(tau.data(), tau.size(), c->stream);
     c->d_inv_det.upload(inv_det.data(), ld, c->stream);
     c->d_inradius.upload(inr.data(), ld, c->stream);
@@ -805,6 +1093,7 @@ int dgb_create(const dgb_mesh_view* m, const dgb_tables_view* t, const dgb_bc_vi
     c->d_eid.upload(eid.data(), eid.size(), c->stream);
     c->d_info.upload(info.data(), ld, c->stream);
     c->d_ref_id.upload(ref_id.data(), ld, c->stream);
+    c->d_cmp.upload(cmp.data(), ld, c->stream);
     c->d_enx.upload(m->edge_nx, m->n_edges, c->stream);
     c->d_eny.upload(m->edge_ny, m->n_edges, c->stream);
     c->d_eh.upload(m->edge_half_length, m->n_edges, c->stream);
@@ -854,6 +1143,9 @@ int dgb_create(const dgb_mesh_view* m, const dgb_tables_view* t, const dgb_bc_vi
     Geo& g = c->geo;
     g.N = N;
     g.ld = ld;
+    g.send_begin = N;  // no sends until dgb_part_finalize
+    g.send_ptr = nullptr;
+    g.send_ent = nullptr;
     g.tau = c->d_tau.p;
     g.inv_det = c->d_inv_det.p;
     g.inradius = c->d_inradius.p;
@@ -924,6 +1216,19 @@ int dgb_create(const dgb_mesh_view* m, const dgb_tables_view* t, const dgb_bc_vi
     CU(cudaMallocHost(&c->h_red, sizeof(unsigned long long)));
     c->state[0].alloc(c->coeff_count());
     CU(cudaMemsetAsync(c->state[0].p, 0, c->coeff_count() * sizeof(double), c->stream));
+    if (c->partitioned) {
+      // the peers address our rotating buffers directly, so they exist from the start
+      c->state[1].alloc(c->coeff_count());
+      c->stage[0].alloc(c->coeff_count());
+      c->stage[1].alloc(c->coeff_count());
+      for (DevBuf<double>* b : {&c->state[1], &c->stage[0], &c->stage[1]})
+        CU(cudaMemsetAsync(b->p, 0, c->coeff_count() * sizeof(double), c->stream));
+      const size_t nx = dgbk::kMaxRanks + 2 * dgbk::kMaxRanks * 4;
+      CU(cudaMalloc(&c->d_xch, nx * sizeof(unsigned long long)));
+      CU(cudaMemsetAsync(c->d_xch, 0, nx * sizeof(unsigned long long), c->stream));
+      CU(cudaMalloc(&c->d_peers, sizeof(dgbk::PeerTab)));
+      CU(cudaMemsetAsync(c->d_peers, 0, sizeof(dgbk::PeerTab), c->stream));
+    }
     reset_scalars(c.get(), 0.0);
     sync(c.get());
     *out = c.release();
@@ -946,6 +1251,9 @@ int dgb_destroy(dgb_ctx* c) {
   if (c->h_sc) cudaFreeHost(c->h_sc);
   if (c->d_red) cudaFree(c->d_red);
   if (c->h_red) cudaFreeHost(c->h_red);
+  if (c->d_xch) cudaFree(c->d_xch);
+  if (c->d_peers) cudaFree(c->d_peers);
+  for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
   const bool own = c->own_stream;
   cudaStream_t s = c->stream;
   delete c;
@@ -1035,6 +1343,7 @@ int dgb_eval_surface_pass(dgb_ctx* c, int in_slot, double t) {
 int dgb_download_surface(dgb_ctx* c, double* left, double* right) {
   return guarded([&] {
     set_device(c);
+    if (c->partitioned) throw Fail{DGB_ERR_ARG, "surface slot buffers are whole-mesh only"};
     const size_t per = static_cast<size_t>(4) * c->np * c->N;
     std::vector<double> all(3 * per);
     if (!c->slots.p) throw Fail{DGB_ERR_ARG, "no surface pass has been evaluated"};
@@ -1059,6 +1368,7 @@ int dgb_download_surface(dgb_ctx* c, double* left, double* right) {
 int dgb_upload_surface(dgb_ctx* c, const double* left, const double* right) {
   return guarded([&] {
     set_device(c);
+    if (c->partitioned) throw Fail{DGB_ERR_ARG, "surface slot buffers are whole-mesh only"};
     const size_t per = static_cast<size_t>(4) * c->np * c->N;
     std::vector<double> all(3 * per);
     const int N = c->N, np = c->np;
@@ -1114,6 +1424,8 @@ int dgb_limit(dgb_ctx* c, int slot) {
     la.c = slot_ptr(c, slot);
     la.u = la.c;
     la.sc = c->d_sc;
+    la.e0 = 0;
+    la.e1 = c->N;
     {
       Timed tm(c, 3);
       CU(dgbk::launch_limit(0, c->geo, la, c->stream));
@@ -1247,8 +1559,8 @@ int dgb_total_mass(dgb_ctx* c, int slot, double* mass) {
     std::vector<double> row(c->N);
     download_dev(c, slot_ptr(c, slot), 1, row.data());
     const double inv_sqrt2 = 1.0 / std::sqrt(2.0);
-    double s = 0.0;
-    for (int i = 0; i < c->N; ++i) s += c->det[i] * row[i] * inv_sqrt2;
+    double s = 0.0;  // partition: this rank's partial sum, reference order (ranks add in rank order)
+    for (int i = 0; i < c->N; ++i) s += c->det[c->lo + i] * row[i] * inv_sqrt2;
     *mass = s;
     return DGB_OK;
   });
@@ -1331,6 +1643,170 @@ int dgb_fp64_peak(int device, double* tflops) {
     *tflops = 2.0 * 8.0 * iters * static_cast<double>(blocks) * threads / (best * 1e-3) / 1e12;
     return DGB_OK;
   });
+}
+
+// ------------------------------------------------------------------ partitions (multi-GPU)
+int dgb_part_get_info(dgb_ctx* c, dgb_part_info* out) {
+  if (!c || !out) return DGB_ERR_ARG;
+  out->rank = c->rank;
+  out->world = c->world;
+  out->lo = c->lo;
+  out->hi = c->hi;
+  out->n_owned = c->N;
+  out->n_halo = c->n_halo;
+  out->n_interior = c->partitioned ? c->n_int : c->N;
+  out->ld = c->ld;
+  out->neighbor_mask = c->nb_mask;
+  return DGB_OK;
+}
+
+int dgb_part_plan(const dgb_mesh_view* m, int rank, int world, dgb_part_info* info, int32_t* halo_ids,
+                  int32_t* boundary_ids) {
+  return guarded([&] {
+    if (!m || !info || world < 1 || world > dgbk::kMaxRanks || rank < 0 || rank >= world || m->n_elements < world)
+      throw Fail{DGB_ERR_ARG, "bad partition arguments"};
+    PartPlan P;
+    make_plan(m, rank, world, P);
+    info->rank = rank;
+    info->world = world;
+    info->lo = P.lo;
+    info->hi = P.hi;
+    info->n_owned = P.hi - P.lo;
+    info->n_halo = static_cast<int32_t>(P.halo.size());
+    info->n_interior = static_cast<int32_t>(P.interior.size());
+    info->ld = (info->n_owned + info->n_halo + 31) / 32 * 32;
+    info->neighbor_mask = P.nb_mask;
+    if (halo_ids) std::copy(P.halo.begin(), P.halo.end(), halo_ids);
+    if (boundary_ids) std::copy(P.boundary.begin(), P.boundary.end(), boundary_ids);
+    return DGB_OK;
+  });
+}
+
+int dgb_part_halo_ids(dgb_ctx* c, int32_t* gids, int32_t* cols) {
+  return guarded([&] {
+    for (int h = 0; h < c->n_halo; ++h) {
+      if (gids) gids[h] = c->halo_gid[h];
+      if (cols) cols[h] = c->N + h;
+    }
+    return DGB_OK;
+  });
+}
+
+int dgb_part_local_ids(dgb_ctx* c, int32_t* gids) {
+  return guarded([&] {
+    for (int l = 0; l < c->N; ++l) gids[l] = c->lo + l;
+    for (int h = 0; h < c->n_halo; ++h) gids[c->N + h] = c->halo_gid[h];
+    return DGB_OK;
+  });
+}
+
+int dgb_part_peer_view(dgb_ctx* c, dgb_peer_view* out) {
+  return guarded([&] {
+    if (!c->partitioned) throw Fail{DGB_ERR_ARG, "not a partitioned context"};
+    out->buf[0] = c->state[0].p;
+    out->buf[1] = c->state[1].p;
+    out->buf[2] = c->stage[0].p;
+    out->buf[3] = c->stage[1].p;
+    out->flags = c->d_xch;
+    out->scal = c->d_xch + dgbk::kMaxRanks;
+    out->ld = c->ld;
+    return DGB_OK;
+  });
+}
+
+int dgb_part_attach_peer(dgb_ctx* c, int peer, const dgb_peer_view* v) {
+  return guarded([&] {
+    if (!c->partitioned || peer < 0 || peer >= c->world || peer == c->rank || !v)
+      throw Fail{DGB_ERR_ARG, "bad peer"};
+    for (int k = 0; k < 4; ++k) c->h_peers.buf[peer][k] = static_cast<double*>(v->buf[k]);
+    c->h_peers.ld[peer] = v->ld;
+    c->h_peers.flag[peer] = static_cast<unsigned long long*>(v->flags);
+    c->h_peers.scal[peer] = static_cast<unsigned long long*>(v->scal);
+    return DGB_OK;
+  });
+}
+
+int dgb_part_ipc_export(dgb_ctx* c, void* handles) {
+  return guarded([&] {
+    if (!c->partitioned) throw Fail{DGB_ERR_ARG, "not a partitioned context"};
+    set_device(c);
+    auto* h = static_cast<cudaIpcMemHandle_t*>(handles);
+    void* ptrs[5] = {c->state[0].p, c->state[1].p, c->stage[0].p, c->stage[1].p, c->d_xch};
+    for (int k = 0; k < 5; ++k) CU(cudaIpcGetMemHandle(&h[k], ptrs[k]));
+    return DGB_OK;
+  });
+}
+
+int dgb_part_attach_peer_ipc(dgb_ctx* c, int peer, const void* handles, int32_t peer_ld) {
+  return guarded([&] {
+    if (!c->partitioned || peer < 0 || peer >= c->world || peer == c->rank) throw Fail{DGB_ERR_ARG, "bad peer"};
+    set_device(c);
+    const auto* h = static_cast<const cudaIpcMemHandle_t*>(handles);
+    void* ptrs[5];
+    for (int k = 0; k < 5; ++k) {
+      CU(cudaIpcOpenMemHandle(&ptrs[k], h[k], cudaIpcMemLazyEnablePeerAccess));
+      c->ipc_opened.push_back(ptrs[k]);
+    }
+    dgb_peer_view v{};
+    for (int k = 0; k < 4; ++k) v.buf[k] = ptrs[k];
+    v.flags = ptrs[4];
+    v.scal = static_cast<unsigned long long*>(ptrs[4]) + dgbk::kMaxRanks;
+    v.ld = peer_ld;
+    return dgb_part_attach_peer(c, peer, &v);
+  });
+}
+
+int dgb_part_set_sends(dgb_ctx* c, int peer, int64_t n, const int32_t* gids, const int32_t* peer_cols) {
+  return guarded([&] {
+    if (!c->partitioned || peer < 0 || peer >= c->world || peer == c->rank) throw Fail{DGB_ERR_ARG, "bad peer"};
+    auto& v = c->sends[peer];
+    v.clear();
+    for (int64_t k = 0; k < n; ++k) {
+      const int g = gids[k];
+      if (g < c->lo || g >= c->hi) throw Fail{DGB_ERR_ARG, "send element not owned by this rank"};
+      if (c->col_of[g] < c->n_int) throw Fail{DGB_ERR_ARG, "send element is not on the partition boundary"};
+      v.emplace_back(g, peer_cols[k]);
+    }
+    c->finalized = false;
+    return DGB_OK;
+  });
+}
+
+int dgb_part_finalize(dgb_ctx* c) {
+  return guarded([&] {
+    if (!c->partitioned) return DGB_OK;
+    set_device(c);
+    for (int r = 0; r < c->world; ++r)
+      if (r != c->rank && (!c->h_peers.flag[r] || !c->h_peers.buf[r][0]))
+        throw Fail{DGB_ERR_ARG, "peer " + std::to_string(r) + " not attached"};
+    const int nb = c->N - c->n_int;
+    std::vector<int> cnt(nb + 1, 0);
+    c->send_mask = 0;
+    for (int r = 0; r < c->world; ++r) {
+      if (!c->sends[r].empty()) c->send_mask |= 1u << r;
+      for (auto& e : c->sends[r]) ++cnt[c->col_of[e.first] - c->n_int + 1];
+    }
+    for (int d = 0; d < nb; ++d) cnt[d + 1] += cnt[d];
+    std::vector<int2> ent(std::max(cnt[nb], 1));
+    std::vector<int> fill(cnt.begin(), cnt.end() - 1);
+    for (int r = 0; r < c->world; ++r)
+      for (auto& e : c->sends[r]) ent[fill[c->col_of[e.first] - c->n_int]++] = make_int2(r, e.second);
+    c->d_send_ptr.upload(cnt.data(), cnt.size(), c->stream);
+    c->d_send_ent.upload(ent.data(), ent.size(), c->stream);
+    c->geo.send_ptr = c->d_send_ptr.p;
+    c->geo.send_ent = c->d_send_ent.p;
+    c->geo.send_begin = c->n_int;
+    CU(cudaMemcpyAsync(c->d_peers, &c->h_peers, sizeof(dgbk::PeerTab), cudaMemcpyHostToDevice, c->stream));
+    sync(c);
+    c->finalized = true;
+    return DGB_OK;
+  });
+}
+
+int dgb_part_set_timeout(dgb_ctx* c, double seconds) {
+  if (!c || !(seconds > 0)) return DGB_ERR_ARG;
+  c->timeout_s = seconds;
+  return DGB_OK;
 }
 
 int dgb_stage_kernel_ms(dgb_ctx* c, double* ms, int64_t* launches) {

@@ -558,26 +558,32 @@ class SolverContext:
                 wall[mask] = np.asarray(bc.wall_normal(xy[mask]), np.float64).reshape(-1, 2)
         return dirichlet, wall
 
+    def _bc_view(self):
+        """dgb_bc_view of the boundary conditions (arrays kept alive on self)."""
+        dirichlet, wall = self._bc_tables(0.0)
+        v = L.BcView()
+        for m in range(4):
+            v.inflow_state[m] = float(self.bc.inflow_state[m])
+        if dirichlet is not None:
+            dirichlet = np.ascontiguousarray(dirichlet)
+            v.dirichlet_state = dptr(dirichlet)
+        if wall is not None:
+            wall = np.ascontiguousarray(wall)
+            v.wall_normal = dptr(wall)
+        if self.bc.shock is not None:
+            s = self.bc.shock
+            v.has_shock = 1
+            v.shock_x0, v.shock_angle_deg, v.shock_speed = s.x0, s.angle_deg, s.speed
+            for m in range(4):
+                v.shock_post[m] = float(s.post[m])
+                v.shock_pre[m] = float(s.pre[m])
+        self._keep = [dirichlet, wall]
+        return v
+
     @property
     def handle(self):
         if self._ctx is None:
-            dirichlet, wall = self._bc_tables(0.0)
-            v = L.BcView()
-            for m in range(4):
-                v.inflow_state[m] = float(self.bc.inflow_state[m])
-            if dirichlet is not None:
-                dirichlet = np.ascontiguousarray(dirichlet)
-                v.dirichlet_state = dptr(dirichlet)
-            if wall is not None:
-                wall = np.ascontiguousarray(wall)
-                v.wall_normal = dptr(wall)
-            if self.bc.shock is not None:
-                s = self.bc.shock
-                v.has_shock = 1
-                v.shock_x0, v.shock_angle_deg, v.shock_speed = s.x0, s.angle_deg, s.speed
-                for m in range(4):
-                    v.shock_post[m] = float(s.post[m])
-                    v.shock_pre[m] = float(s.pre[m])
+            v = self._bc_view()
             h = C.c_void_p()
             _check(lib.dgb_create(C.byref(self.mesh.view), C.byref(self.tables.view), C.byref(v),
                                   self.gas.gamma, self.device, C.byref(h)))
