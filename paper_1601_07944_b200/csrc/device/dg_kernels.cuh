@@ -111,6 +111,8 @@ struct Geo {
   const int* __restrict__ send_ptr;
   const int2* __restrict__ send_ent;
   int send_begin;
+  // basis tables in DMMA fragment order (element_mma.cuh), p >= 3
+  const double* __restrict__ mma_tab;
 };
 
 // Modes of the fused element kernel.

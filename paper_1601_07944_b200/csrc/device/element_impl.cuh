@@ -44,6 +44,31 @@ __device__ __forceinline__ void gather_state(const double (&own)[MG], double (&U
   }
 }
 
+// Branch-free reciprocal / square root for the pointwise physics: the MUFU seed
+// (rcp/rsqrt.approx.ftz.f64) refined by Newton steps to within ~1 ulp.  The IEEE
+// `1.0 / x` and `sqrt(x)` carry a slow-path branch each and cost 8.5 / 14 DFMA
+// slots (measured, profiles/r01_dmma_peak.txt); the flux evaluates 2 of each per
+// edge point.  Arguments are positive whenever the state is admissible (the only
+// case whose result is used); ~1 ulp differences are far inside the 1e-12 bar.
+__device__ __forceinline__ double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+__device__ __forceinline__ double sqrt_nr(double a) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
+  const double h = 0.5 * a;
+  y = y * fma(-h * y, y, 1.5);
+  y = y * fma(-h * y, y, 1.5);
+  const double s = a * y;
+  return fma(0.5 * y, fma(-s, s, a), s);
+}
+
 struct Prim {
   double inv, vx, vy, p;
 };
@@ -51,7 +76,7 @@ struct Prim {
 // EOS (euler.hpp:29-31) through one reciprocal per state.
 __device__ __forceinline__ Prim primitives(const double (&U)[4], double g1) {
   Prim w;
-  w.inv = 1.0 / U[0];
+  w.inv = rcp_nr(U[0]);
   w.vx = U[1] * w.inv;
   w.vy = U[2] * w.inv;
   w.p = g1 * (U[3] - 0.5 * (U[1] * w.vx + U[2] * w.vy));
@@ -77,8 +102,8 @@ __device__ __forceinline__ void euler_flux(const double (&U)[4], const Prim& w, 
 // precomputed primitives; evaluated variable by variable to keep few values live.
 __device__ __forceinline__ void llf_flux(const double (&UL)[4], const Prim& wl, const double (&UR)[4], const Prim& wr,
                                          double nx, double ny, double gamma, double (&fn)[4]) {
-  const double sl = fabs(wl.vx * nx + wl.vy * ny) + sqrt(gamma * wl.p * wl.inv);
-  const double sr = fabs(wr.vx * nx + wr.vy * ny) + sqrt(gamma * wr.p * wr.inv);
+  const double sl = fabs(wl.vx * nx + wl.vy * ny) + sqrt_nr(gamma * wl.p * wl.inv);
+  const double sr = fabs(wr.vx * nx + wr.vy * ny) + sqrt_nr(gamma * wr.p * wr.inv);
   const double hs = 0.5 * fmax(sl, sr);
   const double epl = UL[3] + wl.p, epr = UR[3] + wr.p;
   // F1 = (mx, mx vx + p, my vx, vx (E+p)), F2 = (my, mx vy, my vy + p, vy (E+p))

@@ -1,0 +1,571 @@
+// FP64 tensor-core (DMMA) variant of the fused element kernel, used for p >= 3.
+//
+// Every contraction of the modal-DG stage is a small GEMM over a tile of 8
+// elements (one warp):
+//
+//   interior interpolation   U_m[e][k]  = sum_j C_m[e][j] phi[k][j]          (8 x Q  <- 8 x Np . Np x Q)
+//   volume projection        R_m[e][j] += sum_k Fr_m[e][k] w dphi/dr[k][j]   (8 x Np <- 8 x Q  . Q  x Np)
+//                                        + Fs_m[e][k] w dphi/ds[k][j]
+//   own / neighbour traces   T_m[e][k]  = sum_j C_m[e][j] phi_q[k][j]        (8 x K  <- 8 x Np . Np x K)
+//   surface projection       R_m[e][j] -= sum_k Fn_m[e][k] phi_q[k][j]       (8 x Np <- 8 x K  . K  x Np)
+//
+// issued as mma.sync.m8n8k4 f64 (DMMA.8x8x4 on sm_100a: 256 FMAs per warp
+// instruction, the same FP64 pipe as DFMA but an eighth of the issue slots and
+// no register dependency chains).  Rows are the 8 elements of the warp, one
+// accumulator set per conserved variable.  Lane (g, t) = (lane / 4, lane % 4)
+// holds A[g][t], B[t][g] and D[g][2t], D[g][2t+1], so after an interpolation
+// the lane owns element g at points 2t, 2t+1 of every 8-point tile — exactly
+// what it needs to evaluate the nonlinear flux, and exactly the A fragment of
+// the following projection once the k index of that projection is permuted
+// (k-step (tile n, i) takes point 8n + 2t + i in slot t).  So no data moves
+// between the contractions and the pointwise physics: the basis tables are
+// stored in shared memory in that permuted fragment order (one LDS per DMMA).
+//
+// Both sides of an edge still evaluate the same numerical flux from bit-identical
+// traces: the neighbour's trace is the same DMMA (same A row = the neighbour's
+// coefficients, same B column = its side's basis row, same k order) as the one
+// the neighbour performs for its own trace, and the flux is evaluated in the
+// edge's canonical left -> right orientation.
+#pragma once
+
+#include "element_impl.cuh"
+
+namespace dgbk {
+
+template <int P>
+struct MmaDim {
+  static constexpr int NP = Dim<P>::NP, NQ = Dim<P>::NQ, K = Dim<P>::K;
+  static constexpr int KS = (NP + 3) / 4;  // k-steps over modes
+  static constexpr int NT = (NQ + 7) / 8;  // 8-point tiles of interior points
+  static constexpr int JT = (NP + 7) / 8;  // 8-mode tiles of the projections' output
+  // shared-memory table layout (doubles), fragment order, 32 values per fragment
+  static constexpr int kPhi = 0;                            // [KS][NT][32]
+  static constexpr int kDr = kPhi + KS * NT * 32;           // [NT][2][JT][32]
+  static constexpr int kDs = kDr + NT * 2 * JT * 32;        // [NT][2][JT][32]
+  static constexpr int kPhe = kDs + NT * 2 * JT * 32;       // [3][KS][32] own trace of side q
+  static constexpr int kPheR = kPhe + 3 * KS * 32;          // [3][KS][32] reversed trace of side s
+  static constexpr int kPheP = kPheR + 3 * KS * 32;         // [3][2][JT][32] surface projection
+  static constexpr int kPhm = kPheP + 3 * 2 * JT * 32;      // [3][JT*8] midpoint rows (zero padded)
+  static constexpr int kWe = kPhm + 3 * JT * 8;             // [8] edge weights (zero padded)
+  static constexpr int kSize = kWe + 8;
+  // per-warp staging after the tables: own [4 KS][32] + neighbour [2][4 KS][32]
+  static constexpr int kWarpBuf = 3 * 4 * KS * 32;
+};
+
+// volatile: a non-volatile asm may be duplicated into both arms of a per-lane
+// select (e.g. `a = cond ? load : 0`), giving two predicated DMMAs that the
+// warp executes divergently — which deadlocks the .aligned warp-wide MMA.
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(d[0]), "+d"(d[1])
+      : "d"(a), "d"(b));
+}
+
+constexpr int kMmaWarps = 4;  // warps per block of the DMMA kernel
+
+// Stage prologue shared with element_body: step bookkeeping, stop rules, dt.
+// Returns false when the step must not run (a stop rule fired).
+__device__ __forceinline__ bool mma_prologue(const StageArgs& a, Scalars* sc, double& t0, double& dt) {
+  const int par = a.step & 1;
+  t0 = sc->t[par];
+  if (a.first) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      if (a.hist && a.step > 0) a.hist[a.step - 1] = bits_to_double(sc->resid[par ^ 1]);
+    }
+    bool stop = false;
+    if (a.stop_at_t_end && !(t0 < a.t_end)) stop = true;
+    if (a.stop_steady && a.step > 0 && bits_to_double(sc->resid[par ^ 1]) <= a.tol) stop = true;
+    if (stop) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        sc->halt = 1;
+        sc->halt_step = a.step;
+      }
+      return false;
+    }
+  }
+  if (a.dt_mode == 0) {
+    dt = a.dt_host;
+  } else {
+    dt = a.cfl * bits_to_double(sc->dtmin[par]);
+    if (a.clip_t_end && t0 + dt > a.t_end) dt = a.t_end - t0;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (a.first) {
+      sc->dtmin[par ^ 1] = 0x7ff0000000000000ull;  // +inf
+      sc->resid[par] = 0ull;
+      sc->dt_used[par] = dt;
+    }
+    if (a.last) sc->t[par ^ 1] = t0 + dt;
+  }
+  return true;
+}
+
+// cp.async of one double into shared memory (zero-filled when !pred); lane-private
+// destinations, so the issuing lane's wait_group is the only synchronisation needed.
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool pred) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sa), "l"(src), "r"(pred ? 8 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// A-fragment copy of one element column (4 variables x Np modes) into a lane-private
+// slot array [4 * KS][32] of shared memory.
+template <int NP, int KS>
+__device__ __forceinline__ void fetch_frag(double* __restrict__ slot, const double* __restrict__ base, long long ld,
+                                           int col, bool ok, int lane, int t) {
+#pragma unroll
+  for (int m = 0; m < 4; ++m)
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int j = 4 * ks + t;
+      const bool p = ok && j < NP;
+      cp_async8(slot + (m * KS + ks) * 32 + lane, p ? base + (static_cast<long long>(m) * NP + j) * ld + col : base, p);
+    }
+}
+
+template <int P, int MODE>
+__device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo, const StageArgs& a,
+                                                 double* __restrict__ smem) {
+  using D = MmaDim<P>;
+  constexpr int NP = D::NP, NQ = D::NQ, K = D::K, KS = D::KS, NT = D::NT, JT = D::JT;
+  constexpr int FR = 4 * KS * 32;  // doubles of one fragment buffer
+  const long long ld = geo.ld;
+  const double gamma = geo.gamma, g1 = gamma - 1.0;
+  Scalars* sc = a.sc;
+
+  __shared__ int s_stop;
+  if (threadIdx.x == 0) s_stop = (sc->err_key != kNoError || sc->halt) ? 1 : 0;
+  // basis tables -> shared memory (fragment order, prepared on the host)
+  for (int i = threadIdx.x; i < D::kSize; i += blockDim.x) smem[i] = __ldg(geo.mma_tab + i);
+  __syncthreads();
+  if (s_stop) return;
+
+  double t0 = a.t_host, dt = 0.0;
+  if constexpr (MODE == kModeStage) {
+    if (!mma_prologue(a, sc, t0, dt)) return;
+  }
+  const double tstage = (MODE == kModeStage) ? fma(a.tcoef, dt, t0) : t0;
+
+  const int lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wib = threadIdx.x >> 5;
+  const int warp = blockIdx.x * (blockDim.x >> 5) + wib;
+  const int nwarps = gridDim.x * (blockDim.x >> 5);
+  const int ntiles = (a.e1 - a.e0 + 7) >> 3;
+  // per-warp staging: own coefficients of the tile, neighbour coefficients (2 buffers)
+  double* __restrict__ w_own = smem + D::kSize + wib * 3 * FR;
+  double* __restrict__ w_nbr = w_own + FR;  // [2][FR]
+
+  double lam_min = __longlong_as_double(0x7ff0000000000000ll);
+  double res_max = 0.0;
+
+  auto elem_of = [&](int tile, bool& ok) {
+    int e = a.e0 + tile * 8 + g;
+    ok = tile < ntiles && e < a.e1;
+    return ok ? e : a.e1 - 1;
+  };
+  auto nbr_of = [&](int e, int q) { return __ldg(geo.nbr + q * ld + e); };
+
+  // pipeline prologue: own coefficients and side-0 neighbours of the first tile
+  int sbuf = 0;  // neighbour buffer of the side being processed
+  int nbq[3] = {-4, -4, -4};  // neighbour columns of the current tile's element
+  {
+    bool ok;
+    const int e = elem_of(warp, ok);
+    fetch_frag<NP, KS>(w_own, a.in, ld, e, ok, lane, t);
+    cp_async_commit();
+    if constexpr (MODE != kModeVolume) {
+#pragma unroll
+      for (int q = 0; q < 3; ++q) nbq[q] = nbr_of(e, q);
+      fetch_frag<NP, KS>(w_nbr, a.in, ld, nbq[0], ok && nbq[0] >= 0, lane, t);
+    }
+    cp_async_commit();
+  }
+
+  for (int tile = warp; tile < ntiles; tile += nwarps) {
+    bool valid;
+    const int e = elem_of(tile, valid);
+    bool nvalid;
+    const int e_next = elem_of(tile + nwarps, nvalid);
+    // side data of this tile and the next tile's neighbour columns, issued early so
+    // they land during the volume integral
+    int nbn[3] = {-4, -4, -4}, edq[3] = {0, 0, 0}, inf = 0;
+    if constexpr (MODE != kModeVolume) {
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        nbn[q] = nbr_of(e_next, q);
+        edq[q] = __ldg(geo.eid + q * ld + e);
+      }
+      inf = __ldg(geo.info + e);
+    }
+    cp_async_wait<1>();  // own coefficients of this tile (the newest group is side-0 neighbours)
+    __syncwarp();
+
+    double R[4][JT][2];
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+#pragma unroll
+      for (int jt = 0; jt < JT; ++jt) R[m][jt][0] = R[m][jt][1] = 0.0;
+
+    // ------------------------------------------------------------ volume
+    if constexpr (MODE != kModeSurface) {
+      const double ta = __ldg(geo.tau + e), tb = __ldg(geo.tau + ld + e);
+      const double tc = __ldg(geo.tau + 2 * ld + e), td = __ldg(geo.tau + 3 * ld + e);
+      double U[2][4][2];
+      auto interp = [&](double(&u)[4][2], int nt) {
+#pragma unroll
+        for (int m = 0; m < 4; ++m) u[m][0] = u[m][1] = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+          const double b = smem[D::kPhi + (ks * NT + nt) * 32 + lane];
+#pragma unroll
+          for (int m = 0; m < 4; ++m) dmma(u[m], w_own[(m * KS + ks) * 32 + lane], b);
+        }
+      };
+      interp(U[0], 0);
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        // software pipeline: the next tile of points is interpolated while this
+        // tile's fluxes are evaluated
+        if (nt + 1 < NT) interp(U[(nt + 1) & 1], nt + 1);
+        double fr[4][2], fs[4][2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int k = 8 * nt + 2 * t + i;
+          double v[4] = {U[nt & 1][0][i], U[nt & 1][1][i], U[nt & 1][2][i], U[nt & 1][3][i]};
+          Prim w = primitives(v, g1);
+          const bool bad = !admissible(v, w);
+          if (bad && valid && k < NQ) record_error(sc, err_key(a.seq, kPassVolume, __ldg(geo.ref_id + e), k));
+          if (bad) {  // placeholder (solver.cpp:129-132)
+            v[0] = 1.0; v[1] = 0.0; v[2] = 0.0; v[3] = 2.5;
+            w.inv = 1.0; w.vx = 0.0; w.vy = 0.0; w.p = 1.0;
+          }
+          double f1[4], f2[4];
+          euler_flux(v, w, f1, f2);
+          const double live = (k < NQ) ? 1.0 : 0.0;  // padded points contribute nothing
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            fr[m][i] = live * (ta * f1[m] + tb * f2[m]);  // contravariant flux along r
+            fs[m][i] = live * (tc * f1[m] + td * f2[m]);  // along s
+          }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int jt = 0; jt < JT; ++jt) {
+            const double br = smem[D::kDr + ((nt * 2 + i) * JT + jt) * 32 + lane];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) dmma(R[m][jt], fr[m][i], br);
+          }
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int jt = 0; jt < JT; ++jt) {
+            const double bs = smem[D::kDs + ((nt * 2 + i) * JT + jt) * 32 + lane];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) dmma(R[m][jt], fs[m][i], bs);
+          }
+      }
+    }
+
+    // ------------------------------------------------------------ surface
+    if constexpr (MODE != kModeVolume) {
+      // own traces of the three sides while the own coefficients are staged
+      double Tw[3][4][2];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+#pragma unroll
+        for (int m = 0; m < 4; ++m) Tw[q][m][0] = Tw[q][m][1] = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+          const double b = smem[D::kPhe + (q * KS + ks) * 32 + lane];
+#pragma unroll
+          for (int m = 0; m < 4; ++m) dmma(Tw[q][m], w_own[(m * KS + ks) * 32 + lane], b);
+        }
+      }
+      __syncwarp();
+      // the own buffer is free: prefetch the next tile's coefficients
+      fetch_frag<NP, KS>(w_own, a.in, ld, e_next, nvalid, lane, t);
+      cp_async_commit();
+
+      double enx[3], eny[3], eh[3];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        enx[q] = __ldg(geo.enx + edq[q]);
+        eny[q] = __ldg(geo.eny + edq[q]);
+        eh[q] = __ldg(geo.eh + edq[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const int nb = nbq[q];
+        const int ed = edq[q];
+        const bool left = (inf >> (6 + q)) & 1;
+        const bool bnd = nb < 0;
+        const int snb = bnd ? 0 : ((inf >> (2 * q)) & 3);
+        const double nx = enx[q], ny = eny[q], h = eh[q];
+        // prefetch the following side's neighbours (next tile's side 0 after side 2)
+        {
+          const bool last_side = q == 2;
+          const bool ok = last_side ? nvalid : valid;
+          const int nn = last_side ? nbn[0] : nbq[q < 2 ? q + 1 : 0];
+          fetch_frag<NP, KS>(w_nbr + (sbuf ^ 1) * FR, a.in, ld, nn, ok && nn >= 0, lane, t);
+          cp_async_commit();
+        }
+        cp_async_wait<1>();  // this side's neighbours (and the own prefetch) have landed
+        const double* __restrict__ nbuf = w_nbr + sbuf * FR;
+        if constexpr (MODE == kModeSurface) {
+#pragma unroll
+          for (int m = 0; m < 4; ++m)
+#pragma unroll
+            for (int jt = 0; jt < JT; ++jt) R[m][jt][0] = R[m][jt][1] = 0.0;
+        }
+        // neighbour trace (reversed points) — one pass per neighbour side label
+        // present in the warp (class renumbering makes that one pass almost always)
+        double Tn[4][2];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) Tn[m][0] = Tn[m][1] = 0.0;
+        unsigned todo = __reduce_or_sync(0xffffffffu, snb ? (1u << snb) : 0u);
+        while (todo) {
+          const int s = __ffs(todo) - 1;
+          todo &= todo - 1;
+          const double keep = (snb == s) ? 1.0 : 0.0;
+#pragma unroll
+          for (int ks = 0; ks < KS; ++ks) {
+            const double b = smem[D::kPheR + ((s - 1) * KS + ks) * 32 + lane];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) dmma(Tn[m], keep * nbuf[(m * KS + ks) * 32 + lane], b);
+          }
+        }
+        // numerical flux at points ko = 2t + i, canonical orientation
+        double fn[4][2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int ko = 2 * t + i;
+          double UL[4], UR[4];
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            UL[m] = left ? Tw[q][m][i] : Tn[m][i];
+            UR[m] = left ? Tn[m][i] : Tw[q][m][i];
+          }
+          const int kc = left ? ko : K - 1 - ko;  // canonical (left-element) point index
+          const bool live = ko < K;
+          if (bnd && live) ghost_state<K>(UL, nb, ed, kc, nx, ny, tstage, geo, UR);
+          const Prim wl = primitives(UL, g1), wr = primitives(UR, g1);
+          double f[4];
+          if (admissible(UL, wl) && admissible(UR, wr)) {
+            llf_flux(UL, wl, UR, wr, nx, ny, gamma, f);
+          } else {
+            if (valid && live) record_error(sc, err_key(a.seq, kPassSurface, ed, kc));
+#pragma unroll
+            for (int m = 0; m < 4; ++m) f[m] = 0.0;
+          }
+          const double wh = live ? h * smem[D::kWe + (kc < 8 ? kc : 0)] : 0.0;
+#pragma unroll
+          for (int m = 0; m < 4; ++m) fn[m][i] = left ? -(wh * f[m]) : (wh * f[m]);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int jt = 0; jt < JT; ++jt) {
+            const double b = smem[D::kPheP + ((q * 2 + i) * JT + jt) * 32 + lane];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) dmma(R[m][jt], fn[m][i], b);
+          }
+        sbuf ^= 1;
+        if constexpr (MODE == kModeSurface) {
+          if (valid) {
+#pragma unroll
+            for (int m = 0; m < 4; ++m)
+#pragma unroll
+              for (int jt = 0; jt < JT; ++jt)
+#pragma unroll
+                for (int ii = 0; ii < 2; ++ii) {
+                  const int j = 8 * jt + 2 * t + ii;
+                  if (j < NP) a.out[((static_cast<long long>(q) * 4 + m) * NP + j) * ld + e] = R[m][jt][ii];
+                }
+          }
+        }
+      }
+    } else {
+      // volume-only: keep the pipeline shape (own prefetch for the next tile)
+      __syncwarp();
+      fetch_frag<NP, KS>(w_own, a.in, ld, e_next, nvalid, lane, t);
+      cp_async_commit();
+      cp_async_commit();  // (no neighbour stream)
+    }
+
+    // ------------------------------------------------------------ outputs (lane: element g, modes 8jt+2t+ii)
+    if constexpr (MODE == kModeVolume || MODE == kModeRhs) {
+      const double sc_ = (MODE == kModeRhs) ? __ldg(geo.inv_det + e) : 1.0;
+      if (valid) {
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+#pragma unroll
+          for (int jt = 0; jt < JT; ++jt)
+#pragma unroll
+            for (int ii = 0; ii < 2; ++ii) {
+              const int j = 8 * jt + 2 * t + ii;
+              if (j < NP) a.out[(static_cast<long long>(m) * NP + j) * ld + e] = R[m][jt][ii] * sc_;
+            }
+      }
+    } else if constexpr (MODE == kModeStage) {
+      const double idet = __ldg(geo.inv_det + e);
+      const double gdt = a.gcoef * dt;
+      const double dt6 = dt / 6.0;
+      const bool need_u = a.alpha != 0.0 || a.want_resid || a.kmode == 3;
+      const bool need_c = a.kmode != 3 && a.beta != 0.0;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        // this variable's u^n, stage input and RK4 accumulator: every load issued
+        // before any store, so one memory latency per variable
+        double uv[JT][2], cv[JT][2], kv[JT][2];
+#pragma unroll
+        for (int jt = 0; jt < JT; ++jt)
+#pragma unroll
+          for (int ii = 0; ii < 2; ++ii) {
+            const int j = 8 * jt + 2 * t + ii;
+            const long long idx = (static_cast<long long>(m) * NP + j) * ld + e;
+            uv[jt][ii] = (need_u && j < NP) ? __ldg(a.u + idx) : 0.0;
+            cv[jt][ii] = (need_c && j < NP) ? __ldg(a.in + idx) : 0.0;
+            kv[jt][ii] = ((a.kmode == 2 || a.kmode == 3) && j < NP) ? a.kacc[idx] : 0.0;
+          }
+#pragma unroll
+        for (int jt = 0; jt < JT; ++jt)
+#pragma unroll
+          for (int ii = 0; ii < 2; ++ii) {
+            const int j = 8 * jt + 2 * t + ii;
+            if (j < NP) {
+              const long long idx = (static_cast<long long>(m) * NP + j) * ld + e;
+              const double d = R[m][jt][ii] * idet;
+              const double uu = uv[jt][ii], cj = cv[jt][ii];
+              double o;
+              if (a.kmode == 3) {
+                o = fma(dt6, kv[jt][ii] + d, uu);
+              } else {
+                const double base = (a.alpha != 0.0) ? fma(a.alpha, uu, a.beta * cj) : a.beta * cj;
+                o = fma(gdt, d, base);
+                if (a.kmode == 1 && valid) a.kacc[idx] = d;
+                if (a.kmode == 2 && valid) a.kacc[idx] = fma(2.0, d, kv[jt][ii]);
+              }
+              if (valid) {
+                a.out[idx] = o;
+                if (a.want_resid) res_max = fmax(res_max, fabs(uu - o));
+              }
+              R[m][jt][ii] = o;  // keep the new stage for the CFL epilogue / halo push
+            } else {
+              R[m][jt][ii] = 0.0;
+            }
+          }
+      }
+      if (a.push && valid && e >= geo.send_begin) {
+        const int s0 = __ldg(geo.send_ptr + (e - geo.send_begin));
+        const int s1 = __ldg(geo.send_ptr + (e - geo.send_begin) + 1);
+        for (int sidx = s0; sidx < s1; ++sidx) {
+          const int2 ent = __ldg(geo.send_ent + sidx);
+          double* __restrict__ dst = a.peers->buf[ent.x][a.out_buf];
+          const long long pld = a.peers->ld[ent.x];
+#pragma unroll
+          for (int m = 0; m < 4; ++m)
+#pragma unroll
+            for (int jt = 0; jt < JT; ++jt)
+#pragma unroll
+              for (int ii = 0; ii < 2; ++ii) {
+                const int j = 8 * jt + 2 * t + ii;
+                if (j < NP) dst[(static_cast<long long>(m) * NP + j) * pld + ent.y] = R[m][jt][ii];
+              }
+        }
+      }
+      if (a.want_lambda) {
+        // states at the 3 side midpoints: partial sums over this lane's modes, then
+        // reduced over the 4 lanes of the element
+        double v[3][4];
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            double s = 0.0;
+#pragma unroll
+            for (int jt = 0; jt < JT; ++jt)
+#pragma unroll
+              for (int ii = 0; ii < 2; ++ii) s = fma(smem[D::kPhm + q * JT * 8 + 8 * jt + 2 * t + ii], R[m][jt][ii], s);
+            s += __shfl_xor_sync(0xffffffffu, s, 1);
+            s += __shfl_xor_sync(0xffffffffu, s, 2);
+            v[q][m] = s;
+          }
+        // lane t < 3 evaluates the wave speed at midpoint t
+        double U[4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) U[m] = t == 0 ? v[0][m] : (t == 1 ? v[1][m] : v[2][m]);
+        const int qq = t < 3 ? t : 2;
+        const int edq = __ldg(geo.eid + qq * ld + e);
+        const Prim w = primitives(U, g1);
+        double lam = 0.0;
+        if (admissible(U, w)) {
+          lam = fabs(w.vx * __ldg(geo.enx + edq) + w.vy * __ldg(geo.eny + edq)) + sqrt(gamma * w.p * w.inv);
+        } else if (valid && t < 3) {
+          record_error(sc, err_key(a.seq_next, kPassDt, __ldg(geo.ref_id + e), t + 1));
+        }
+        if (t == 3) lam = 0.0;
+        lam = fmax(lam, __shfl_xor_sync(0xffffffffu, lam, 1));
+        lam = fmax(lam, __shfl_xor_sync(0xffffffffu, lam, 2));
+        if (valid && t == 0) lam_min = fmin(lam_min, 2.0 * __ldg(geo.inradius + e) / ((2.0 * P + 1.0) * lam));
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 3; ++q) nbq[q] = nbn[q];
+  }
+  cp_async_wait<0>();
+
+  if constexpr (MODE == kModeStage) {
+    const int par = a.step & 1;
+    if (a.want_lambda) block_reduce_atomic<true>(lam_min, &sc->dtmin[par ^ 1]);
+    if (a.want_resid) block_reduce_atomic<false>(res_max, &sc->resid[par]);
+    if (a.push) __threadfence_system();
+  }
+}
+
+// Host-side preparation of the fragment-ordered tables (see MmaDim for the layout).
+template <int P>
+inline void fill_mma_tab(const Tab<P>& T, double* out) {
+  using D = MmaDim<P>;
+  constexpr int NP = D::NP, NQ = D::NQ, K = D::K, KS = D::KS, NT = D::NT, JT = D::JT;
+  for (int i = 0; i < D::kSize; ++i) out[i] = 0.0;
+  for (int lane = 0; lane < 32; ++lane) {
+    const int g = lane >> 2, t = lane & 3;  // B fragment: row t, column g
+    for (int ks = 0; ks < KS; ++ks)
+      for (int nt = 0; nt < NT; ++nt) {
+        const int j = 4 * ks + t, k = 8 * nt + g;
+        out[D::kPhi + (ks * NT + nt) * 32 + lane] = (j < NP && k < NQ) ? T.phi[k][j] : 0.0;
+      }
+    for (int nt = 0; nt < NT; ++nt)
+      for (int i = 0; i < 2; ++i)
+        for (int jt = 0; jt < JT; ++jt) {
+          const int k = 8 * nt + 2 * t + i, j = 8 * jt + g;
+          const bool ok = k < NQ && j < NP;
+          out[D::kDr + ((nt * 2 + i) * JT + jt) * 32 + lane] = ok ? T.drw[k][j] : 0.0;
+          out[D::kDs + ((nt * 2 + i) * JT + jt) * 32 + lane] = ok ? T.dsw[k][j] : 0.0;
+        }
+    for (int q = 0; q < 3; ++q)
+      for (int ks = 0; ks < KS; ++ks) {
+        const int j = 4 * ks + t, ko = g;
+        const bool ok = j < NP && ko < K;
+        out[D::kPhe + (q * KS + ks) * 32 + lane] = ok ? T.phe[q][ko][j] : 0.0;
+        out[D::kPheR + (q * KS + ks) * 32 + lane] = ok ? T.phe[q][K - 1 - ko][j] : 0.0;
+      }
+    for (int q = 0; q < 3; ++q)
+      for (int i = 0; i < 2; ++i)
+        for (int jt = 0; jt < JT; ++jt) {
+          const int ko = 2 * t + i, j = 8 * jt + g;
+          out[D::kPheP + ((q * 2 + i) * JT + jt) * 32 + lane] = (ko < K && j < NP) ? T.phe[q][ko][j] : 0.0;
+        }
+  }
+  for (int q = 0; q < 3; ++q)
+    for (int j = 0; j < NP; ++j) out[D::kPhm + q * JT * 8 + j] = T.phm[q][j];
+  for (int k = 0; k < K; ++k) out[D::kWe + k] = T.we[k];
+}
+
+}  // namespace dgbk

@@ -1,8 +1,15 @@
 // One translation unit per polynomial degree: its constant bank, the four
 // element-kernel modes and the CFL kernel.  Included by kernels_pN.cu with
 // DGB_P defined.
-#include "element_impl.cuh"
+#include "element_mma.cuh"
 #include "launch.hpp"
+
+#ifndef DGB_MMA_MINP
+#define DGB_MMA_MINP 3  // degrees >= this use the DMMA (FP64 tensor core) element kernel
+#endif
+#ifndef DGB_MMA_MINB
+#define DGB_MMA_MINB(P) ((P) == 3 ? 3 : 2)
+#endif
 
 namespace dgbk {
 
@@ -12,12 +19,21 @@ namespace {
 __constant__ Tab<DGB_P> c_tab;
 constexpr int kG = Lanes<DGB_P>::value;  // lanes per element
 
+constexpr bool kMma = DGB_P >= DGB_MMA_MINP;
+constexpr int kMinB = kMma ? DGB_MMA_MINB(DGB_P) : MinBlocks<DGB_P>::value;
+// dynamic shared memory (bytes): tables + per-warp staging buffers
+constexpr int kSmem = kMma ? (MmaDim<DGB_P>::kSize + (kBlock / 32) * MmaDim<DGB_P>::kWarpBuf) * 8 : 0;
+
 template <int MODE>
-__global__ void __launch_bounds__(kBlock, MinBlocks<DGB_P>::value) k_element(Geo geo, StageArgs a) {
-  if constexpr (kG == 1)
+__global__ void __launch_bounds__(kBlock, kMinB) k_element(Geo geo, StageArgs a) {
+  if constexpr (kMma) {
+    extern __shared__ double smem[];
+    element_body_mma<DGB_P, MODE>(c_tab, geo, a, smem);
+  } else if constexpr (kG == 1) {
     element_body_g1<DGB_P, MODE>(c_tab, geo, a);
-  else
+  } else {
     element_body<DGB_P, MODE>(c_tab, geo, a);
+  }
 }
 
 __global__ void __launch_bounds__(kBlock) k_dt(Geo geo, const double* __restrict__ c, Scalars* sc, int slot,
@@ -35,9 +51,9 @@ int sm_count() {
   return g_sms;
 }
 template <class Kern>
-int occupancy(Kern k) {
+int occupancy(Kern k, int smem = 0) {
   int n = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, kBlock, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, kBlock, smem);
   return n > 0 ? n : 1;
 }
 int grid_for(long long threads, int blocks_per_sm) {
@@ -49,6 +65,16 @@ int grid_for(long long threads, int blocks_per_sm) {
 
 template <>
 cudaError_t Launch<DGB_P>::upload(const Tab<DGB_P>& t, cudaStream_t s) {
+  if constexpr (kMma) {  // opt in to > 48 KB of dynamic shared memory
+    static bool done = false;
+    if (!done) {
+      cudaFuncSetAttribute(k_element<kModeVolume>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+      cudaFuncSetAttribute(k_element<kModeSurface>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+      cudaFuncSetAttribute(k_element<kModeRhs>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+      cudaFuncSetAttribute(k_element<kModeStage>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+      done = true;
+    }
+  }
   return cudaMemcpyToSymbolAsync(c_tab, &t, sizeof(t), 0, cudaMemcpyHostToDevice, s);
 }
 
@@ -57,10 +83,10 @@ int Launch<DGB_P>::resident_blocks(int mode) {
   static int cache[4] = {0, 0, 0, 0};
   if (!cache[mode]) {
     switch (mode) {
-      case kModeVolume: cache[mode] = occupancy(k_element<kModeVolume>); break;
-      case kModeSurface: cache[mode] = occupancy(k_element<kModeSurface>); break;
-      case kModeRhs: cache[mode] = occupancy(k_element<kModeRhs>); break;
-      default: cache[mode] = occupancy(k_element<kModeStage>); break;
+      case kModeVolume: cache[mode] = occupancy(k_element<kModeVolume>, kSmem); break;
+      case kModeSurface: cache[mode] = occupancy(k_element<kModeSurface>, kSmem); break;
+      case kModeRhs: cache[mode] = occupancy(k_element<kModeRhs>, kSmem); break;
+      default: cache[mode] = occupancy(k_element<kModeStage>, kSmem); break;
     }
   }
   return cache[mode];
@@ -68,18 +94,33 @@ int Launch<DGB_P>::resident_blocks(int mode) {
 
 template <>
 int Launch<DGB_P>::lanes() {
-  return kG;
+  return kMma ? 0 : kG;
+}
+
+template <>
+int Launch<DGB_P>::mma_table(const Tab<DGB_P>& t, double* out) {
+  if constexpr (kMma) {
+    if (out) fill_mma_tab<DGB_P>(t, out);
+    return MmaDim<DGB_P>::kSize;
+  } else {
+    return 0;
+  }
 }
 
 template <>
 cudaError_t Launch<DGB_P>::element(int mode, int grid, const Geo& g, const StageArgs& a, cudaStream_t s) {
   if (a.e1 <= a.e0) return cudaSuccess;
-  if (grid <= 0) grid = grid_for(static_cast<long long>((a.e1 - a.e0 + 31) & ~31) * kG, resident_blocks(mode));
+  if (grid <= 0) {
+    // DMMA variant: one 8-element tile per warp; others: kG lanes per element
+    const long long threads = kMma ? static_cast<long long>((a.e1 - a.e0 + 7) / 8) * 32
+                                   : static_cast<long long>((a.e1 - a.e0 + 31) & ~31) * kG;
+    grid = grid_for(threads, resident_blocks(mode));
+  }
   switch (mode) {
-    case kModeVolume: k_element<kModeVolume><<<grid, kBlock, 0, s>>>(g, a); break;
-    case kModeSurface: k_element<kModeSurface><<<grid, kBlock, 0, s>>>(g, a); break;
-    case kModeRhs: k_element<kModeRhs><<<grid, kBlock, 0, s>>>(g, a); break;
-    default: k_element<kModeStage><<<grid, kBlock, 0, s>>>(g, a); break;
+    case kModeVolume: k_element<kModeVolume><<<grid, kBlock, kSmem, s>>>(g, a); break;
+    case kModeSurface: k_element<kModeSurface><<<grid, kBlock, kSmem, s>>>(g, a); break;
+    case kModeRhs: k_element<kModeRhs><<<grid, kBlock, kSmem, s>>>(g, a); break;
+    default: k_element<kModeStage><<<grid, kBlock, kSmem, s>>>(g, a); break;
   }
   return cudaGetLastError();
 }

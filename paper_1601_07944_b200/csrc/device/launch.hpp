@@ -17,7 +17,10 @@ struct Launch {
   static cudaError_t dt(int grid, const Geo& g, const double* c, Scalars* sc, int slot, unsigned long long seq,
                         cudaStream_t s);
   static int resident_blocks(int mode);  // blocks per SM for the element kernel
-  static int lanes();                    // G
+  static int lanes();                    // G (0 = DMMA tile kernel)
+  // DMMA fragment-ordered tables: size in doubles (0 when the degree does not use
+  // the DMMA kernel); fills `out` when non-null
+  static int mma_table(const Tab<P>& t, double* out);
 };
 
 cudaError_t upload_limtab(const LimTab& t, cudaStream_t s);

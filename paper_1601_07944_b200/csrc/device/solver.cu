@@ -286,7 +286,7 @@ struct dgb_ctx {
   std::string bc_error;  // deferred boundary-condition failure (reference throws in the surface pass)
 
   // device geometry
-  DevBuf<double> d_tau, d_inv_det, d_inradius, d_enx, d_eny, d_eh, d_bstate, d_bwn, d_bx;
+  DevBuf<double> d_tau, d_inv_det, d_inradius, d_enx, d_eny, d_eh, d_bstate, d_bwn, d_bx, d_mma;
   DevBuf<int> d_nbr, d_eid, d_info, d_ref_id;  // d_ref_id: reference id of each device column
   Geo geo{};
 
@@ -397,6 +397,18 @@ void upload_tab(dgb_ctx* c, dgbk::Tab<P>& tab) {
   if (g_bank_owner[key] != c) {
     CU(dgbk::Launch<P>::upload(tab, c->stream));
     g_bank_owner[key] = c;
+  }
+  if (!c->d_mma.p) {  // DMMA fragment-ordered copy (global memory, staged to smem per block)
+    const int n = dgbk::Launch<P>::mma_table(tab, nullptr);
+    if (n > 0) {
+      std::vector<double> h(n);
+      dgbk::Launch<P>::mma_table(tab, h.data());
+      c->d_mma.upload(h.data(), n, c->stream);
+      CU(cudaStreamSynchronize(c->stream));
+    } else {
+      c->d_mma.alloc(1);
+    }
+    c->geo.mma_tab = c->d_mma.p;
   }
 }
 

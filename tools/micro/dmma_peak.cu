@@ -29,6 +29,23 @@ __global__ void k_dmma884(double* out, int iters) {
   if (s == 1.2345) out[0] = s;
 }
 
+// one dependent DMMA chain per warp (latency probe) and two chains
+template <int CH>
+__global__ void k_dmma_chain(double* out, int iters) {
+  double a = threadIdx.x * 1e-3, b = 1.0 - threadIdx.x * 1e-4;
+  double d[CH][2];
+  for (int k = 0; k < CH; ++k) d[k][0] = d[k][1] = k;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < CH; ++k)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                   : "+d"(d[k][0]), "+d"(d[k][1]) : "d"(a), "d"(b));
+  }
+  double s = 0;
+  for (int k = 0; k < CH; ++k) s += d[k][0] + d[k][1];
+  if (s == 1.2345) out[0] = s;
+}
+
 // m16n8k4: A 2 doubles, B 1, C/D 4.
 __global__ void k_dmma1684(double* out, int iters) {
   double a0 = threadIdx.x * 1e-3, a1 = a0 + 1, b = 1.0 - threadIdx.x * 1e-4;
@@ -108,8 +125,9 @@ int main() {
   double* d; cudaMalloc(&d, 8);
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const int it = 4096;
-  for (int wpb : {4, 8, 16}) {
-    int blocks = sms * 4, threads = 32 * wpb;
+  // warps per SM sub-partition: 1, 2, 4 (one block per SM) and the saturated case
+  for (int wpb : {4, 8, 16, 32}) {
+    int blocks = sms, threads = 32 * wpb;
     double n = double(blocks) * threads;
     float t = timeit(k_dfma, blocks, threads, it, d);
     printf("warps/blk %2d  DFMA      %.2f TFLOP/s\n", wpb, 2.0 * 8 * it * n / (t * 1e-3) / 1e12);
@@ -119,6 +137,13 @@ int main() {
     printf("warps/blk %2d  DMMA 1684 %.2f TFLOP/s\n", wpb, 2.0 * 4 * it * (n / 32) * 512 / (t * 1e-3) / 1e12);
     t = timeit(k_dmma16816, blocks, threads, it, d);
     printf("warps/blk %2d  DMMA16816 %.2f TFLOP/s\n", wpb, 2.0 * 4 * it * (n / 32) * 2048 / (t * 1e-3) / 1e12);
+    t = timeit(k_dmma_chain<1>, blocks, threads, it, d);
+    printf("warps/blk %2d  DMMA 1 chain  %.2f TFLOP/s  (%.1f cycles per DMMA per warp at 1.965 GHz)\n", wpb,
+           2.0 * it * (n / 32) * 256 / (t * 1e-3) / 1e12, t * 1e-3 * 1.965e9 / it);
+    t = timeit(k_dmma_chain<2>, blocks, threads, it, d);
+    printf("warps/blk %2d  DMMA 2 chains %.2f TFLOP/s\n", wpb, 2.0 * 2 * it * (n / 32) * 256 / (t * 1e-3) / 1e12);
+    t = timeit(k_dmma_chain<4>, blocks, threads, it, d);
+    printf("warps/blk %2d  DMMA 4 chains %.2f TFLOP/s\n", wpb, 2.0 * 4 * it * (n / 32) * 256 / (t * 1e-3) / 1e12);
     t = timeit(k_div, blocks, threads, it, d);
     printf("warps/blk %2d  DDIV      %.3f Gop/s (%.1f DFMA-equiv)\n", wpb, 4.0 * it * n / (t * 1e-3) / 1e9, 0.0);
     t = timeit(k_sqrt, blocks, threads, it, d);
