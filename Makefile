@@ -29,7 +29,7 @@ $(OBJ)/%.o: $(SRC)/host/%.cpp $(HOST_HDRS)
 
 oracle:
 	$(MAKE) -C oracle liboracle.so
-	@if [ -d /root/reference/proj ]; then $(MAKE) -C oracle ref; fi
+	@if [ -d /root/reference/proj ]; then $(MAKE) -C oracle ref && $(MAKE) -C oracle cpptest; fi
 
 clean:
 	rm -rf build $(LIB)

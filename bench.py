@@ -52,6 +52,15 @@ def alg_flops(p, e):
     return NQ[p] * (24 * n + 52) + e * (p + 1) * (32 * n + 115) + 24 * n
 
 
+def ncu_traffic(p):
+    """DRAM bytes per stage-kernel launch measured by ncu (profiles/traffic.json), or None."""
+    try:
+        with open(os.path.join(HERE, "profiles", "traffic.json")) as f:
+            return float(json.load(f)["bytes_per_launch"][str(p)])
+    except Exception:
+        return None
+
+
 def measured_peaks():
     path = os.path.join(HERE, "MEASURED_PEAKS.json")
     try:
@@ -215,7 +224,7 @@ def run_b200(args, rank, world, local, pg):
                     "achieved": ach_bw if bound == "hbm" else ach_fl,
                     "peak": hbm_gbs if bound == "hbm" else fp64_tf,
                     "unit": "GB/s" if bound == "hbm" else "TFLOP/s",
-                    "traffic": None}
+                    "traffic": ncu_traffic(p)}
             roof["frac"] = roof["achieved"] / roof["peak"]
             roof["kernel_ms"] = k_avg
             roof["alg_bytes_per_launch"] = b

@@ -5,7 +5,8 @@
 #include "launch.hpp"
 
 #ifndef DGB_MMA_MINP
-#define DGB_MMA_MINP 3  // degrees >= this use the DMMA (FP64 tensor core) element kernel
+#define DGB_MMA_MINP 4  // degrees >= this use the DMMA (FP64 tensor core) element kernel (p=3: the
+                        // 4-lane DFMA kernel measured 1.03 vs 1.08 ms per stage, so DMMA starts at p=4)
 #endif
 #ifndef DGB_MMA_MINB
 #define DGB_MMA_MINB(P) ((P) == 3 ? 3 : 2)
