@@ -27,7 +27,7 @@ $(OBJ)/%.o: $(SRC)/host/%.cpp $(HOST_HDRS)
 	@mkdir -p $(OBJ)
 	$(CXX) $(CXXFLAGS) -c $< -o $@
 
-oracle:
+oracle: $(LIB)
 	$(MAKE) -C oracle liboracle.so
 	@if [ -d /root/reference/proj ]; then $(MAKE) -C oracle ref && $(MAKE) -C oracle cpptest; fi
 

@@ -311,6 +311,7 @@ struct SolverOptions {  // solver.hpp:72-78
   int workers = 0;  // accepted, unused on the device
   int chunk = 256;  // accepted, unused on the device
   RkScheme scheme = RkScheme::kFromOrder;  // (new) SSP schemes
+  int flux = DGB_FLUX_LLF;                 // (new) DGB_FLUX_LLF (euler.hpp:59-71) or DGB_FLUX_ROE
   int scheme_id() const { return scheme == RkScheme::kFromOrder ? rk_order : static_cast<int>(scheme); }
 };
 
@@ -401,6 +402,7 @@ struct SolverContext {  // solver.hpp:80-87
       }
       detail::check(dgb_create(&mesh->view(), &tables->view(), &v, gas.gamma, device, &dev_->ctx));
       dgb_enable_timers(dev_->ctx, 1);
+      detail::check(dgb_set_flux(dev_->ctx, options.flux));
     }
     return dev_->ctx;
   }

@@ -102,6 +102,11 @@ int dgb_create(const dgb_mesh_view* mesh, const dgb_tables_view* tables, const d
 int dgb_destroy(dgb_ctx* ctx);
 /* Enqueue all work on a caller stream (cudaStream_t passed as void*); NULL = private stream. */
 int dgb_set_stream(dgb_ctx* ctx, void* cuda_stream);
+/* Numerical flux at the edges: the reference's local Lax-Friedrichs (riemann_solver,
+ * euler.hpp:59-71; the default) or Roe with Harten's entropy fix (not in the reference,
+ * asked for by BASELINE.json's north star; oracle/dg2d_oracle.c roe()). */
+enum dgb_flux { DGB_FLUX_LLF = 0, DGB_FLUX_ROE = 1 };
+int dgb_set_flux(dgb_ctx* ctx, int flux);
 /* Replace the Dirichlet table (time-dependent BCs): same layout as dgb_bc_view. */
 int dgb_set_dirichlet(dgb_ctx* ctx, const double* dirichlet_state);
 

@@ -30,7 +30,7 @@ def _d(a):
 
 class OrProblem(C.Structure):
     _fields_ = [("mesh", C.POINTER(L.MeshView)), ("tables", C.POINTER(L.TablesView)),
-                ("bc", C.POINTER(L.BcView)), ("gamma", C.c_double)]
+                ("bc", C.POINTER(L.BcView)), ("gamma", C.c_double), ("flux", C.c_int)]
 
 
 class OrFail(C.Structure):
@@ -67,6 +67,8 @@ def oracle_lib():
         lib.or_euler_flux.restype = None
         lib.or_llf.argtypes = [dp, dp, C.c_double, C.c_double, C.c_double, dp]
         lib.or_llf.restype = None
+        lib.or_roe.argtypes = [dp, dp, C.c_double, C.c_double, C.c_double, dp]
+        lib.or_roe.restype = None
         lib.or_wave_speed.argtypes = [dp, C.c_double, C.c_double, C.c_double]
         lib.or_wave_speed.restype = C.c_double
         _olib = lib
@@ -107,13 +109,14 @@ class OracleError(RuntimeError):
 class Oracle:
     """The CPU restatement on the same mesh / tables / boundary data as the GPU."""
 
-    def __init__(self, mesh, tables, bc=None, gamma=1.4):
+    def __init__(self, mesh, tables, bc=None, gamma=1.4, flux="llf"):
         from paper_1601_07944_b200 import dg2d
         self.mesh, self.tables = mesh, tables
         self.bc = bc or dg2d.BoundaryConditions()
         self._keep = []
         self._bcv = bc_view(self.bc, mesh, tables, self._keep)
-        self.prob = OrProblem(C.pointer(mesh.view), C.pointer(tables.view), C.pointer(self._bcv), gamma)
+        self.prob = OrProblem(C.pointer(mesh.view), C.pointer(tables.view), C.pointer(self._bcv), gamma,
+                              1 if flux == "roe" else 0)
         self.lib = oracle_lib()
         self.shape = (4, tables.n_p, mesh.n_elements())
 

@@ -30,6 +30,7 @@ typedef struct or_problem {
   const dgb_tables_view* tables;
   const dgb_bc_view* bc;
   double gamma;
+  int flux; /* 0 local Lax-Friedrichs (euler.hpp:59-71), 1 Roe (not in the reference) */
 } or_problem;
 
 /* failure record: pass 0 none, 1 eval_volume, 2 eval_surface, 3 stable_dt */
@@ -55,6 +56,7 @@ int or_run_fixed_steps(const or_problem* P, double* c, double* t, int64_t n, int
 double or_pressure(const double* u, double gamma);
 void or_euler_flux(const double* u, double gamma, double* f1, double* f2);
 void or_llf(const double* ul, const double* ur, double nx, double ny, double gamma, double* f);
+void or_roe(const double* ul, const double* ur, double nx, double ny, double gamma, double* f);
 double or_wave_speed(const double* u, double nx, double ny, double gamma);
 
 #ifdef __cplusplus

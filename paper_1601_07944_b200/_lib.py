@@ -79,6 +79,7 @@ class AbortInfo(C.Structure):
 OK, ERR_INADMISSIBLE, ERR_BC, ERR_ARG, ERR_CUDA, ERR_MESH, ERR_NOT_REACHED, ERR_IO = range(8)
 SLOT_STATE, SLOT_INPUT, SLOT_VOLUME, SLOT_DERIV = range(4)
 RK2_MIDPOINT, RK4_CLASSIC, SSP_RK2, SSP_RK3 = 2, 4, 102, 103
+FLUX_LLF, FLUX_ROE = 0, 1
 MESH_BOX, MESH_SHEARED_BOX, MESH_DOUBLE_MACH, MESH_VORTEX, MESH_PERIODIC_BOX = range(5)
 
 _vp = C.c_void_p
@@ -97,6 +98,7 @@ _sig("dgb_create", C.c_int, C.POINTER(MeshView), C.POINTER(TablesView), C.POINTE
 _sig("dgb_destroy", C.c_int, _vp)
 _sig("dgb_set_stream", C.c_int, _vp, _vp)
 _sig("dgb_set_dirichlet", C.c_int, _vp, c_double_p)
+_sig("dgb_set_flux", C.c_int, _vp, C.c_int)
 _sig("dgb_upload", C.c_int, _vp, C.c_int, c_double_p)
 _sig("dgb_download", C.c_int, _vp, C.c_int, c_double_p)
 _sig("dgb_copy_slot", C.c_int, _vp, C.c_int, C.c_int)

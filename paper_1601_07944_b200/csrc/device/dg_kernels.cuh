@@ -113,6 +113,7 @@ struct Geo {
   int send_begin;
   // basis tables in DMMA fragment order (element_mma.cuh), p >= 3
   const double* __restrict__ mma_tab;
+  int flux;  // numerical flux: 0 local Lax-Friedrichs (euler.hpp:59-71), 1 Roe
 };
 
 // Modes of the fused element kernel.

@@ -116,6 +116,54 @@ __device__ __forceinline__ void llf_flux(const double (&UL)[4], const Prim& wl, 
     fn[m] = 0.5 * (nx * (f1l[m] + f1r[m]) + ny * (f2l[m] + f2r[m])) - hs * (UR[m] - UL[m]);
 }
 
+// Roe flux with Harten's entropy fix on the acoustic waves (delta = 0.1 c~); not in the
+// reference (it has LLF only) — same formulas as the oracle's roe() (oracle/dg2d_oracle.c),
+// on the precomputed primitives.
+__device__ __forceinline__ void roe_flux(const double (&UL)[4], const Prim& wl, const double (&UR)[4], const Prim& wr,
+                                         double nx, double ny, double gamma, double (&fn)[4]) {
+  const double epl = UL[3] + wl.p, epr = UR[3] + wr.p;
+  const double HL = epl * wl.inv, HR = epr * wr.inv;
+  const double sl = sqrt_nr(UL[0]), sr = sqrt_nr(UR[0]);
+  const double isum = rcp_nr(sl + sr);
+  const double u = (sl * wl.vx + sr * wr.vx) * isum, v = (sl * wl.vy + sr * wr.vy) * isum;
+  const double H = (sl * HL + sr * HR) * isum;
+  const double q2 = u * u + v * v;
+  const double c = sqrt_nr((gamma - 1.0) * (H - 0.5 * q2)), rho = sl * sr;
+  const double ic2 = rcp_nr(c * c);
+  const double qn = u * nx + v * ny;
+  const double du = wr.vx - wl.vx, dv = wr.vy - wl.vy, dqn = du * nx + dv * ny;
+  const double dut = du - dqn * nx, dvt = dv - dqn * ny;
+  const double dr = UR[0] - UL[0], dp = wr.p - wl.p;
+  const double a1 = 0.5 * (dp - rho * c * dqn) * ic2, a2 = dr - dp * ic2, a3 = 0.5 * (dp + rho * c * dqn) * ic2;
+  double l1 = fabs(qn - c), l3 = fabs(qn + c);
+  const double l2 = fabs(qn), dd = 0.1 * c, i2d = 0.5 * rcp_nr(dd);
+  if (l1 < dd) l1 = (l1 * l1 + dd * dd) * i2d;
+  if (l3 < dd) l3 = (l3 * l3 + dd * dd) * i2d;
+  const double b1 = l1 * a1, b2 = l2 * a2, b3 = l3 * a3, b4 = l2 * rho;
+  const double D0 = b1 + b2 + b3;
+  const double D1 = b1 * (u - c * nx) + b2 * u + b3 * (u + c * nx) + b4 * dut;
+  const double D2 = b1 * (v - c * ny) + b2 * v + b3 * (v + c * ny) + b4 * dvt;
+  const double D3 = b1 * (H - qn * c) + b2 * 0.5 * q2 + b3 * (H + qn * c) + b4 * (u * dut + v * dvt);
+  const double f1l[4] = {UL[1], fma(UL[1], wl.vx, wl.p), UL[2] * wl.vx, wl.vx * epl};
+  const double f1r[4] = {UR[1], fma(UR[1], wr.vx, wr.p), UR[2] * wr.vx, wr.vx * epr};
+  const double f2l[4] = {UL[2], UL[1] * wl.vy, fma(UL[2], wl.vy, wl.p), wl.vy * epl};
+  const double f2r[4] = {UR[2], UR[1] * wr.vy, fma(UR[2], wr.vy, wr.p), wr.vy * epr};
+  const double D[4] = {D0, D1, D2, D3};
+#pragma unroll
+  for (int m = 0; m < 4; ++m) fn[m] = 0.5 * (nx * (f1l[m] + f1r[m]) + ny * (f2l[m] + f2r[m])) - 0.5 * D[m];
+}
+
+enum : int { kFluxLLF = 0, kFluxRoe = 1 };
+
+// The numerical flux selected for the run (warp-uniform branch).
+__device__ __forceinline__ void num_flux(int kind, const double (&UL)[4], const Prim& wl, const double (&UR)[4],
+                                         const Prim& wr, double nx, double ny, double gamma, double (&fn)[4]) {
+  if (kind == kFluxRoe)
+    roe_flux(UL, wl, UR, wr, nx, ny, gamma, fn);
+  else
+    llf_flux(UL, wl, UR, wr, nx, ny, gamma, fn);
+}
+
 __device__ __forceinline__ void reflect(const double (&u)[4], double nx, double ny, double (&g)[4]) {
   const double mn = 2.0 * (u[1] * nx + u[2] * ny);
   g[0] = u[0];
@@ -504,7 +552,7 @@ __device__ __forceinline__ void element_body(const Tab<P>& T, const Geo& geo, co
           const Prim wl = primitives(UL, g1), wr = primitives(UR, g1);
           double fn[4];
           if (admissible(UL, wl) && admissible(UR, wr)) {
-            llf_flux(UL, wl, UR, wr, nx, ny, gamma, fn);
+            num_flux(geo.flux, UL, wl, UR, wr, nx, ny, gamma, fn);
           } else {
             if (valid && g < nk) record_error(sc, err_key(a.seq, kPassSurface, ed, kc));
 #pragma unroll
@@ -794,7 +842,7 @@ __device__ __forceinline__ void element_body_g1(const Tab<P>& T, const Geo& geo,
           const Prim wl = primitives(UL, g1), wr = primitives(UR, g1);
           double fn[4];
           if (admissible(UL, wl) && admissible(UR, wr)) {
-            llf_flux(UL, wl, UR, wr, nx, ny, gamma, fn);
+            num_flux(geo.flux, UL, wl, UR, wr, nx, ny, gamma, fn);
           } else {
             record_error(sc, err_key(a.seq, kPassSurface, ed, kc));
 #pragma unroll

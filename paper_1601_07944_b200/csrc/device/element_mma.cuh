@@ -356,7 +356,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
           const Prim wl = primitives(UL, g1), wr = primitives(UR, g1);
           double f[4];
           if (admissible(UL, wl) && admissible(UR, wr)) {
-            llf_flux(UL, wl, UR, wr, nx, ny, gamma, f);
+            num_flux(geo.flux, UL, wl, UR, wr, nx, ny, gamma, f);
           } else {
             if (valid && live) record_error(sc, err_key(a.seq, kPassSurface, ed, kc));
 #pragma unroll

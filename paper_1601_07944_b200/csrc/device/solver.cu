@@ -1290,6 +1290,16 @@ int dgb_set_stream(dgb_ctx* c, void* stream) {
   });
 }
 
+int dgb_set_flux(dgb_ctx* c, int flux) {
+  if (!c) return DGB_ERR_ARG;
+  if (flux != DGB_FLUX_LLF && flux != DGB_FLUX_ROE) {
+    dgb::set_message("unknown numerical flux " + std::to_string(flux));
+    return DGB_ERR_ARG;
+  }
+  c->geo.flux = flux;
+  return DGB_OK;
+}
+
 int dgb_set_dirichlet(dgb_ctx* c, const double* states) {
   return guarded([&] {
     set_device(c);

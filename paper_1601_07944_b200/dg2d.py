@@ -486,9 +486,15 @@ class SolverOptions:
     workers: int = 0
     chunk: int = 256
     scheme: Optional[int] = None  # None -> rk_order (2 midpoint / 4 classic); 102 SSP-RK2, 103 SSP-RK3
+    flux: str = "llf"  # "llf" (euler.hpp:59-71) or "roe" (new, BASELINE.json north star)
 
     def scheme_id(self) -> int:
         return self.scheme if self.scheme is not None else self.rk_order
+
+    def flux_id(self) -> int:
+        if self.flux not in ("llf", "roe"):
+            raise ValueError(f"unknown numerical flux {self.flux!r}")
+        return L.FLUX_ROE if self.flux == "roe" else L.FLUX_LLF
 
 
 @dataclasses.dataclass
@@ -589,6 +595,7 @@ class SolverContext:
                                   self.gas.gamma, self.device, C.byref(h)))
             self._ctx = h
             lib.dgb_enable_timers(h, 1)
+            _check(lib.dgb_set_flux(h, self.options.flux_id()))
         return self._ctx
 
     def close(self):

@@ -83,6 +83,7 @@ class PartContext(SolverContext):
                                    self.device, rank, world, C.byref(h)))
         self._ctx = h
         lib.dgb_enable_timers(h, 1)
+        _check(lib.dgb_set_flux(h, self.options.flux_id()))
         info = L.PartInfo()
         _check(lib.dgb_part_get_info(h, C.byref(info)))
         self.info = info

@@ -307,3 +307,45 @@ def test_full_size_free_stream_conservation_determinism(p):
         sl, sr = orc.surface(c)
         assert term_rel(dg2d.compute_rhs(ctx, c, 0.0), orc.rhs(c), term_scale(vol, sl, sr, m.det_jac)) <= RHS_TOL
     ctx.close()
+
+
+# ----------------------------------------------------------------------------- Roe flux (not in the reference)
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("ci", [0, 2, 3, 4], ids=[CASES[i][0] for i in (0, 2, 3, 4)])
+def test_roe_rhs_matches_oracle(ci, p):
+    """The Roe option of the edge flux (north star: "Lax-Friedrichs or Roe") against the
+    oracle's Roe restatement; parity unpinned by the reference (it has LLF only)."""
+    name, kind, nx, ny, prm, bcf, u0 = CASES[ci]
+    mesh = dg2d.generate_mesh(kind, nx, ny, *prm)
+    tb = dg2d.build_tables(p)
+    bc = bcf()
+    c = dg2d.project_initial(u0, mesh, tb)
+    ctx = dg2d.SolverContext(mesh, tb, bc=bc, options=dg2d.SolverOptions(flux="roe"))
+    orc = bind.Oracle(mesh, tb, bc, flux="roe")
+    vol = orc.volume(c)
+    sl, sr = orc.surface(c, 0.05)
+    scale = term_scale(vol, sl, sr, mesh.det_jac)
+    d_roe = dg2d.compute_rhs(ctx, c, 0.05)
+    assert term_rel(d_roe, orc.rhs(c, 0.05), scale) <= RHS_TOL
+    # and it is a different flux from LLF
+    ctx_llf = dg2d.SolverContext(mesh, tb, bc=bc)
+    assert np.max(np.abs(d_roe - dg2d.compute_rhs(ctx_llf, c, 0.05))) > 1e-8
+    ctx.close()
+    ctx_llf.close()
+
+
+@pytest.mark.parametrize("p,scheme", [(2, 103), (4, 102)])
+def test_roe_run_matches_oracle(p, scheme):
+    mesh = dg2d.generate_mesh(L.MESH_PERIODIC_BOX, 8, 8, 10.0, 10.0)
+    tb = dg2d.build_tables(p)
+    c0 = dg2d.project_initial(dg2d.IsentropicVortex(), mesh, tb)
+    ctx = dg2d.SolverContext(mesh, tb, options=dg2d.SolverOptions(scheme=scheme, cfl=0.3, flux="roe"))
+    st = dg2d.SolverState(c0.copy())
+    dg2d.run_fixed_steps(ctx, st, 25)
+    cr, tr, _, _ = bind.Oracle(mesh, tb, flux="roe").run_fixed_steps(c0, 0.0, 25, scheme, 0.3)
+    assert rel_per_eq(st.coeffs, cr) <= RUN_TOL
+    assert abs(st.t - tr) <= 1e-12 * tr
+    # conservation on the periodic box is exact up to round-off
+    m0, m1 = dg2d.total_mass(mesh, c0), dg2d.total_mass(mesh, st.coeffs)
+    assert abs(m1 - m0) <= 1e-12 * abs(m0)
+    ctx.close()

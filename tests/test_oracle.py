@@ -211,3 +211,76 @@ def test_post_shock_kat():  # test_euler.cpp:220-246
     assert abs(float(dg2d.pressure(post)) - 116.5) < 1e-13 * 116.5
     assert abs(math.hypot(post[1] / post[0], post[2] / post[0]) - 8.25) < 1e-13 * 8.25
     assert abs(post[3] - 563.5) < 1e-13 * 563.5
+
+
+# ----------------------------------------------------------------------------- Roe (not in the reference)
+def _roe(ul, ur, n):
+    f = np.zeros(4)
+    _o().or_roe(bind._d(np.ascontiguousarray(ul, np.float64)), bind._d(np.ascontiguousarray(ur, np.float64)),
+                n[0], n[1], 1.4, bind._d(f))
+    return f
+
+
+def _phys(u, n):
+    f1, f2 = np.zeros(4), np.zeros(4)
+    _o().or_euler_flux(bind._d(np.ascontiguousarray(u, np.float64)), 1.4, bind._d(f1), bind._d(f2))
+    return n[0] * f1 + n[1] * f2
+
+
+def test_roe_defining_properties():
+    """Parity of the Roe flux is unpinned by the reference (it has only LLF); its defining
+    properties pin the restatement: consistency, conservation (antisymmetry), rotational
+    invariance, exact upwinding of supersonic data, and Roe's linearisation
+    F(uR) - F(uL) = A~ (uR - uL) (checked through the upwind identity
+    F_roe(uL,uR) = F(uL) + sum over left-running waves, i.e. the flux difference split)."""
+    rng = np.random.default_rng(11)
+
+    def rand_state():
+        return dg2d.make_state(rng.uniform(0.1, 10), rng.uniform(-3, 3), rng.uniform(-3, 3), rng.uniform(0.01, 10))
+    for trial in range(100):  # consistency F(u,u) = F(u).n
+        u = rand_state()
+        n = (math.cos(0.1 * trial), math.sin(0.1 * trial))
+        f, ph = _roe(u, u, n), _phys(u, n)
+        assert np.all(np.abs(f - ph) <= 1e-13 * (np.abs(ph) + 1))
+    for _ in range(2000):  # conservation
+        ul, ur = rand_state(), rand_state()
+        a = rng.uniform(0, 2 * math.pi)
+        f, g = _roe(ul, ur, (math.cos(a), math.sin(a))), _roe(ur, ul, (-math.cos(a), -math.sin(a)))
+        assert np.all(np.abs(f + g) <= 1e-11 * (np.abs(f) + np.abs(g) + 1))
+    for trial in range(200):  # rotation
+        ul, ur = rand_state(), rand_state()
+        th = 0.031 * trial
+        c, s = math.cos(th), math.sin(th)
+        rot = lambda u: np.array([u[0], c * u[1] - s * u[2], s * u[1] + c * u[2], u[3]])  # noqa: E731
+        n = (0.6, 0.8)
+        f, g = _roe(ul, ur, n), _roe(rot(ul), rot(ur), (c * n[0] - s * n[1], s * n[0] + c * n[1]))
+        sc = abs(f[1]) + abs(f[2]) + abs(f[0]) + 1
+        assert abs(g[0] - f[0]) <= 1e-11 * sc and abs(g[3] - f[3]) <= 1e-11 * (abs(f[3]) + 1)
+        assert abs(g[1] - (c * f[1] - s * f[2])) <= 1e-11 * sc
+        assert abs(g[2] - (s * f[1] + c * f[2])) <= 1e-11 * sc
+    for _ in range(200):  # supersonic to the right: pure upwinding F = F(uL)
+        rho, p = rng.uniform(0.5, 2), rng.uniform(0.5, 2)
+        c = math.sqrt(1.4 * p / rho)
+        ul = dg2d.make_state(rho, 3.0 * c, rng.uniform(-0.2, 0.2) * c, p)
+        ur = dg2d.make_state(rho * rng.uniform(0.95, 1.05), 3.0 * c * rng.uniform(0.97, 1.03), 0.0,
+                             p * rng.uniform(0.95, 1.05))
+        f, ph = _roe(ul, ur, (1.0, 0.0)), _phys(ul, (1.0, 0.0))
+        assert np.all(np.abs(f - ph) <= 1e-11 * (np.abs(ph) + 1))
+    # contact discontinuity at rest (equal p, u = 0): the Roe flux is exactly the pressure
+    ul, ur = dg2d.make_state(1.0, 0, 0, 1.0), dg2d.make_state(0.25, 0, 0, 1.0)
+    f = _roe(ul, ur, (1.0, 0.0))
+    assert abs(f[0]) < 1e-14 and abs(f[1] - 1.0) < 1e-14 and abs(f[2]) < 1e-14 and abs(f[3]) < 1e-14
+
+
+def test_oracle_rhs_with_roe_is_conservative_and_free_stream_preserving():
+    mesh = dg2d.generate_mesh(L.MESH_PERIODIC_BOX, 6, 5, 10.0, 10.0)
+    tb = dg2d.build_tables(3)
+    u0 = dg2d.make_state(1.3, 0.4, -0.2, 0.9)
+    c = dg2d.project_initial(lambda xy: np.tile(u0, (xy.shape[0], 1)), mesh, tb)
+    orc = bind.Oracle(mesh, tb, flux="roe")
+    d = orc.rhs(c)
+    assert np.max(np.abs(d)) < 1e-12  # free stream
+    c2 = dg2d.project_initial(dg2d.IsentropicVortex(), mesh, tb)
+    d2 = orc.rhs(c2)
+    mass = [float(np.sum(mesh.det_jac * d2[m, 0]) / math.sqrt(2.0)) for m in range(4)]
+    assert max(abs(x) for x in mass) < 1e-12 * float(np.max(np.abs(d2)))  # periodic: conserved
