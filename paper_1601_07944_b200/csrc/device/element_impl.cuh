@@ -338,7 +338,7 @@ __device__ __forceinline__ void push_element(const Geo& geo, const PeerTab* __re
 
 // Minimum registers per launch for the fused kernel (occupancy target per degree).
 #ifndef DGB_MINB
-#define DGB_MINB(P) ((P) == 1 ? 5 : (P) == 2 ? 3 : (P) == 3 ? 5 : (P) == 4 ? 4 : 3)
+#define DGB_MINB(P) ((P) == 1 ? 5 : (P) == 2 ? 4 : (P) == 3 ? 5 : (P) == 4 ? 4 : 3)
 #endif
 #ifndef DGB_G1_SIDE_UNROLL
 #define DGB_G1_SIDE_UNROLL 1  // sides of the one-thread-per-element kernel: runtime loop
