@@ -48,8 +48,8 @@ struct MmaDim {
   static constexpr int kPhm = kPheP + 3 * 2 * JT * 32;      // [3][JT*8] midpoint rows (zero padded)
   static constexpr int kWe = kPhm + 3 * JT * 8;             // [8] edge weights (zero padded)
   static constexpr int kSize = kWe + 8;
-  // per-warp staging after the tables: own [4 KS][32] + neighbour [2][4 KS][32]
-  static constexpr int kWarpBuf = 3 * 4 * KS * 32;
+  // per-warp staging after the tables: own [4 KS][32] + neighbour [4 KS][32]
+  static constexpr int kWarpBuf = 2 * 4 * KS * 32;
 };
 
 // volatile: a non-volatile asm may be duplicated into both arms of a per-lane
@@ -154,9 +154,9 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
   const int warp = blockIdx.x * (blockDim.x >> 5) + wib;
   const int nwarps = gridDim.x * (blockDim.x >> 5);
   const int ntiles = (a.e1 - a.e0 + 7) >> 3;
-  // per-warp staging: own coefficients of the tile, neighbour coefficients (2 buffers)
-  double* __restrict__ w_own = smem + D::kSize + wib * 3 * FR;
-  double* __restrict__ w_nbr = w_own + FR;  // [2][FR]
+  // per-warp staging: own coefficients of the tile, neighbour coefficients of one side
+  double* __restrict__ w_own = smem + D::kSize + wib * 2 * FR;
+  double* __restrict__ w_nbr = w_own + FR;
 
   double lam_min = __longlong_as_double(0x7ff0000000000000ll);
   double res_max = 0.0;
@@ -169,7 +169,6 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
   auto nbr_of = [&](int e, int q) { return __ldg(geo.nbr + q * ld + e); };
 
   // pipeline prologue: own coefficients and side-0 neighbours of the first tile
-  int sbuf = 0;  // neighbour buffer of the side being processed
   int nbq[3] = {-4, -4, -4};  // neighbour columns of the current tile's element
   {
     bool ok;
@@ -200,7 +199,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
       }
       inf = __ldg(geo.info + e);
     }
-    cp_async_wait<1>();  // own coefficients of this tile (the newest group is side-0 neighbours)
+    cp_async_wait<0>();  // own coefficients and side-0 neighbours of this tile
     __syncwarp();
 
     double R[4][JT][2];
@@ -273,24 +272,6 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
 
     // ------------------------------------------------------------ surface
     if constexpr (MODE != kModeVolume) {
-      // own traces of the three sides while the own coefficients are staged
-      double Tw[3][4][2];
-#pragma unroll
-      for (int q = 0; q < 3; ++q) {
-#pragma unroll
-        for (int m = 0; m < 4; ++m) Tw[q][m][0] = Tw[q][m][1] = 0.0;
-#pragma unroll
-        for (int ks = 0; ks < KS; ++ks) {
-          const double b = smem[D::kPhe + (q * KS + ks) * 32 + lane];
-#pragma unroll
-          for (int m = 0; m < 4; ++m) dmma(Tw[q][m], w_own[(m * KS + ks) * 32 + lane], b);
-        }
-      }
-      __syncwarp();
-      // the own buffer is free: prefetch the next tile's coefficients
-      fetch_frag<NP, KS>(w_own, a.in, ld, e_next, nvalid, lane, t);
-      cp_async_commit();
-
       double enx[3], eny[3], eh[3];
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
@@ -306,21 +287,22 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
         const bool bnd = nb < 0;
         const int snb = bnd ? 0 : ((inf >> (2 * q)) & 3);
         const double nx = enx[q], ny = eny[q], h = eh[q];
-        // prefetch the following side's neighbours (next tile's side 0 after side 2)
-        {
-          const bool last_side = q == 2;
-          const bool ok = last_side ? nvalid : valid;
-          const int nn = last_side ? nbn[0] : nbq[q < 2 ? q + 1 : 0];
-          fetch_frag<NP, KS>(w_nbr + (sbuf ^ 1) * FR, a.in, ld, nn, ok && nn >= 0, lane, t);
-          cp_async_commit();
-        }
-        cp_async_wait<1>();  // this side's neighbours (and the own prefetch) have landed
-        const double* __restrict__ nbuf = w_nbr + sbuf * FR;
+        if (q > 0) cp_async_wait<0>();  // this side's neighbour column (prefetched during the previous side)
         if constexpr (MODE == kModeSurface) {
 #pragma unroll
           for (int m = 0; m < 4; ++m)
 #pragma unroll
             for (int jt = 0; jt < JT; ++jt) R[m][jt][0] = R[m][jt][1] = 0.0;
+        }
+        // own trace of side q
+        double Tw[4][2];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) Tw[m][0] = Tw[m][1] = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+          const double b = smem[D::kPhe + (q * KS + ks) * 32 + lane];
+#pragma unroll
+          for (int m = 0; m < 4; ++m) dmma(Tw[m], w_own[(m * KS + ks) * 32 + lane], b);
         }
         // neighbour trace (reversed points) — one pass per neighbour side label
         // present in the warp (class renumbering makes that one pass almost always)
@@ -336,9 +318,19 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
           for (int ks = 0; ks < KS; ++ks) {
             const double b = smem[D::kPheR + ((s - 1) * KS + ks) * 32 + lane];
 #pragma unroll
-            for (int m = 0; m < 4; ++m) dmma(Tn[m], keep * nbuf[(m * KS + ks) * 32 + lane], b);
+            for (int m = 0; m < 4; ++m) dmma(Tn[m], keep * w_nbr[(m * KS + ks) * 32 + lane], b);
           }
         }
+        __syncwarp();
+        // the neighbour buffer is consumed: prefetch the next side (after side 2: the
+        // next tile's side 0 and, the own buffer being free too, its own coefficients)
+        if (q < 2) {
+          fetch_frag<NP, KS>(w_nbr, a.in, ld, nbq[q + 1], valid && nbq[q + 1] >= 0, lane, t);
+        } else {
+          fetch_frag<NP, KS>(w_nbr, a.in, ld, nbn[0], nvalid && nbn[0] >= 0, lane, t);
+          fetch_frag<NP, KS>(w_own, a.in, ld, e_next, nvalid, lane, t);
+        }
+        cp_async_commit();
         // numerical flux at points ko = 2t + i, canonical orientation
         double fn[4][2];
 #pragma unroll
@@ -347,8 +339,8 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
           double UL[4], UR[4];
 #pragma unroll
           for (int m = 0; m < 4; ++m) {
-            UL[m] = left ? Tw[q][m][i] : Tn[m][i];
-            UR[m] = left ? Tn[m][i] : Tw[q][m][i];
+            UL[m] = left ? Tw[m][i] : Tn[m][i];
+            UR[m] = left ? Tn[m][i] : Tw[m][i];
           }
           const int kc = left ? ko : K - 1 - ko;  // canonical (left-element) point index
           const bool live = ko < K;
@@ -375,7 +367,6 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
 #pragma unroll
             for (int m = 0; m < 4; ++m) dmma(R[m][jt], fn[m][i], b);
           }
-        sbuf ^= 1;
         if constexpr (MODE == kModeSurface) {
           if (valid) {
 #pragma unroll
@@ -391,11 +382,10 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
         }
       }
     } else {
-      // volume-only: keep the pipeline shape (own prefetch for the next tile)
+      // volume-only: own prefetch for the next tile
       __syncwarp();
       fetch_frag<NP, KS>(w_own, a.in, ld, e_next, nvalid, lane, t);
       cp_async_commit();
-      cp_async_commit();  // (no neighbour stream)
     }
 
     // ------------------------------------------------------------ outputs (lane: element g, modes 8jt+2t+ii)

@@ -8,8 +8,11 @@
 #define DGB_MMA_MINP 4  // degrees >= this use the DMMA (FP64 tensor core) element kernel (p=3: the
                         // 4-lane DFMA kernel measured 1.03 vs 1.08 ms per stage, so DMMA starts at p=4)
 #endif
+#ifndef DGB_MMA_THREADS
+#define DGB_MMA_THREADS 384  // DMMA kernel: 12 warps per block, one block per SM (<= 170 registers)
+#endif
 #ifndef DGB_MMA_MINB
-#define DGB_MMA_MINB(P) ((P) == 3 ? 3 : 2)
+#define DGB_MMA_MINB(P) 1
 #endif
 
 namespace dgbk {
@@ -22,11 +25,12 @@ constexpr int kG = Lanes<DGB_P>::value;  // lanes per element
 
 constexpr bool kMma = DGB_P >= DGB_MMA_MINP;
 constexpr int kMinB = kMma ? DGB_MMA_MINB(DGB_P) : MinBlocks<DGB_P>::value;
+constexpr int kThreads = kMma ? DGB_MMA_THREADS : kBlock;  // threads per block of k_element
 // dynamic shared memory (bytes): tables + per-warp staging buffers
-constexpr int kSmem = kMma ? (MmaDim<DGB_P>::kSize + (kBlock / 32) * MmaDim<DGB_P>::kWarpBuf) * 8 : 0;
+constexpr int kSmem = kMma ? (MmaDim<DGB_P>::kSize + (kThreads / 32) * MmaDim<DGB_P>::kWarpBuf) * 8 : 0;
 
 template <int MODE>
-__global__ void __launch_bounds__(kBlock, kMinB) k_element(Geo geo, StageArgs a) {
+__global__ void __launch_bounds__(kThreads, kMinB) k_element(Geo geo, StageArgs a) {
   if constexpr (kMma) {
     extern __shared__ double smem[];
     element_body_mma<DGB_P, MODE>(c_tab, geo, a, smem);
@@ -52,13 +56,13 @@ int sm_count() {
   return g_sms;
 }
 template <class Kern>
-int occupancy(Kern k, int smem = 0) {
+int occupancy(Kern k, int smem = 0, int threads = kBlock) {
   int n = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, kBlock, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, threads, smem);
   return n > 0 ? n : 1;
 }
-int grid_for(long long threads, int blocks_per_sm) {
-  const long long need = (threads + kBlock - 1) / kBlock;
+int grid_for(long long threads, int blocks_per_sm, int block = kBlock) {
+  const long long need = (threads + block - 1) / block;
   const long long cap = static_cast<long long>(blocks_per_sm) * sm_count();
   return static_cast<int>(need < cap ? need : cap);
 }
@@ -84,10 +88,10 @@ int Launch<DGB_P>::resident_blocks(int mode) {
   static int cache[4] = {0, 0, 0, 0};
   if (!cache[mode]) {
     switch (mode) {
-      case kModeVolume: cache[mode] = occupancy(k_element<kModeVolume>, kSmem); break;
-      case kModeSurface: cache[mode] = occupancy(k_element<kModeSurface>, kSmem); break;
-      case kModeRhs: cache[mode] = occupancy(k_element<kModeRhs>, kSmem); break;
-      default: cache[mode] = occupancy(k_element<kModeStage>, kSmem); break;
+      case kModeVolume: cache[mode] = occupancy(k_element<kModeVolume>, kSmem, kThreads); break;
+      case kModeSurface: cache[mode] = occupancy(k_element<kModeSurface>, kSmem, kThreads); break;
+      case kModeRhs: cache[mode] = occupancy(k_element<kModeRhs>, kSmem, kThreads); break;
+      default: cache[mode] = occupancy(k_element<kModeStage>, kSmem, kThreads); break;
     }
   }
   return cache[mode];
@@ -115,13 +119,13 @@ cudaError_t Launch<DGB_P>::element(int mode, int grid, const Geo& g, const Stage
     // DMMA variant: one 8-element tile per warp; others: kG lanes per element
     const long long threads = kMma ? static_cast<long long>((a.e1 - a.e0 + 7) / 8) * 32
                                    : static_cast<long long>((a.e1 - a.e0 + 31) & ~31) * kG;
-    grid = grid_for(threads, resident_blocks(mode));
+    grid = grid_for(threads, resident_blocks(mode), kThreads);
   }
   switch (mode) {
-    case kModeVolume: k_element<kModeVolume><<<grid, kBlock, kSmem, s>>>(g, a); break;
-    case kModeSurface: k_element<kModeSurface><<<grid, kBlock, kSmem, s>>>(g, a); break;
-    case kModeRhs: k_element<kModeRhs><<<grid, kBlock, kSmem, s>>>(g, a); break;
-    default: k_element<kModeStage><<<grid, kBlock, kSmem, s>>>(g, a); break;
+    case kModeVolume: k_element<kModeVolume><<<grid, kThreads, kSmem, s>>>(g, a); break;
+    case kModeSurface: k_element<kModeSurface><<<grid, kThreads, kSmem, s>>>(g, a); break;
+    case kModeRhs: k_element<kModeRhs><<<grid, kThreads, kSmem, s>>>(g, a); break;
+    default: k_element<kModeStage><<<grid, kThreads, kSmem, s>>>(g, a); break;
   }
   return cudaGetLastError();
 }
