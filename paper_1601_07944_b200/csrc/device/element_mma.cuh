@@ -243,11 +243,12 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
           }
           double f1[4], f2[4];
           euler_flux(v, w, f1, f2);
-          const double live = (k < NQ) ? 1.0 : 0.0;  // padded points contribute nothing
+          const bool live = k < NQ;  // padded points contribute nothing
 #pragma unroll
           for (int m = 0; m < 4; ++m) {
-            fr[m][i] = live * (ta * f1[m] + tb * f2[m]);  // contravariant flux along r
-            fs[m][i] = live * (tc * f1[m] + td * f2[m]);  // along s
+            const double r_ = ta * f1[m] + tb * f2[m], s_ = tc * f1[m] + td * f2[m];
+            fr[m][i] = live ? r_ : 0.0;  // contravariant flux along r
+            fs[m][i] = live ? s_ : 0.0;  // along s
           }
         }
         __syncwarp();
@@ -313,12 +314,15 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
         while (todo) {
           const int s = __ffs(todo) - 1;
           todo &= todo - 1;
-          const double keep = (snb == s) ? 1.0 : 0.0;
+          const bool mine = snb == s;
 #pragma unroll
           for (int ks = 0; ks < KS; ++ks) {
             const double b = smem[D::kPheR + ((s - 1) * KS + ks) * 32 + lane];
 #pragma unroll
-            for (int m = 0; m < 4; ++m) dmma(Tn[m], keep * w_nbr[(m * KS + ks) * 32 + lane], b);
+            for (int m = 0; m < 4; ++m) {
+              const double an = w_nbr[(m * KS + ks) * 32 + lane];
+              dmma(Tn[m], mine ? an : 0.0, b);  // a select, not an FP64 multiply
+            }
           }
         }
         __syncwarp();

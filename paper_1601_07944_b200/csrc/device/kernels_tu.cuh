@@ -5,11 +5,12 @@
 #include "launch.hpp"
 
 #ifndef DGB_MMA_MINP
-#define DGB_MMA_MINP 4  // degrees >= this use the DMMA (FP64 tensor core) element kernel (p=3: the
-                        // 4-lane DFMA kernel measured 1.03 vs 1.08 ms per stage, so DMMA starts at p=4)
+#define DGB_MMA_MINP 3  // degrees >= this use the DMMA (FP64 tensor core) element kernel (measured
+                        // per stage at p=3: DMMA 0.98 ms vs 1.05 ms for the 4-lane DFMA kernel)
 #endif
 #ifndef DGB_MMA_THREADS
-#define DGB_MMA_THREADS 384  // DMMA kernel: 12 warps per block, one block per SM (<= 170 registers)
+// DMMA kernel: one block per SM; p=3 16 warps (128 registers), p=4,5 12 warps (168 registers)
+#define DGB_MMA_THREADS(P) ((P) == 3 ? 512 : 384)
 #endif
 #ifndef DGB_MMA_MINB
 #define DGB_MMA_MINB(P) 1
@@ -25,7 +26,7 @@ constexpr int kG = Lanes<DGB_P>::value;  // lanes per element
 
 constexpr bool kMma = DGB_P >= DGB_MMA_MINP;
 constexpr int kMinB = kMma ? DGB_MMA_MINB(DGB_P) : MinBlocks<DGB_P>::value;
-constexpr int kThreads = kMma ? DGB_MMA_THREADS : kBlock;  // threads per block of k_element
+constexpr int kThreads = kMma ? DGB_MMA_THREADS(DGB_P) : kBlock;  // threads per block of k_element
 // dynamic shared memory (bytes): tables + per-warp staging buffers
 constexpr int kSmem = kMma ? (MmaDim<DGB_P>::kSize + (kThreads / 32) * MmaDim<DGB_P>::kWarpBuf) * 8 : 0;
 
