@@ -173,6 +173,12 @@ int dgb_run_to_steady(dgb_ctx* ctx, int scheme, double cfl, int limiting, double
 /* ---------------------------------------------------------------- reductions, diagnostics */
 /* total_mass (solver.cpp:662-670), serial-order sum on the host for determinism. */
 int dgb_total_mass(dgb_ctx* ctx, int slot, double* mass);
+/* compute_l2_error (runner.cpp:127-150): L2 norm of the density error against exact values
+ * given at every interior quadrature point, exact_rho[n_elem][n_quad] (reference order, points
+ * from dgb_interior_points).  Per-element partials on the device, summed on the host in element
+ * order.  For a partitioned context: the rank's partial sum of squares (exact_rho over its owned
+ * elements, ascending id); the caller adds the ranks in rank order and takes the square root. */
+int dgb_l2_error(dgb_ctx* ctx, int slot, const double* exact_rho, double* l2);
 /* max_abs_diff (solver.cpp:672-678). */
 int dgb_max_abs_diff(dgb_ctx* ctx, int slot_a, int slot_b, double* diff);
 

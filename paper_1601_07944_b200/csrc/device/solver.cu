@@ -182,6 +182,25 @@ __global__ void k_gather(double* __restrict__ deriv, const double* __restrict__ 
   }
 }
 
+// compute_l2_error (runner.cpp:127-150), per-element partials: det_i * sum_k w_k (rho_h - rho_ex)^2.
+// exact[(local i) * nq + k] holds the exact density at interior point k of owned element i (reference
+// order); part[local i] receives the partial (the host adds them in element order).
+__global__ void k_l2_partial(const double* __restrict__ c, const double* __restrict__ exact,
+                             const double* __restrict__ tab /* phi[nq][np], w[nq] */, const int* __restrict__ cmp,
+                             const double* __restrict__ inv_det, int n, int ld, int np, int nq, double* part) {
+  for (int d = blockIdx.x * blockDim.x + threadIdx.x; d < n; d += gridDim.x * blockDim.x) {
+    const int i = cmp[d];
+    double acc = 0.0;
+    for (int k = 0; k < nq; ++k) {
+      double rho = 0.0;
+      for (int j = 0; j < np; ++j) rho += c[static_cast<long long>(j) * ld + d] * tab[k * np + j];
+      const double diff = rho - exact[static_cast<long long>(i) * nq + k];
+      acc += tab[nq * np + k] * diff * diff;
+    }
+    part[i] = acc / inv_det[d];
+  }
+}
+
 __global__ void k_max_abs_diff(const double* __restrict__ a, const double* __restrict__ b, int n, int ld, int rows,
                                unsigned long long* out) {
   const long long total = static_cast<long long>(rows) * ld;
@@ -262,7 +281,7 @@ struct dgb_ctx {
   std::vector<double> enx, eny;
   std::vector<double> bc_dir, bc_wn;
   dgb_bc_view bc{};
-  std::vector<double> t_phi, t_phe, t_phm, t_xi;
+  std::vector<double> t_phi, t_phe, t_phm, t_xi, t_w;
   std::vector<int> ref_of;   // device column -> reference element id (owned, then halo)
   std::vector<int> col_of;   // reference element id -> device column (-1 when not local)
   std::vector<int> halo_gid; // reference ids of the halo columns [N, N + n_halo)
@@ -1037,6 +1056,7 @@ int dgb_part_create(const dgb_mesh_view* m, const dgb_tables_view* t, const dgb_
     c->t_phe.assign(t->phi_edge, t->phi_edge + 3 * c->K * np);
     c->t_phm.assign(t->phi_edge_mid, t->phi_edge_mid + 3 * np);
     c->t_xi.assign(t->xi_edge, t->xi_edge + c->K);
+    c->t_w.assign(t->w_interior, t->w_interior + c->nq);
 
     PartPlan P;
     make_plan(m, rank, world, P);
@@ -1584,6 +1604,32 @@ int dgb_total_mass(dgb_ctx* c, int slot, double* mass) {
     double s = 0.0;  // partition: this rank's partial sum, reference order (ranks add in rank order)
     for (int i = 0; i < c->N; ++i) s += c->det[c->lo + i] * row[i] * inv_sqrt2;
     *mass = s;
+    return DGB_OK;
+  });
+}
+
+int dgb_l2_error(dgb_ctx* c, int slot, const double* exact_rho, double* l2) {
+  return guarded([&] {
+    set_device(c);
+    if (!exact_rho || !l2) throw Fail{DGB_ERR_ARG, "null argument"};
+    const int n = c->N, nq = c->nq, np = c->np;
+    DevBuf<double> tab, ex, part;
+    std::vector<double> h(static_cast<size_t>(nq) * np + nq);
+    std::copy(c->t_phi.begin(), c->t_phi.end(), h.begin());
+    std::copy(c->t_w.begin(), c->t_w.end(), h.begin() + static_cast<size_t>(nq) * np);
+    tab.upload(h.data(), h.size(), c->stream);
+    ex.upload(exact_rho, static_cast<size_t>(n) * nq, c->stream);
+    part.alloc(n);
+    k_l2_partial<<<small_grid(n), 256, 0, c->stream>>>(slot_ptr(c, slot), ex.p, tab.p, c->d_cmp.p, c->d_inv_det.p, n,
+                                                        c->ld, np, nq, part.p);
+    CU(cudaGetLastError());
+    ++c->launches;
+    std::vector<double> hp(n);
+    CU(cudaMemcpyAsync(hp.data(), part.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    double total = 0.0;  // element order (runner.cpp:146-148); a partition returns its partial sum squared
+    for (int i = 0; i < n; ++i) total += hp[i];
+    *l2 = c->partitioned ? total : std::sqrt(total);
     return DGB_OK;
   });
 }

@@ -889,6 +889,54 @@ def total_mass(mesh: Mesh, coeffs) -> float:
     return s
 
 
+def compute_l2_error(ctx: SolverContext, coeffs, exact: Callable) -> float:
+    """runner.cpp:127-150: L2 norm of the density error against ``exact(xy[n,2]) -> states[n,4]``
+    (per-element partials on the device, summed in element order on the host)."""
+    xy = interior_points(ctx.mesh, ctx.tables).reshape(-1, 2)
+    rho = np.ascontiguousarray(np.asarray(exact(xy), np.float64).reshape(-1, 4)[:, 0])
+    ctx.upload(L.SLOT_INPUT, coeffs)
+    out = C.c_double()
+    _check(lib.dgb_l2_error(ctx.handle, L.SLOT_INPUT, dptr(rho), C.byref(out)))
+    return out.value
+
+
+@dataclasses.dataclass
+class ConvergenceRow:
+    """runner.hpp ConvergenceRow"""
+    mesh_letter: str
+    elements: int
+    error: float
+    rate: Optional[float]
+    steps: int
+
+
+def convergence_study(p: int, letters: str = "A,B,C,D", rk_order: int = 4, cfl: float = 0.9,
+                      steady_tol: float = 1e-14, max_steps: int = 5_000_000,
+                      geo: "VortexGeometry" = None, gas: GasModel = GasModel(), device: Optional[int] = None):
+    """runner.cpp:261-284 for the supersonic vortex (the only problem it accepts): per mesh of the
+    family A.. (levels 0..), project the exact solution, run to steady state on the device,
+    L2 density error, and the rate log2(e_prev / e)."""
+    geo = geo or VortexGeometry()
+    rows, prev = [], None
+    for letter in [x for x in letters.replace(" ", "").split(",") if x]:
+        level = ord(letter.upper()) - ord("A")
+        mesh = generate_mesh(L.MESH_VORTEX, level, 0, geo.r_inner, geo.r_outer)
+        tb = build_tables(p)
+        exact = lambda xy: vortex_exact(xy, geo, gas)  # noqa: E731
+        ctx = SolverContext(mesh, tb, gas=gas, bc=vortex_boundary(geo, gas),
+                            options=SolverOptions(rk_order=rk_order, cfl=cfl), device=device)
+        st = SolverState(project_initial(exact, mesh, tb, gas))
+        sr = run_to_steady(ctx, st, steady_tol, max_steps)
+        if not sr.converged:  # runner.cpp:192-194
+            raise SolverAbort(f"steady run did not converge within {max_steps} steps (residual {sr.residual})")
+        err = compute_l2_error(ctx, st.coeffs, exact)
+        rows.append(ConvergenceRow(letter.upper(), mesh.n_elements(), err,
+                                   math.log2(prev / err) if prev is not None else None, sr.steps))
+        prev = err
+        ctx.close()
+    return rows
+
+
 def max_abs_diff(a, b) -> float:
     """solver.cpp:672-678"""
     a, b = np.asarray(a), np.asarray(b)

@@ -349,3 +349,35 @@ def test_roe_run_matches_oracle(p, scheme):
     m0, m1 = dg2d.total_mass(mesh, c0), dg2d.total_mass(mesh, st.coeffs)
     assert abs(m1 - m0) <= 1e-12 * abs(m0)
     ctx.close()
+
+
+# ----------------------------------------------------------------------------- accuracy (paper table)
+def test_l2_error_matches_host_restatement():
+    """compute_l2_error (runner.cpp:127-150): device partials vs a host restatement."""
+    mesh, tb, bc, c, ctx, orc = build(CASES[2], 3)
+    exact = lambda xy: dg2d.vortex_exact(xy)  # noqa: E731
+    xy = dg2d.interior_points(mesh, tb).reshape(-1, 2)
+    rho_ex = exact(xy)[:, 0].reshape(mesh.n_elements(), tb.n_quad)
+    phi = np.asarray(tb.view.phi_interior[:tb.n_quad * tb.n_p]).reshape(tb.n_quad, tb.n_p)
+    w = np.asarray(tb.view.w_interior[:tb.n_quad])
+    c2 = c * (1.0 + 1e-3 * np.sin(np.arange(c.size)).reshape(c.shape))  # not the projection itself
+    rho_h = np.einsum("kj,ji->ik", phi, c2[0])
+    part = mesh.det_jac * ((rho_h - rho_ex) ** 2 @ w)
+    host = math.sqrt(sum(float(x) for x in part))
+    dev = dg2d.compute_l2_error(ctx, c2, exact)
+    assert abs(dev - host) <= 1e-13 * host
+    ctx.close()
+
+
+def test_convergence_rates_match_the_paper():
+    """acceptance.cpp:95-146 / PAPER.md:757-785: supersonic vortex, meshes A-D, p=1..4, RK4,
+    cfl 0.9, steady tolerance 1e-14; C->D rates within 0.35 of 1.910/2.953/4.086/4.983 and
+    the mesh-A p=1 error within a factor 3 of 4.934e-3.  (~16 s on a B200.)"""
+    expected = {1: 1.910, 2: 2.953, 3: 4.086, 4: 4.983}
+    for p in (1, 2, 3, 4):
+        rows = dg2d.convergence_study(p, "A,B,C,D")
+        assert abs(rows[3].rate - expected[p]) <= 0.35, (p, [(r.mesh_letter, r.error, r.rate) for r in rows])
+        if p == 1:
+            assert 4.934e-3 / 3 <= rows[0].error <= 4.934e-3 * 3
+        for a, b in zip(rows, rows[1:]):
+            assert b.error < a.error
