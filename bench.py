@@ -299,7 +299,52 @@ def run_b200(args, rank, world, local, pg):
                        "note": "per step: pinned host state -> dgb_upload -> one RK step -> dgb_download"}
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(mesh, orders, args)
+    if world == 1 and args.dmr_nx > 0:
+        line["dmr"] = dmr_leg(args, local)
     return line
+
+
+def dmr_leg(args, local):
+    """BASELINE.json configs[3] (C4): double Mach reflection, p=1, Barth-Jespersen limiter on
+    every stage, midpoint RK2 (dmr_desk.cfg), on the 2000x500 channel (2M triangles): the
+    paper's own headline path (GTX 580 mesh C: 1.31e8 DOF-updates/s/stage).
+    Informational; not part of `value`."""
+    import torch
+    from paper_1601_07944_b200 import _lib as L
+    from paper_1601_07944_b200 import dg2d
+    nx, ny = args.dmr_nx, args.dmr_nx // 4
+    mesh = dg2d.generate_mesh(L.MESH_DOUBLE_MACH, nx, ny, 1.0 / 6.0)
+    tb = dg2d.build_tables(1)
+    setup = dg2d.DoubleMachSetup()
+    ctx = dg2d.SolverContext(mesh, tb, bc=dg2d.double_mach_boundary(setup),
+                             options=dg2d.SolverOptions(rk_order=2, cfl=0.3, limiting=True), device=local)
+    c0 = dg2d.limit(ctx, dg2d.project_initial(lambda xy: dg2d.double_mach_initial(xy, setup), mesh, tb))
+    h = ctx.handle
+    stream = torch.cuda.Stream(device=local)
+    dg2d._check(L.lib.dgb_set_stream(h, C.c_void_p(stream.cuda_stream)))
+    ctx.upload(L.SLOT_STATE, c0)
+    res = C.c_double()
+    dg2d._check(L.lib.dgb_run_fixed_steps(h, 2, 0.3, 1, args.warmup, C.byref(res), None))
+    L.lib.dgb_reset_timers(h)
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    dg2d._check(L.lib.dgb_run_fixed_steps(h, 2, 0.3, 1, args.steps, C.byref(res), None))
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    t = L.PassTimers()
+    dg2d._check(L.lib.dgb_timers(h, C.byref(t)))
+    N = mesh.n_elements()
+    upd = 4 * 3 * N * 2 * args.steps
+    ctx.close()
+    return {"workload": f"double Mach reflection {nx}x{ny} channel ({N} triangles), p=1, BJ limiter every "
+                        f"stage, RK2 midpoint, cfl 0.3", "steps": args.steps,
+            "value": upd / (ms * 1e-3), "unit": "DOF-updates/s/stage", "ms_per_step": ms / args.steps,
+            "stage_kernel_ms_per_stage": t.stage * 1e3 / (2 * args.steps),
+            "limiter_ms_per_stage": t.limiter * 1e3 / (2 * args.steps),
+            "limiter_share": t.limiter / max(t.stage + t.limiter + t.other, 1e-30),
+            "vs_paper_gtx580_mesh_c": upd / (ms * 1e-3) / 1.31e8}
 
 
 # ----------------------------------------------------------------------------- CPU reference
@@ -393,6 +438,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-box", dest="cpu_n", type=int, default=708, help="box size of the CPU sample")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--dmr-nx", type=int, default=2000, help="DMR channel cells in x (C4 leg; 0 = skip)")
     ap.add_argument("--same-device", action="store_true",
                     help="test mode: all ranks share cuda:0 (partitioned path on one GPU)")
     args = ap.parse_args()
