@@ -241,14 +241,13 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
             v[0] = 1.0; v[1] = 0.0; v[2] = 0.0; v[3] = 2.5;
             w.inv = 1.0; w.vx = 0.0; w.vy = 0.0; w.p = 1.0;
           }
-          double f1[4], f2[4];
-          euler_flux(v, w, f1, f2);
+          double r_[4], s_[4];
+          contravariant_flux(v, w, ta, tb, tc, td, r_, s_);
           const bool live = k < NQ;  // padded points contribute nothing
 #pragma unroll
           for (int m = 0; m < 4; ++m) {
-            const double r_ = ta * f1[m] + tb * f2[m], s_ = tc * f1[m] + td * f2[m];
-            fr[m][i] = live ? r_ : 0.0;  // contravariant flux along r
-            fs[m][i] = live ? s_ : 0.0;  // along s
+            fr[m][i] = live ? r_[m] : 0.0;  // contravariant flux along r
+            fs[m][i] = live ? s_[m] : 0.0;  // along s
           }
         }
         __syncwarp();
