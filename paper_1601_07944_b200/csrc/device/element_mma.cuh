@@ -47,7 +47,12 @@ struct MmaDim {
   static constexpr int kPheP = kPheR + 3 * KS * 32;         // [3][2][JT][32] surface projection
   static constexpr int kPhm = kPheP + 3 * 2 * JT * 32;      // [3][JT*8] midpoint rows (zero padded)
   static constexpr int kWe = kPhm + 3 * JT * 8;             // [8] edge weights (zero padded)
-  static constexpr int kSize = kWe + 8;
+  // a single trailing interior point (NQ % 8 == 1, p = 5) is done with DFMAs instead of a
+  // whole padded DMMA tile: its basis row (mode 4ks+t at [ks][t]) and weighted gradient rows
+  static constexpr bool kTail1 = (NQ % 8) == 1;
+  static constexpr int NTD = kTail1 ? NQ / 8 : NT;  // point tiles done with DMMA
+  static constexpr int kTail = kWe + 8;                     // [KS*4] phi, [JT*8] w dr, [JT*8] w ds
+  static constexpr int kSize = kTail + (kTail1 ? KS * 4 + 2 * JT * 8 : 0);
   // per-warp staging after the tables: own [4 KS][32] + neighbour [4 KS][32]
   static constexpr int kWarpBuf = 2 * 4 * KS * 32;
 };
@@ -223,12 +228,13 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
           for (int m = 0; m < 4; ++m) dmma(u[m], w_own[(m * KS + ks) * 32 + lane], b);
         }
       };
+      constexpr int NTD = D::NTD;
       interp(U[0], 0);
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
+      for (int nt = 0; nt < NTD; ++nt) {
         // software pipeline: the next tile of points is interpolated while this
         // tile's fluxes are evaluated
-        if (nt + 1 < NT) interp(U[(nt + 1) & 1], nt + 1);
+        if (nt + 1 < NTD) interp(U[(nt + 1) & 1], nt + 1);
         double fr[4][2], fs[4][2];
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
@@ -267,6 +273,39 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
 #pragma unroll
             for (int m = 0; m < 4; ++m) dmma(R[m][jt], fs[m][i], bs);
           }
+      }
+      if constexpr (D::kTail1) {
+        // the last interior point: the 4 lanes of an element reduce their modes' share
+        // of the interpolation, all 4 evaluate the flux, each projects onto its own modes
+        constexpr int k = NQ - 1;
+        double v[4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          double sum = 0.0;
+#pragma unroll
+          for (int ks = 0; ks < KS; ++ks) sum = fma(w_own[(m * KS + ks) * 32 + lane], smem[D::kTail + ks * 4 + t], sum);
+          sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+          sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+          v[m] = sum;
+        }
+        Prim w = primitives(v, g1);
+        if (!admissible(v, w)) {
+          if (valid && t == 0) record_error(sc, err_key(a.seq, kPassVolume, __ldg(geo.ref_id + e), k));
+          v[0] = 1.0; v[1] = 0.0; v[2] = 0.0; v[3] = 2.5;  // placeholder (solver.cpp:129-132)
+          w.inv = 1.0; w.vx = 0.0; w.vy = 0.0; w.p = 1.0;
+        }
+        double fr[4], fs[4];
+        contravariant_flux(v, w, ta, tb, tc, td, fr, fs);
+#pragma unroll
+        for (int jt = 0; jt < JT; ++jt)
+#pragma unroll
+          for (int ii = 0; ii < 2; ++ii) {
+            const int jj = 8 * jt + 2 * t + ii;
+            const double dr = smem[D::kTail + KS * 4 + jj], ds = smem[D::kTail + KS * 4 + JT * 8 + jj];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) R[m][jt][ii] = fma(dr, fr[m], fma(ds, fs[m], R[m][jt][ii]));
+          }
+        __syncwarp();
       }
     }
 
@@ -559,6 +598,14 @@ inline void fill_mma_tab(const Tab<P>& T, double* out) {
   for (int q = 0; q < 3; ++q)
     for (int j = 0; j < NP; ++j) out[D::kPhm + q * JT * 8 + j] = T.phm[q][j];
   for (int k = 0; k < K; ++k) out[D::kWe + k] = T.we[k];
+  if (D::kTail1) {
+    const int k = NQ - 1;
+    for (int j = 0; j < NP; ++j) {
+      out[D::kTail + j] = T.phi[k][j];  // mode j = 4ks + t sits at ks*4 + t
+      out[D::kTail + KS * 4 + j] = T.drw[k][j];
+      out[D::kTail + KS * 4 + JT * 8 + j] = T.dsw[k][j];
+    }
+  }
 }
 
 }  // namespace dgbk
