@@ -142,15 +142,3 @@ cudaError_t Launch<DGB_P>::dt(int grid, const Geo& g, const double* c, Scalars* 
 }
 
 }  // namespace dgbk
-
-#ifdef DGB_PHASE_TIMING
-#define DGB_CAT2(a, b) a##b
-#define DGB_CAT(a, b) DGB_CAT2(a, b)
-// tuning builds: read and clear the phase counters of this degree's DMMA kernel
-extern "C" int DGB_CAT(dgb_debug_phase_p, DGB_P)(unsigned long long* out) {
-  if (cudaMemcpyFromSymbol(out, dgbk::g_phase, sizeof(unsigned long long) * 8) != cudaSuccess) return 4;
-  unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  cudaMemcpyToSymbol(dgbk::g_phase, z, sizeof z);
-  return 0;
-}
-#endif
