@@ -259,3 +259,49 @@ def test_two_processes_ipc_halo_exchange_bit_identical():
     assert all(o[3] == "" for o in out), out
     assert np.array_equal(out[0][1], ref.coeffs)
     assert out[0][2] == res_ref and out[1][2] == res_ref
+
+
+@pytest.mark.gpu
+def test_eight_partitions_roe_flux_bit_identical():
+    """kMaxRanks = 8 partitions of one mesh (the 8xB200 box) with the Roe flux, in one process."""
+    mesh, tb, bc, c0 = _problem("periodic", 3)
+    opts = dg2d.SolverOptions(scheme=L.SSP_RK3, cfl=0.3, flux="roe")
+    ref, res_ref = _whole(mesh, tb, bc, c0, opts, 6)
+    parts = [D.PartContext(mesh, tb, r, 8, options=opts, device=0) for r in range(8)]
+    for q in parts:
+        q.set_timeout(30.0)
+    D.connect_local(parts)
+    st = dg2d.SolverState(c0.copy())
+    res = D.run_fixed_steps_group(parts, st, 6)
+    assert np.array_equal(st.coeffs, ref.coeffs) and res == res_ref
+    for q in parts:
+        q.close()
+
+
+@pytest.mark.gpu
+def test_partition_run_to_steady_matches_whole_mesh():
+    """run_to_steady (solver.cpp:559-579) on the supersonic vortex, 3 partitions: the global
+    residual decides the stop, so every rank takes the same number of steps."""
+    mesh, tb, bc, c0 = _problem("vortex", 2)
+    opts = dg2d.SolverOptions(rk_order=4, cfl=0.9)
+    ctx = dg2d.SolverContext(mesh, tb, bc=bc, options=opts, device=0)
+    ref = dg2d.SolverState(c0.copy())
+    sr = dg2d.run_to_steady(ctx, ref, 1e-9, 20_000)
+    assert sr.converged
+    parts = [D.PartContext(mesh, tb, r, 3, bc=bc, options=opts, device=0) for r in range(3)]
+    D.connect_local(parts)
+    for q in parts:
+        q.upload(L.SLOT_STATE, c0)
+
+    def go(q):
+        import ctypes as C
+        n, r, conv = C.c_int64(), C.c_double(), C.c_int()
+        dg2d._check(L.lib.dgb_run_to_steady(q.handle, 4, 0.9, 0, 1e-9, 20_000, C.byref(n), C.byref(r),
+                                            C.byref(conv), None, 0))
+        return n.value, r.value, conv.value
+    outs = D.run_group(parts, go)
+    assert all(o == (sr.steps, sr.residual, 1) for o in outs), (outs, sr)
+    out = np.empty_like(c0)
+    for q in parts:
+        out[:, :, q.owned] = q.download(L.SLOT_STATE)
+    assert np.array_equal(out, ref.coeffs)
