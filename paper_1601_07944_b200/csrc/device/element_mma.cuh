@@ -52,9 +52,19 @@ struct MmaDim {
   static constexpr bool kTail1 = (NQ % 8) == 1;
   static constexpr int NTD = kTail1 ? NQ / 8 : NT;  // point tiles done with DMMA
   static constexpr int kTail = kWe + 8;                     // [KS*4] phi, [JT*8] w dr, [JT*8] w ds
-  static constexpr int kSize = kTail + (kTail1 ? KS * 4 + 2 * JT * 8 : 0);
-  // per-warp staging after the tables: own [4 KS][32] + neighbour [4 KS][32]
-  static constexpr int kWarpBuf = 2 * 4 * KS * 32;
+  // Packed surface (K <= 5, i.e. p = 3, 4): the 3K edge points of the three sides share
+  // NSP = ceil(3K/8) column tiles instead of one padded tile per side, so fewer flux
+  // evaluations, own-trace and projection DMMAs.  Column c of tile s is point 8s + c =
+  // (side (8s+c) / K, point (8s+c) % K).
+  static constexpr int NSP = (3 * K + 7) / 8;
+  static constexpr bool kPacked = NSP < 3;
+  static constexpr int kPkOwn = kTail + (kTail1 ? KS * 4 + 2 * JT * 8 : 0);  // [NSP][KS][32]
+  static constexpr int kPkNb = kPkOwn + (kPacked ? NSP * KS * 32 : 0);      // [NSP][3 sides][3 classes][KS][32]
+  static constexpr int kPkProj = kPkNb + (kPacked ? NSP * 9 * KS * 32 : 0);  // [NSP][2][JT][32]
+  static constexpr int kSize = kPkProj + (kPacked ? NSP * 2 * JT * 32 : 0);
+  // per-warp staging after the tables: own [4 KS][32] + neighbour [4 KS][32] (two
+  // neighbour buffers when the surface is packed: a tile spans two sides)
+  static constexpr int kWarpBuf = (kPacked ? 3 : 2) * 4 * KS * 32;
 };
 
 // volatile: a non-volatile asm may be duplicated into both arms of a per-lane
@@ -160,8 +170,11 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
   const int nwarps = gridDim.x * (blockDim.x >> 5);
   const int ntiles = (a.e1 - a.e0 + 7) >> 3;
   // per-warp staging: own coefficients of the tile, neighbour coefficients of one side
-  double* __restrict__ w_own = smem + D::kSize + wib * 2 * FR;
+  double* __restrict__ w_own = smem + D::kSize + wib * D::kWarpBuf;
   double* __restrict__ w_nbr = w_own + FR;
+  // packed surface (p = 3, 4): a second neighbour buffer, side q lives in buffer q & 1
+  constexpr bool kPk = D::kPacked && (MODE == kModeRhs || MODE == kModeStage);
+  double* __restrict__ w_nbr2 = w_own + 2 * FR;
 
   double lam_min = __longlong_as_double(0x7ff0000000000000ll);
   double res_max = 0.0;
@@ -184,6 +197,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
 #pragma unroll
       for (int q = 0; q < 3; ++q) nbq[q] = nbr_of(e, q);
       fetch_frag<NP, KS>(w_nbr, a.in, ld, nbq[0], ok && nbq[0] >= 0, lane, t);
+      if constexpr (kPk) fetch_frag<NP, KS>(w_nbr2, a.in, ld, nbq[1], ok && nbq[1] >= 0, lane, t);
     }
     cp_async_commit();
   }
@@ -310,7 +324,106 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
     }
 
     // ------------------------------------------------------------ surface
-    if constexpr (MODE != kModeVolume) {
+    if constexpr (kPk) {
+      double enx[3], eny[3], eh[3];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        enx[q] = __ldg(geo.enx + edq[q]);
+        eny[q] = __ldg(geo.eny + edq[q]);
+        eh[q] = __ldg(geo.eh + edq[q]);
+      }
+      auto sel3 = [](int q, auto x0, auto x1, auto x2) { return q == 0 ? x0 : (q == 1 ? x1 : x2); };
+#pragma unroll
+      for (int sp = 0; sp < D::NSP; ++sp) {
+        if (sp > 0) cp_async_wait<0>();  // side 2's neighbour column (prefetched during tile 0)
+        // own trace of the packed tile
+        double Tw[4][2], Tn[4][2];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) Tw[m][0] = Tw[m][1] = Tn[m][0] = Tn[m][1] = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+          const double b = smem[D::kPkOwn + (sp * KS + ks) * 32 + lane];
+#pragma unroll
+          for (int m = 0; m < 4; ++m) dmma(Tw[m], w_own[(m * KS + ks) * 32 + lane], b);
+        }
+        // neighbour traces of the sides present in this tile (their columns only)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          if (q * K >= 8 * (sp + 1) || (q + 1) * K <= 8 * sp) continue;  // side q not in tile sp
+          const double* __restrict__ nbuf = (q & 1) ? w_nbr2 : w_nbr;
+          const int snb_q = nbq[q] < 0 ? 0 : ((inf >> (2 * q)) & 3);
+          unsigned todo = __reduce_or_sync(0xffffffffu, snb_q ? (1u << snb_q) : 0u);
+          while (todo) {
+            const int cls = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const bool mine = snb_q == cls;
+#pragma unroll
+            for (int ks = 0; ks < KS; ++ks) {
+              const double b = smem[D::kPkNb + (((sp * 3 + q) * 3 + (cls - 1)) * KS + ks) * 32 + lane];
+#pragma unroll
+              for (int m = 0; m < 4; ++m) {
+                const double an = nbuf[(m * KS + ks) * 32 + lane];
+                dmma(Tn[m], mine ? an : 0.0, b);
+              }
+            }
+          }
+        }
+        __syncwarp();
+        // buffers consumed: tile 0 frees side 0's buffer (side 2 goes there); the last
+        // tile frees everything (the next tile's sides 0, 1 and own coefficients)
+        if (sp + 1 < D::NSP) {
+          fetch_frag<NP, KS>(w_nbr, a.in, ld, nbq[2], valid && nbq[2] >= 0, lane, t);
+        } else {
+          fetch_frag<NP, KS>(w_nbr, a.in, ld, nbn[0], nvalid && nbn[0] >= 0, lane, t);
+          fetch_frag<NP, KS>(w_nbr2, a.in, ld, nbn[1], nvalid && nbn[1] >= 0, lane, t);
+          fetch_frag<NP, KS>(w_own, a.in, ld, e_next, nvalid, lane, t);
+        }
+        cp_async_commit();
+        // numerical flux at this lane's two packed points, canonical orientation
+        double fn[4][2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int pt = 8 * sp + 2 * t + i;
+          const bool live = pt < 3 * K;
+          const int q = live ? pt / K : 0, ko = live ? pt % K : 0;
+          const int nb = sel3(q, nbq[0], nbq[1], nbq[2]);
+          const int ed = sel3(q, edq[0], edq[1], edq[2]);
+          const double nx = sel3(q, enx[0], enx[1], enx[2]), ny = sel3(q, eny[0], eny[1], eny[2]);
+          const double h = sel3(q, eh[0], eh[1], eh[2]);
+          const bool left = (inf >> (6 + q)) & 1;
+          const bool bnd = nb < 0;
+          double UL[4], UR[4];
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            UL[m] = left ? Tw[m][i] : Tn[m][i];
+            UR[m] = left ? Tn[m][i] : Tw[m][i];
+          }
+          const int kc = left ? ko : K - 1 - ko;  // canonical (left-element) point index
+          if (bnd && live) ghost_state<K>(UL, nb, ed, kc, nx, ny, tstage, geo, UR);
+          const Prim wl = primitives(UL, g1), wr = primitives(UR, g1);
+          double f[4];
+          if (admissible(UL, wl) && admissible(UR, wr)) {
+            num_flux(geo.flux, UL, wl, UR, wr, nx, ny, gamma, f);
+          } else {
+            if (valid && live) record_error(sc, err_key(a.seq, kPassSurface, ed, kc));
+#pragma unroll
+            for (int m = 0; m < 4; ++m) f[m] = 0.0;
+          }
+          const double wh = live ? h * smem[D::kWe + kc] : 0.0;
+#pragma unroll
+          for (int m = 0; m < 4; ++m) fn[m][i] = left ? -(wh * f[m]) : (wh * f[m]);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int jt = 0; jt < JT; ++jt) {
+            const double b = smem[D::kPkProj + ((sp * 2 + i) * JT + jt) * 32 + lane];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) dmma(R[m][jt], fn[m][i], b);
+          }
+      }
+    } else if constexpr (MODE != kModeVolume) {
       double enx[3], eny[3], eh[3];
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
@@ -598,6 +711,28 @@ inline void fill_mma_tab(const Tab<P>& T, double* out) {
   for (int q = 0; q < 3; ++q)
     for (int j = 0; j < NP; ++j) out[D::kPhm + q * JT * 8 + j] = T.phm[q][j];
   for (int k = 0; k < K; ++k) out[D::kWe + k] = T.we[k];
+  if (D::kPacked) {
+    for (int sp = 0; sp < D::NSP; ++sp)
+      for (int lane = 0; lane < 32; ++lane) {
+        const int g = lane >> 2, t = lane & 3;
+        for (int ks = 0; ks < KS; ++ks) {
+          const int j = 4 * ks + t, pt = 8 * sp + g;  // B[row t = mode][col g = packed point]
+          const bool okc = j < NP && pt < 3 * K;
+          const int q = okc ? pt / K : 0, ko = okc ? pt % K : 0;
+          out[D::kPkOwn + (sp * KS + ks) * 32 + lane] = okc ? T.phe[q][ko][j] : 0.0;
+          for (int qq = 0; qq < 3; ++qq)
+            for (int cls = 0; cls < 3; ++cls)  // neighbour side label cls+1, reversed points
+              out[D::kPkNb + (((sp * 3 + qq) * 3 + cls) * KS + ks) * 32 + lane] =
+                  (okc && q == qq) ? T.phe[cls][K - 1 - ko][j] : 0.0;
+        }
+        for (int i = 0; i < 2; ++i)
+          for (int jt = 0; jt < JT; ++jt) {
+            const int pt = 8 * sp + 2 * t + i, j = 8 * jt + g;  // B[row t = k slot][col g = mode]
+            const bool ok = pt < 3 * K && j < NP;
+            out[D::kPkProj + ((sp * 2 + i) * JT + jt) * 32 + lane] = ok ? T.phe[pt / K][pt % K][j] : 0.0;
+          }
+      }
+  }
   if (D::kTail1) {
     const int k = NQ - 1;
     for (int j = 0; j < NP; ++j) {
