@@ -288,30 +288,6 @@ __device__ __forceinline__ void neighbour_trace(const Tab<P>& T, const double* _
   }
 }
 
-// Same trace as neighbour_trace, from a neighbour column already in registers.
-template <int P, int S>
-__device__ __forceinline__ void trace_from_regs(const Tab<P>& T, const double (&cn)[4][Dim<P>::NP],
-                                                double (&un)[Dim<P>::K][4]) {
-  constexpr int NP = Dim<P>::NP, K = Dim<P>::K;
-#pragma unroll
-  for (int j = 0; j < NP; ++j)
-#pragma unroll
-    for (int mm = 0; mm < 4; ++mm)
-#pragma unroll
-      for (int ko = 0; ko < K; ++ko) {
-        const double ph = T.phe[S][K - 1 - ko][j];
-        un[ko][mm] = (j == 0) ? ph * cn[mm][j] : fma(ph, cn[mm][j], un[ko][mm]);
-      }
-}
-
-template <int NP>
-__device__ __forceinline__ void load_column(const double* __restrict__ in, long long ld, int col, double (&cn)[4][NP]) {
-#pragma unroll
-  for (int m = 0; m < 4; ++m)
-#pragma unroll
-    for (int j = 0; j < NP; ++j) cn[m][j] = col >= 0 ? __ldg(in + (static_cast<long long>(m) * NP + j) * ld + col) : 0.0;
-}
-
 // 4x4 transpose across the 4 lanes of an element group: on entry lane g holds
 // v[i] = (variable g) at point i; on exit lane g holds v[m] = (variable m) at
 // point g.  Two butterfly rounds, 4 double shuffles.
@@ -366,9 +342,6 @@ __device__ __forceinline__ void push_element(const Geo& geo, const PeerTab* __re
 #define DGB_G1_SIDE_UNROLL 1  // sides of the one-thread-per-element kernel: runtime loop
 #endif
 constexpr int kG1SideUnroll = DGB_G1_SIDE_UNROLL;
-#ifndef DGB_G1_HOIST_MAXP
-#define DGB_G1_HOIST_MAXP 0  // degrees whose one-thread kernel pipelines the neighbour columns
-#endif
 #ifndef DGB_G1_MAXP
 #define DGB_G1_MAXP 2
 #endif
@@ -741,20 +714,6 @@ __device__ __forceinline__ void element_body_g1(const Tab<P>& T, const Geo& geo,
 #pragma unroll
       for (int j = 0; j < NP; ++j) acc[m][j] = 0.0;
 
-    // side indices and the first side's neighbour column are requested before
-    // the volume integral so their latency overlaps it
-    constexpr bool kHoist = (MODE != kModeVolume) && (P <= DGB_G1_HOIST_MAXP);
-    int nbv[3] = {0, 0, 0}, edv[3] = {0, 0, 0};
-    double cnext[4][NP];
-    if constexpr (kHoist) {
-#pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        nbv[q] = __ldg(geo.nbr + q * ld + e);
-        edv[q] = __ldg(geo.eid + q * ld + e);
-      }
-      load_column<NP>(a.in, ld, nbv[0], cnext);
-    }
-
     // ------------------------------------------------------------ volume
     if constexpr (MODE != kModeSurface) {
       const double ta = __ldg(geo.tau + e), tb = __ldg(geo.tau + ld + e);
@@ -789,33 +748,14 @@ __device__ __forceinline__ void element_body_g1(const Tab<P>& T, const Geo& geo,
       const int inf = __ldg(geo.info + e);
 #pragma unroll kG1SideUnroll
       for (int q = 0; q < 3; ++q) {
-        int nb, ed;
-        if constexpr (kHoist) {
-          nb = nbv[q];
-          ed = edv[q];
-        } else {
-          nb = __ldg(geo.nbr + q * ld + e);
-          ed = __ldg(geo.eid + q * ld + e);
-        }
+        const int nb = __ldg(geo.nbr + q * ld + e);
+        const int ed = __ldg(geo.eid + q * ld + e);
         const int snb = (inf >> (2 * q)) & 3;
         const bool left = (inf >> (6 + q)) & 1;
         const double nx = __ldg(geo.enx + ed), ny = __ldg(geo.eny + ed), h = __ldg(geo.eh + ed);
         const bool bnd = nb < 0;
         double un[K][4];
-        if constexpr (kHoist) {
-          // this side's neighbour column is in registers; start the next side's loads
-          double cn[4][NP];
-#pragma unroll
-          for (int m = 0; m < 4; ++m)
-#pragma unroll
-            for (int j = 0; j < NP; ++j) cn[m][j] = cnext[m][j];
-          if (q < 2) load_column<NP>(a.in, ld, q == 0 ? nbv[1] : nbv[2], cnext);
-          switch (snb) {
-            case 1: trace_from_regs<P, 0>(T, cn, un); break;
-            case 2: trace_from_regs<P, 1>(T, cn, un); break;
-            default: trace_from_regs<P, 2>(T, cn, un); break;
-          }
-        } else if (!bnd) {
+        if (!bnd) {
           switch (snb) {
             case 1: neighbour_trace<P, 0, 4>(T, a.in, ld, 0, nb, un); break;
             case 2: neighbour_trace<P, 1, 4>(T, a.in, ld, 0, nb, un); break;
