@@ -694,6 +694,63 @@ inline SolverState load_checkpoint(const std::string& path) {
   return s;
 }
 
+// output.cpp:30-65 — legacy VTK with 3 corner points per cell (corner states evaluated on the device)
+inline void export_vtk(const SolverContext& ctx, const CoefficientArray& coeffs, const std::string& path) {
+  const Mesh& mesh = *ctx.mesh;
+  const BasisTables& tb = *ctx.tables;
+  const int n = mesh.n_elements();
+  std::vector<double> phic(3 * static_cast<size_t>(tb.n_p)), st(12 * static_cast<size_t>(n));
+  const double corner[3][2] = {{0.0, 0.0}, {1.0, 0.0}, {0.0, 1.0}};
+  for (int c = 0; c < 3; ++c)
+    for (int j = 0; j < tb.n_p; ++j)
+      detail::check(dgb_eval_basis(tb.p, j, corner[c][0], corner[c][1], &phic[c * tb.n_p + j], nullptr, nullptr));
+  detail::upload(ctx, DGB_SLOT_INPUT, coeffs);
+  detail::check(dgb_corner_states(ctx.handle(), DGB_SLOT_INPUT, phic.data(), st.data()));
+  std::ofstream out(path);
+  if (!out) throw std::runtime_error("cannot open output file '" + path + "'");
+  out.precision(12);
+  out << "# vtk DataFile Version 3.0\ndg2d solution\nASCII\nDATASET UNSTRUCTURED_GRID\n";
+  out << "POINTS " << 3 * n << " double\n";
+  for (int i = 0; i < n; ++i)
+    for (int c = 0; c < 3; ++c) {
+      const Vec2 v = mesh.vertex_of(i, c);
+      out << v.x << ' ' << v.y << " 0\n";
+    }
+  out << "CELLS " << n << ' ' << 4 * n << "\n";
+  for (int i = 0; i < n; ++i) out << "3 " << 3 * i << ' ' << 3 * i + 1 << ' ' << 3 * i + 2 << "\n";
+  out << "CELL_TYPES " << n << "\n";
+  for (int i = 0; i < n; ++i) out << "5\n";
+  out << "POINT_DATA " << 3 * n << "\n";
+  const char* names[5] = {"rho", "rho_u", "rho_v", "E", "p"};
+  for (int field = 0; field < 5; ++field) {
+    out << "SCALARS " << names[field] << " double 1\nLOOKUP_TABLE default\n";
+    for (size_t k = 0; k < 3 * static_cast<size_t>(n); ++k) {
+      const EulerState u{st[4 * k], st[4 * k + 1], st[4 * k + 2], st[4 * k + 3]};
+      out << (field < kEq ? u[field] : pressure(u, ctx.gas)) << "\n";
+    }
+  }
+  if (!out) throw std::runtime_error("failed writing '" + path + "'");
+}
+
+// output.cpp:67-81 — one row per cell: centroid, cell means, pressure
+inline void export_csv(const SolverContext& ctx, const CoefficientArray& coeffs, const std::string& path) {
+  const Mesh& mesh = *ctx.mesh;
+  std::ofstream out(path);
+  if (!out) throw std::runtime_error("cannot open output file '" + path + "'");
+  out.precision(12);
+  const double sqrt2 = std::sqrt(2.0);
+  out << "x,y,rho,rho_u,rho_v,E,p\n";
+  for (int i = 0; i < mesh.n_elements(); ++i) {
+    const Vec2 a = mesh.vertex_of(i, 0), b = mesh.vertex_of(i, 1), c = mesh.vertex_of(i, 2);
+    const double cx = (1.0 / 3.0) * (a.x + b.x + c.x), cy = (1.0 / 3.0) * (a.y + b.y + c.y);
+    EulerState mean;
+    for (int m = 0; m < kEq; ++m) mean[m] = coeffs.at(m, 0, i) * sqrt2;
+    out << cx << ',' << cy << ',' << mean.rho << ',' << mean.mx << ',' << mean.my << ',' << mean.E << ','
+        << pressure(mean, ctx.gas) << "\n";
+  }
+  if (!out) throw std::runtime_error("failed writing '" + path + "'");
+}
+
 // solver.cpp:662-678 — deterministic host reductions
 inline double total_mass(const Mesh& mesh, const CoefficientArray& c) {
   const double inv_sqrt2 = 1.0 / std::sqrt(2.0);

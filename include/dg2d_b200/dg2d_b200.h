@@ -179,6 +179,10 @@ int dgb_total_mass(dgb_ctx* ctx, int slot, double* mass);
  * order.  For a partitioned context: the rank's partial sum of squares (exact_rho over its owned
  * elements, ascending id); the caller adds the ranks in rank order and takes the square root. */
 int dgb_l2_error(dgb_ctx* ctx, int slot, const double* exact_rho, double* l2);
+/* Output extraction for export_vtk (output.cpp:10-20, 30-65): the conserved state at the three
+ * corners (reference coordinates (0,0), (1,0), (0,1)) of every owned element,
+ * out[(i*3 + c)*4 + m]; phi_corner[c*n_p + j] = eval_basis(p, j, corner c). */
+int dgb_corner_states(dgb_ctx* ctx, int slot, const double* phi_corner, double* out);
 /* max_abs_diff (solver.cpp:672-678). */
 int dgb_max_abs_diff(dgb_ctx* ctx, int slot_a, int slot_b, double* diff);
 

@@ -458,6 +458,14 @@ class RefSolver:
         return self.lib.ref_total_mass(self.h, _d(np.ascontiguousarray(c)))
 
 
+def ref_export(mesh: "RefMesh", tables: "RefTables", coeffs, path, csv=False, gamma=1.4):
+    """The reference's export_vtk / export_csv (output.cpp:30-81) on the same coefficients."""
+    lib = ref_lib()
+    lib.ref_export.argtypes = [C.c_void_p, C.c_void_p, C.c_double, dp, C.c_int, C.c_char_p]
+    c = np.ascontiguousarray(coeffs, np.float64)
+    _rchk(lib.ref_export(mesh.h, tables.h, gamma, _d(c), int(csv), path.encode()))
+
+
 def ref_project(mesh: RefMesh, tables: RefTables, kind, params, gamma=1.4):
     out = np.zeros((4, tables.n_p, mesh.ne))
     p = (C.c_double * max(1, len(params)))(*params)

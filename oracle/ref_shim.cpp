@@ -16,6 +16,7 @@
 #include <omp.h>
 #endif
 
+#include "dg2d/output.hpp"
 #include "dg2d/problems.hpp"
 #include "dg2d/reference.hpp"
 #include "dg2d/solver.hpp"
@@ -572,6 +573,20 @@ int ref_project(void* mp, void* tp, double gamma, int kind, const double* prm, d
     }
     CoefficientArray c = project_initial(f, mesh, tb, gas);
     std::memcpy(out, c.data.data(), c.data.size() * 8);
+  });
+}
+
+// --------------------------------------------------------------- output (output.cpp:30-81)
+int ref_export(void* mp, void* tp, double gamma, const double* c, int csv, const char* path) {
+  const Mesh& mesh = *static_cast<Mesh*>(mp);
+  const BasisTables& tb = *static_cast<BasisTables*>(tp);
+  return guard([&] {
+    CoefficientArray a(kEq, tb.n_p, mesh.n_elements());
+    std::memcpy(a.data.data(), c, a.data.size() * 8);
+    if (csv)
+      export_csv(a, mesh, tb, GasModel{gamma}, path);
+    else
+      export_vtk(a, mesh, tb, GasModel{gamma}, path);
   });
 }
 

@@ -201,6 +201,21 @@ __global__ void k_l2_partial(const double* __restrict__ c, const double* __restr
   }
 }
 
+// Output extraction (output.cpp:10-20, 30-65): the state at the three corners of every
+// owned element, out[(i * 3 + c) * 4 + m] (reference order), same j order as corner_state.
+__global__ void k_corner_states(const double* __restrict__ c, const double* __restrict__ phic /* [3][np] */,
+                                const int* __restrict__ cmp, int n, int ld, int np, double* __restrict__ out) {
+  for (int d = blockIdx.x * blockDim.x + threadIdx.x; d < n; d += gridDim.x * blockDim.x) {
+    const long long i = cmp[d];
+    for (int cc = 0; cc < 3; ++cc)
+      for (int m = 0; m < 4; ++m) {
+        double s = 0.0;
+        for (int j = 0; j < np; ++j) s = fma(c[(static_cast<long long>(m) * np + j) * ld + d], phic[cc * np + j], s);
+        out[(i * 3 + cc) * 4 + m] = s;
+      }
+  }
+}
+
 __global__ void k_max_abs_diff(const double* __restrict__ a, const double* __restrict__ b, int n, int ld, int rows,
                                unsigned long long* out) {
   const long long total = static_cast<long long>(rows) * ld;
@@ -1630,6 +1645,23 @@ int dgb_l2_error(dgb_ctx* c, int slot, const double* exact_rho, double* l2) {
     double total = 0.0;  // element order (runner.cpp:146-148); a partition returns its partial sum squared
     for (int i = 0; i < n; ++i) total += hp[i];
     *l2 = c->partitioned ? total : std::sqrt(total);
+    return DGB_OK;
+  });
+}
+
+int dgb_corner_states(dgb_ctx* c, int slot, const double* phi_corner, double* out) {
+  return guarded([&] {
+    set_device(c);
+    if (!phi_corner || !out) throw Fail{DGB_ERR_ARG, "null argument"};
+    DevBuf<double> tab, dev;
+    tab.upload(phi_corner, 3 * static_cast<size_t>(c->np), c->stream);
+    dev.alloc(12 * static_cast<size_t>(c->N));
+    k_corner_states<<<small_grid(c->N), 256, 0, c->stream>>>(slot_ptr(c, slot), tab.p, c->d_cmp.p, c->N, c->ld, c->np,
+                                                             dev.p);
+    CU(cudaGetLastError());
+    ++c->launches;
+    CU(cudaMemcpyAsync(out, dev.p, sizeof(double) * 12 * c->N, cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
     return DGB_OK;
   });
 }

@@ -937,6 +937,67 @@ def convergence_study(p: int, letters: str = "A,B,C,D", rk_order: int = 4, cfl: 
     return rows
 
 
+# ----------------------------------------------------------------------------- output (output.cpp)
+def _g12(x: float) -> str:
+    """std::ostream << double with precision(12) (output.cpp:22-27): printf %.12g."""
+    return "%.12g" % x
+
+
+def _pressure_ref(u, gamma):
+    return (gamma - 1.0) * (u[..., 3] - 0.5 * (u[..., 1] * u[..., 1] + u[..., 2] * u[..., 2]) / u[..., 0])
+
+
+def export_vtk(ctx: SolverContext, coeffs, path: str):
+    """output.cpp:30-65: legacy VTK, 3 corner points per cell, point data rho, rho_u, rho_v, E, p;
+    the corner states are evaluated on the device."""
+    mesh, tb = ctx.mesh, ctx.tables
+    n = mesh.n_elements()
+    phic = np.ascontiguousarray([[eval_basis(tb.p, j, rs) for j in range(tb.n_p)]
+                                 for rs in ((0.0, 0.0), (1.0, 0.0), (0.0, 1.0))], np.float64)
+    ctx.upload(L.SLOT_INPUT, coeffs)
+    st = np.empty((n, 3, 4))
+    _check(lib.dgb_corner_states(ctx.handle, L.SLOT_INPUT, dptr(phic), dptr(st)))
+    pr = _pressure_ref(st, ctx.gas.gamma)
+    ev = mesh.elem_v
+    try:
+        f = open(path, "w")
+    except OSError:
+        raise RuntimeError(f"cannot open output file '{path}'")
+    with f:
+        w = f.write
+        w("# vtk DataFile Version 3.0\ndg2d solution\nASCII\nDATASET UNSTRUCTURED_GRID\n")
+        w(f"POINTS {3 * n} double\n")
+        w("".join(f"{_g12(mesh.vx[v])} {_g12(mesh.vy[v])} 0\n" for v in ev.reshape(-1)))
+        w(f"CELLS {n} {4 * n}\n")
+        w("".join(f"3 {3 * i} {3 * i + 1} {3 * i + 2}\n" for i in range(n)))
+        w(f"CELL_TYPES {n}\n" + "5\n" * n)
+        w(f"POINT_DATA {3 * n}\n")
+        for k, name in enumerate(("rho", "rho_u", "rho_v", "E", "p")):
+            vals = st[:, :, k] if k < 4 else pr
+            w(f"SCALARS {name} double 1\nLOOKUP_TABLE default\n")
+            w("".join(_g12(x) + "\n" for x in vals.reshape(-1)))
+
+
+def export_csv(ctx: SolverContext, coeffs, path: str):
+    """output.cpp:67-81: one row per cell: centroid, cell means (constant mode x sqrt 2), p."""
+    mesh = ctx.mesh
+    c = np.asarray(coeffs)
+    sqrt2 = math.sqrt(2.0)
+    mean = np.stack([c[m, 0] * sqrt2 for m in range(4)], 1)
+    pr = _pressure_ref(mean, ctx.gas.gamma)
+    ev = mesh.elem_v
+    cx = (1.0 / 3.0) * (mesh.vx[ev[:, 0]] + mesh.vx[ev[:, 1]] + mesh.vx[ev[:, 2]])
+    cy = (1.0 / 3.0) * (mesh.vy[ev[:, 0]] + mesh.vy[ev[:, 1]] + mesh.vy[ev[:, 2]])
+    try:
+        f = open(path, "w")
+    except OSError:
+        raise RuntimeError(f"cannot open output file '{path}'")
+    with f:
+        f.write("x,y,rho,rho_u,rho_v,E,p\n")
+        f.write("".join(",".join(_g12(v) for v in (cx[i], cy[i], *mean[i], pr[i])) + "\n"
+                        for i in range(mesh.n_elements())))
+
+
 def max_abs_diff(a, b) -> float:
     """solver.cpp:672-678"""
     a, b = np.asarray(a), np.asarray(b)

@@ -15,7 +15,10 @@
 #include <sstream>
 #include <string>
 
+#include <fstream>
+
 #include "dg2d/mesh.hpp"
+#include "dg2d/output.hpp"
 #include "dg2d/problems.hpp"
 #include "dg2d/solver.hpp"
 #include "dg2d_b200/dg2d.hpp"
@@ -246,6 +249,41 @@ static void case_operator_seam_and_checkpoint() {
   CHECK(back.coeffs.data == a.coeffs.data, "checkpoint round trip");
 }
 
+static bool files_match(const std::string& a, const std::string& b) {
+  std::ifstream fa(a), fb(b);
+  std::string ta, tb;
+  while (true) {
+    const bool ra = static_cast<bool>(fa >> ta), rb = static_cast<bool>(fb >> tb);
+    if (ra != rb) return false;
+    if (!ra) return true;
+    if (ta == tb) continue;
+    char* ea = nullptr;
+    char* eb = nullptr;
+    const double va = std::strtod(ta.c_str(), &ea), vb = std::strtod(tb.c_str(), &eb);
+    if (*ea || *eb) return false;  // differing non-numeric tokens
+    if (std::fabs(va - vb) > 1e-11 * std::fabs(vb)) return false;
+  }
+}
+
+static void case_output() {
+  std::printf("export_vtk / export_csv (output.cpp:30-81)\n");
+  Pair m = meshes(B::gen_vortex_msh(1));
+  const R::BasisTables rt = R::build_tables(2);
+  const B::BasisTables bt = B::build_tables(2);
+  const B::BoundaryConditions bbc = B::vortex_boundary({}, {});
+  B::SolverContext bc;
+  bc.mesh = &m.bm;
+  bc.tables = &bt;
+  bc.bc = &bbc;
+  R::CoefficientArray c = R::project_initial([](R::Vec2 x) { return R::vortex_exact(x, {}, {}); }, m.rm, rt, {});
+  R::export_vtk(c, m.rm, rt, {}, "/tmp/dg2d_b200_ref.vtk");
+  R::export_csv(c, m.rm, rt, {}, "/tmp/dg2d_b200_ref.csv");
+  B::export_vtk(bc, to_b(c), "/tmp/dg2d_b200_ours.vtk");
+  B::export_csv(bc, to_b(c), "/tmp/dg2d_b200_ours.csv");
+  CHECK(files_match("/tmp/dg2d_b200_ours.vtk", "/tmp/dg2d_b200_ref.vtk"), "vtk files differ");
+  CHECK(files_match("/tmp/dg2d_b200_ours.csv", "/tmp/dg2d_b200_ref.csv"), "csv files differ");
+}
+
 int main() {
   case_connectivity();
   for (int p = 1; p <= 5; ++p) case_rhs(p, 3 + p);
@@ -254,6 +292,7 @@ int main() {
   case_run(1, 2, true, 30);
   case_errors();
   case_operator_seam_and_checkpoint();
+  case_output();
   std::printf(g_fail ? "FAILED %d check(s)\n" : "ALL PASSED\n", g_fail);
   return g_fail ? 1 : 0;
 }

@@ -381,3 +381,37 @@ def test_convergence_rates_match_the_paper():
             assert 4.934e-3 / 3 <= rows[0].error <= 4.934e-3 * 3
         for a, b in zip(rows, rows[1:]):
             assert b.error < a.error
+
+
+# ----------------------------------------------------------------------------- output (output.cpp)
+def _read_numbers(path):
+    toks, nums = [], []
+    for line in open(path):
+        for tok in line.replace(",", " ").split():
+            try:
+                nums.append(float(tok))
+                toks.append("#")
+            except ValueError:
+                toks.append(tok)
+    return toks, np.array(nums)
+
+
+@pytest.mark.parametrize("fmt", ["vtk", "csv"])
+def test_export_matches_reference_output(fmt, tmp_path):
+    """export_vtk / export_csv (output.cpp:30-81): corner states evaluated on the device, same
+    file structure and values (to the 12 printed digits) as the reference's own writer."""
+    if not bind.ref_available():
+        pytest.skip("oracle/_ref not built")
+    rm = bind.RefMesh.generate(L.MESH_VORTEX, 1, 0, 1.0, 1.384)
+    rt = bind.RefTables(2)
+    c = bind.ref_project(rm, rt, 2, (1.0, 1.384, 2.25, 1.0, 1.0))
+    mesh, tb = dg2d.ArrayMesh(rm.export(), rm.nb), rt.as_external()
+    ctx = dg2d.SolverContext(mesh, tb, bc=dg2d.vortex_boundary())
+    ours, ref = str(tmp_path / f"ours.{fmt}"), str(tmp_path / f"ref.{fmt}")
+    (dg2d.export_csv if fmt == "csv" else dg2d.export_vtk)(ctx, c, ours)
+    bind.ref_export(rm, rt, c, ref, csv=(fmt == "csv"))
+    ta, na = _read_numbers(ours)
+    tr, nr = _read_numbers(ref)
+    assert ta == tr
+    assert np.all(np.abs(na - nr) <= 1e-11 * np.maximum(np.abs(nr), 1e-300))
+    ctx.close()
