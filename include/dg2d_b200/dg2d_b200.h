@@ -179,6 +179,11 @@ int dgb_total_mass(dgb_ctx* ctx, int slot, double* mass);
  * order.  For a partitioned context: the rank's partial sum of squares (exact_rho over its owned
  * elements, ascending id); the caller adds the ranks in rank order and takes the square root. */
 int dgb_l2_error(dgb_ctx* ctx, int slot, const double* exact_rho, double* l2);
+/* project_initial (solver.cpp:74-97) on the device, straight into a coefficient slot:
+ * point_states[(i*n_quad + k)*4 + m] at the interior points of every local element (compact
+ * order: reference order for a whole-mesh context; owned then halo ids for a partition).
+ * DGB_ERR_INADMISSIBLE with the reference's message for an inadmissible point state. */
+int dgb_project_slot(dgb_ctx* ctx, int slot, const double* point_states);
 /* Output extraction for export_vtk (output.cpp:10-20, 30-65): the conserved state at the three
  * corners (reference coordinates (0,0), (1,0), (0,1)) of every owned element,
  * out[(i*3 + c)*4 + m]; phi_corner[c*n_p + j] = eval_basis(p, j, corner c). */

@@ -122,6 +122,7 @@ _sig("dgb_total_mass", C.c_int, _vp, C.c_int, c_double_p)
 _sig("dgb_max_abs_diff", C.c_int, _vp, C.c_int, C.c_int, c_double_p)
 _sig("dgb_l2_error", C.c_int, _vp, C.c_int, c_double_p, c_double_p)
 _sig("dgb_corner_states", C.c_int, _vp, C.c_int, c_double_p, c_double_p)
+_sig("dgb_project_slot", C.c_int, _vp, C.c_int, c_double_p)
 _sig("dgb_timers", C.c_int, _vp, C.POINTER(PassTimers))
 _sig("dgb_reset_timers", C.c_int, _vp)
 _sig("dgb_enable_timers", C.c_int, _vp, C.c_int)

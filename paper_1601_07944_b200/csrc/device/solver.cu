@@ -201,6 +201,28 @@ __global__ void k_l2_partial(const double* __restrict__ c, const double* __restr
   }
 }
 
+// project_initial (solver.cpp:74-97) on the device: coefficient (m, j) of element i is
+// sum_k w_k phi[k][j] u_k[m] (orthonormal basis: the mass matrix is detJ I, which cancels
+// against the detJ of the quadrature); ps[(i * nq + k) * 4 + m] in reference order.
+__global__ void k_project(const double* __restrict__ ps, const double* __restrict__ tab /* phi[nq][np], w[nq] */,
+                          const int* __restrict__ cmp, int n, int ld, int np, int nq, double* __restrict__ c,
+                          double gamma, unsigned long long* bad) {
+  for (int d = blockIdx.x * blockDim.x + threadIdx.x; d < n; d += gridDim.x * blockDim.x) {
+    const long long i = cmp[d];
+    for (int m = 0; m < 4; ++m)
+      for (int j = 0; j < np; ++j) {
+        double s = 0.0;
+        for (int k = 0; k < nq; ++k) s += tab[nq * np + k] * tab[k * np + j] * ps[(i * nq + k) * 4 + m];
+        c[(static_cast<long long>(m) * np + j) * ld + d] = s;
+      }
+    for (int k = 0; k < nq; ++k) {  // admissibility, lowest (element, point) wins as on the host
+      const double* u = ps + (i * nq + k) * 4;
+      const double pr = (gamma - 1.0) * (u[3] - 0.5 * (u[1] * u[1] + u[2] * u[2]) / u[0]);
+      if (!(u[0] > 0.0 && pr > 0.0)) atomicMin(bad, static_cast<unsigned long long>(i) * 64 + k);
+    }
+  }
+}
+
 // Output extraction (output.cpp:10-20, 30-65): the state at the three corners of every
 // owned element, out[(i * 3 + c) * 4 + m] (reference order), same j order as corner_state.
 __global__ void k_corner_states(const double* __restrict__ c, const double* __restrict__ phic /* [3][np] */,
@@ -1645,6 +1667,37 @@ int dgb_l2_error(dgb_ctx* c, int slot, const double* exact_rho, double* l2) {
     double total = 0.0;  // element order (runner.cpp:146-148); a partition returns its partial sum squared
     for (int i = 0; i < n; ++i) total += hp[i];
     *l2 = c->partitioned ? total : std::sqrt(total);
+    return DGB_OK;
+  });
+}
+
+int dgb_project_slot(dgb_ctx* c, int slot, const double* point_states) {
+  return guarded([&] {
+    set_device(c);
+    if (!point_states) throw Fail{DGB_ERR_ARG, "null argument"};
+    const int nl = c->N + c->n_halo, nq = c->nq, np = c->np;
+    std::vector<double> h(static_cast<size_t>(nq) * np + nq);
+    std::copy(c->t_phi.begin(), c->t_phi.end(), h.begin());
+    std::copy(c->t_w.begin(), c->t_w.end(), h.begin() + static_cast<size_t>(nq) * np);
+    DevBuf<double> tab, ps;
+    tab.upload(h.data(), h.size(), c->stream);
+    ps.upload(point_states, static_cast<size_t>(nl) * nq * 4, c->stream);
+    double* dst = slot_ptr(c, slot);
+    CU(cudaMemsetAsync(dst, 0, c->coeff_count() * sizeof(double), c->stream));
+    *c->h_red = ~0ull;
+    CU(cudaMemcpyAsync(c->d_red, c->h_red, sizeof(unsigned long long), cudaMemcpyHostToDevice, c->stream));
+    k_project<<<small_grid(nl), 256, 0, c->stream>>>(ps.p, tab.p, c->d_cmp.p, nl, c->ld, np, nq, dst, c->gamma, c->d_red);
+    CU(cudaGetLastError());
+    ++c->launches;
+    CU(cudaMemcpyAsync(c->h_red, c->d_red, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    if (*c->h_red != ~0ull) {
+      const unsigned long long i = *c->h_red / 64, k = *c->h_red % 64;
+      const double* u = point_states + (i * nq + k) * 4;
+      throw Fail{DGB_ERR_INADMISSIBLE, "project_initial: inadmissible state at id " + std::to_string(i) + ", point " +
+                                           std::to_string(k) + " (rho=" + std::to_string(u[0]) +
+                                           ", p=" + std::to_string(pressure_ref(u, c->gamma)) + ")"};
+    }
     return DGB_OK;
   });
 }

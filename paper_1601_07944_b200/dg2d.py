@@ -653,6 +653,14 @@ def project_initial(u0: Callable, mesh: Mesh, tables, gas: GasModel = GasModel()
     return out
 
 
+def project_on_device(ctx: SolverContext, u0: Callable, slot: int = L.SLOT_STATE) -> None:
+    """project_initial (solver.cpp:74-97) evaluated on the device straight into a slot (the
+    point values of ``u0`` are computed on the host, the projection on the GPU)."""
+    xy = interior_points(ctx.mesh, ctx.tables)
+    vals = np.ascontiguousarray(np.asarray(u0(xy.reshape(-1, 2)), np.float64).reshape(-1, 4))
+    _check(lib.dgb_project_slot(ctx.handle, slot, dptr(vals)))
+
+
 def eval_volume_pass(ctx: SolverContext, coeffs) -> np.ndarray:
     ctx.upload(L.SLOT_INPUT, coeffs)
     _check(lib.dgb_eval_volume_pass(ctx.handle, L.SLOT_INPUT))

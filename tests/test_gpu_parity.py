@@ -415,3 +415,20 @@ def test_export_matches_reference_output(fmt, tmp_path):
     assert ta == tr
     assert np.all(np.abs(na - nr) <= 1e-11 * np.maximum(np.abs(nr), 1e-300))
     ctx.close()
+
+
+def test_device_projection_matches_host_projection():
+    """project_initial on the device (dgb_project_slot) vs the host restatement used everywhere
+    else (bit-compatible with solver.cpp:74-97): equal to rounding; inadmissible data aborts."""
+    for ci, p in ((2, 4), (4, 5), (3, 1)):
+        name, kind, nx, ny, prm, bcf, u0 = CASES[ci]
+        mesh = dg2d.generate_mesh(kind, nx, ny, *prm)
+        tb = dg2d.build_tables(p)
+        ctx = dg2d.SolverContext(mesh, tb, bc=bcf())
+        host = dg2d.project_initial(u0, mesh, tb)
+        dg2d.project_on_device(ctx, u0, L.SLOT_INPUT)
+        dev = ctx.download(L.SLOT_INPUT)
+        assert rel_per_eq(dev, host) <= 1e-14
+        with pytest.raises(dg2d.SolverAbort, match="project_initial: inadmissible state"):
+            dg2d.project_on_device(ctx, lambda xy: -np.abs(np.asarray(u0(xy))), L.SLOT_INPUT)
+        ctx.close()
