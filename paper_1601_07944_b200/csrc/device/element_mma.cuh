@@ -32,6 +32,14 @@
 
 namespace dgbk {
 
+#ifndef DGB_MMA_VOL_PIPE
+#define DGB_MMA_VOL_PIPE 1  // interpolate the next point tile while this tile's fluxes run
+#endif
+#ifndef DGB_MMA_SIDE_UNROLL
+#define DGB_MMA_SIDE_UNROLL 1  // per-side surface loop (p = 5): runtime loop, 1.84 vs 1.91 ms unrolled
+#endif
+constexpr int kMmaSideUnroll = DGB_MMA_SIDE_UNROLL;
+
 template <int P>
 struct MmaDim {
   static constexpr int NP = Dim<P>::NP, NQ = Dim<P>::NQ, K = Dim<P>::K;
@@ -76,7 +84,12 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
       : "d"(a), "d"(b));
 }
 
-constexpr int kMmaWarps = 4;  // warps per block of the DMMA kernel
+#ifndef DGB_MMA_VOL_PIPE
+#define DGB_MMA_VOL_PIPE 1  // interpolate the next point tile while this tile's fluxes run
+#endif
+#ifndef DGB_MMA_SIDE_UNROLL
+#define DGB_MMA_SIDE_UNROLL 1  // per-side surface loop (p = 5): runtime loop, 1.84 vs 1.91 ms unrolled
+#endif
 
 // Stage prologue shared with element_body: step bookkeeping, stop rules, dt.
 // Returns false when the step must not run (a stop rule fired).
@@ -243,12 +256,16 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
         }
       };
       constexpr int NTD = D::NTD;
-      interp(U[0], 0);
+      if (DGB_MMA_VOL_PIPE) interp(U[0], 0);
 #pragma unroll
       for (int nt = 0; nt < NTD; ++nt) {
         // software pipeline: the next tile of points is interpolated while this
         // tile's fluxes are evaluated
-        if (nt + 1 < NTD) interp(U[(nt + 1) & 1], nt + 1);
+        if (DGB_MMA_VOL_PIPE) {
+          if (nt + 1 < NTD) interp(U[(nt + 1) & 1], nt + 1);
+        } else {
+          interp(U[nt & 1], nt);
+        }
         double fr[4][2], fs[4][2];
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
@@ -431,7 +448,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
         eny[q] = __ldg(geo.eny + edq[q]);
         eh[q] = __ldg(geo.eh + edq[q]);
       }
-#pragma unroll
+#pragma unroll kMmaSideUnroll
       for (int q = 0; q < 3; ++q) {
         const int nb = nbq[q];
         const int ed = edq[q];
