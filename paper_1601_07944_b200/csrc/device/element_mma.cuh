@@ -84,13 +84,6 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
       : "d"(a), "d"(b));
 }
 
-#ifndef DGB_MMA_VOL_PIPE
-#define DGB_MMA_VOL_PIPE 1  // interpolate the next point tile while this tile's fluxes run
-#endif
-#ifndef DGB_MMA_SIDE_UNROLL
-#define DGB_MMA_SIDE_UNROLL 1  // per-side surface loop (p = 5): runtime loop, 1.84 vs 1.91 ms unrolled
-#endif
-
 // Stage prologue shared with element_body: step bookkeeping, stop rules, dt.
 // Returns false when the step must not run (a stop rule fired).
 __device__ __forceinline__ bool mma_prologue(const StageArgs& a, Scalars* sc, double& t0, double& dt) {
