@@ -39,6 +39,13 @@ namespace dgbk {
 #define DGB_MMA_SIDE_UNROLL 1  // per-side surface loop (p = 5): runtime loop, 1.84 vs 1.91 ms unrolled
 #endif
 constexpr int kMmaSideUnroll = DGB_MMA_SIDE_UNROLL;
+#ifndef DGB_MMA_PACK_UNROLL
+#define DGB_MMA_PACK_UNROLL 2  // packed surface tile loop (p = 3, 4)
+#endif
+constexpr int kMmaPackUnroll = DGB_MMA_PACK_UNROLL;
+#ifndef DGB_MMA_PACK_MAXK
+#define DGB_MMA_PACK_MAXK 5  // largest edge-point count K that uses the packed surface
+#endif
 
 template <int P>
 struct MmaDim {
@@ -65,7 +72,7 @@ struct MmaDim {
   // evaluations, own-trace and projection DMMAs.  Column c of tile s is point 8s + c =
   // (side (8s+c) / K, point (8s+c) % K).
   static constexpr int NSP = (3 * K + 7) / 8;
-  static constexpr bool kPacked = NSP < 3;
+  static constexpr bool kPacked = NSP < 3 && K <= DGB_MMA_PACK_MAXK;
   static constexpr int kPkOwn = kTail + (kTail1 ? KS * 4 + 2 * JT * 8 : 0);  // [NSP][KS][32]
   static constexpr int kPkNb = kPkOwn + (kPacked ? NSP * KS * 32 : 0);      // [NSP][3 sides][3 classes][KS][32]
   static constexpr int kPkProj = kPkNb + (kPacked ? NSP * 9 * KS * 32 : 0);  // [NSP][2][JT][32]
@@ -343,7 +350,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
         eh[q] = __ldg(geo.eh + edq[q]);
       }
       auto sel3 = [](int q, auto x0, auto x1, auto x2) { return q == 0 ? x0 : (q == 1 ? x1 : x2); };
-#pragma unroll
+#pragma unroll kMmaPackUnroll
       for (int sp = 0; sp < D::NSP; ++sp) {
         if (sp > 0) cp_async_wait<0>();  // side 2's neighbour column (prefetched during tile 0)
         // own trace of the packed tile
