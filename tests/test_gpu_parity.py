@@ -432,3 +432,28 @@ def test_device_projection_matches_host_projection():
         with pytest.raises(dg2d.SolverAbort, match="project_initial: inadmissible state"):
             dg2d.project_on_device(ctx, lambda xy: -np.abs(np.asarray(u0(xy))), L.SLOT_INPUT)
         ctx.close()
+
+
+def test_double_mach_full_run_to_t02_matches_reference():
+    """The north star's per-run bar on the paper's own case: double Mach reflection 200x50
+    (dmr_desk.cfg), p=1, limiter on every stage, RK2, cfl 0.3, run to t = 0.2 (3,114 steps
+    measured in SURVEY Appendix B) — identical step count, relative difference <= 1e-9."""
+    if not bind.ref_available():
+        pytest.skip("oracle/_ref not built")
+    rm = bind.RefMesh.generate(L.MESH_DOUBLE_MACH, 200, 50, 1.0 / 6.0)
+    rt = bind.RefTables(1)
+    rbc = bind.RefBC()
+    bind.ref_lib().ref_bc_set_double_mach(rbc.h, 1.0 / 6.0, 10.0, 60.0, 1.4)
+    rs = bind.RefSolver(rm, rt, rbc, rk_order=2, cfl=0.3, limiting=True)
+    c = rs.limit(bind.ref_project(rm, rt, 3, (1.0 / 6.0, 10.0, 60.0)))
+    cr, tr, sr, _ = rs.run_to_time(c, 0.0, 0.2, 100_000)
+    mesh, tb = dg2d.ArrayMesh(rm.export(), rm.nb), rt.as_external()
+    ctx = dg2d.SolverContext(mesh, tb, bc=dg2d.double_mach_boundary(dg2d.DoubleMachSetup()),
+                             options=dg2d.SolverOptions(rk_order=2, cfl=0.3, limiting=True))
+    st = dg2d.SolverState(c.copy())
+    dg2d.run_to_time(ctx, st, 0.2, 100_000)
+    assert st.step_count == sr and abs(st.t - tr) <= 1e-14
+    assert rel_per_eq(st.coeffs, cr) <= RUN_TOL, rel_per_eq(st.coeffs, cr)
+    m_ref, m_gpu = rs.total_mass(cr), dg2d.total_mass(mesh, st.coeffs)
+    assert abs(m_gpu - m_ref) <= 1e-12 * abs(m_ref)
+    ctx.close()
