@@ -50,12 +50,6 @@ struct LimTab {
   int n_pts, edge_begin, n_edge;
 };
 
-// Lanes per element for each degree (register budget / FP64 redundancy trade-off).
-template <int P>
-struct LanesPerElem {
-  static constexpr int G = P == 1 ? 1 : P == 2 ? 2 : 4;
-};
-
 // Boundary codes (euler.hpp:80-86).
 enum : int { kReflecting = -1, kCurved = -2, kInflow = -3, kOutflow = -4, kShock = -5 };
 

@@ -85,19 +85,6 @@ __device__ __forceinline__ Prim primitives(const double (&U)[4], double g1) {
 
 __device__ __forceinline__ bool admissible(const double (&U)[4], const Prim& w) { return U[0] > 0.0 && w.p > 0.0; }
 
-// Analytic flux (euler.hpp:43-50).
-__device__ __forceinline__ void euler_flux(const double (&U)[4], const Prim& w, double (&f1)[4], double (&f2)[4]) {
-  const double ep = U[3] + w.p;
-  f1[0] = U[1];
-  f1[1] = fma(U[1], w.vx, w.p);
-  f1[2] = U[2] * w.vx;
-  f1[3] = w.vx * ep;
-  f2[0] = U[2];
-  f2[1] = U[1] * w.vy;
-  f2[2] = fma(U[2], w.vy, w.p);
-  f2[3] = w.vy * ep;
-}
-
 // Contravariant fluxes fr = ta F1 + tb F2, fs = tc F1 + td F2 of the analytic flux
 // (euler.hpp:43-50) through the contravariant velocities: 16 FP64 operations instead of
 // forming F1, F2 and rotating them (26).
