@@ -305,3 +305,27 @@ def test_partition_run_to_steady_matches_whole_mesh():
     for q in parts:
         out[:, :, q.owned] = q.download(L.SLOT_STATE)
     assert np.array_equal(out, ref.coeffs)
+
+
+def test_plan_rejects_bad_arguments():
+    mesh = MESHES["periodic"]()
+    for rank, world in ((0, 0), (0, 9), (2, 2), (-1, 2)):
+        with pytest.raises(ValueError):
+            D.plan(mesh, rank, world)
+    tiny = dg2d.generate_mesh(L.MESH_BOX, 1, 1, 1.0, 1.0, 4)  # 2 triangles
+    with pytest.raises(ValueError):
+        D.plan(tiny, 0, 3)
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_strip_partition_of_the_bench_box_has_two_neighbours(world):
+    """The bench's weak-scaling box (n x n*world cells, periodic): every rank owns exactly
+    2 n^2 triangles and exchanges halos with its two strip neighbours only."""
+    n = 12
+    mesh = dg2d.generate_mesh(L.MESH_PERIODIC_BOX, n, n * world, 10.0, 10.0 * world)
+    for r in range(world):
+        p = D.plan(mesh, r, world)
+        assert p["n_owned"] == 2 * n * n
+        nbrs = {k for k in range(world) if (p["neighbor_mask"] >> k) & 1}
+        assert nbrs == {(r - 1) % world, (r + 1) % world}
+        assert p["n_halo"] <= 4 * n  # one row of cells above and below
