@@ -457,3 +457,21 @@ def test_double_mach_full_run_to_t02_matches_reference():
     m_ref, m_gpu = rs.total_mass(cr), dg2d.total_mass(mesh, st.coeffs)
     assert abs(m_gpu - m_ref) <= 1e-12 * abs(m_ref)
     ctx.close()
+
+
+def test_roe_with_limiter_and_moving_shock_matches_oracle():
+    """Roe flux through every boundary code of the double Mach problem (reflecting wall,
+    inflow, outflow, moving shock) with the limiter on every stage, 40 RK2 steps."""
+    mesh = dg2d.generate_mesh(L.MESH_DOUBLE_MACH, 40, 10, 1.0 / 6.0)
+    tb = dg2d.build_tables(1)
+    setup = dg2d.DoubleMachSetup()
+    bc = dg2d.double_mach_boundary(setup)
+    opts = dg2d.SolverOptions(rk_order=2, cfl=0.3, limiting=True, flux="roe")
+    ctx = dg2d.SolverContext(mesh, tb, bc=bc, options=opts)
+    c0 = dg2d.limit(ctx, dg2d.project_initial(lambda xy: dg2d.double_mach_initial(xy, setup), mesh, tb))
+    st = dg2d.SolverState(c0.copy())
+    dg2d.run_fixed_steps(ctx, st, 40)
+    cr, tr, _, _ = bind.Oracle(mesh, tb, bc, flux="roe").run_fixed_steps(c0, 0.0, 40, 2, 0.3, limiting=True)
+    assert rel_per_eq(st.coeffs, cr) <= RUN_TOL
+    assert abs(st.t - tr) <= 1e-12 * tr
+    ctx.close()
