@@ -16,9 +16,12 @@ __device__ __forceinline__ double ref_pressure(double rho, double mx, double my,
 namespace {
 // One thread per element, in place on modes 1..2 (mode 0 is never written, so
 // reading the neighbours' means while limiting is race-free, solver.cpp:419-422).
+// NE / NPT: edge points and all check points as compile-time constants (0: read from c_lim),
+// so the point loops unroll onto immediate constant-bank operands.
 #ifndef DGB_LIMIT_MINB
 #define DGB_LIMIT_MINB 8  // 64 registers: 0.149 ms per stage on the 2M DMR vs 0.206 at 116 (measured)
 #endif
+template <int NE, int NPT>
 __global__ void __launch_bounds__(kBlock, DGB_LIMIT_MINB) k_limit(Geo geo, LimArgs a) {
   constexpr int NP = 3;
   const long long ld = geo.ld;
@@ -32,6 +35,9 @@ __global__ void __launch_bounds__(kBlock, DGB_LIMIT_MINB) k_limit(Geo geo, LimAr
 
   const LimTab& L = c_lim;
   const Tab<1>& T = c_tab;
+  const int n_edge = NE ? NE : L.n_edge;
+  const int e_begin = NE ? NPT - NE - 3 : L.edge_begin;
+  const int n_pts = NPT ? NPT : L.n_pts;
   double lam_min = __longlong_as_double(0x7ff0000000000000ll);
   double res_max = 0.0;
 
@@ -70,18 +76,19 @@ __global__ void __launch_bounds__(kBlock, DGB_LIMIT_MINB) k_limit(Geo geo, LimAr
       // min over the edge points of clamp((umax-uc)/d) for d > tol and clamp((umin-uc)/d) for
       // d < -tol (solver.cpp:348-358).  The numerators have fixed signs and correctly rounded
       // division is monotone in the divisor, so the minimum is the quotient by the extreme d:
-      // two divisions per variable instead of one per point, bit-identical.
+      // two divisions per variable instead of one per point.  tol >= 0, so the extreme d
+      // beyond +-tol is the extreme of all d when that clears the threshold (and NaN d are
+      // skipped by fmax/fmin as by the comparisons): bit-identical.
       double dpos = 0.0, dneg = 0.0;
-      for (int k = L.edge_begin; k < L.edge_begin + L.n_edge; ++k) {
+#pragma unroll
+      for (int k = e_begin; k < e_begin + n_edge; ++k) {
         const double d = c1[m] * L.phi1[k] + c2[m] * L.phi2[k];
-        if (d > tol)
-          dpos = fmax(dpos, d);
-        else if (d < -tol)
-          dneg = fmin(dneg, d);
+        dpos = fmax(dpos, d);
+        dneg = fmin(dneg, d);
       }
       double alpha = 1.0;
-      if (dpos > 0.0) alpha = fmin(alpha, fmin(fmax((umax - uc) / dpos, 0.0), 1.0));
-      if (dneg < 0.0) alpha = fmin(alpha, fmin(fmax((umin - uc) / dneg, 0.0), 1.0));
+      if (dpos > tol) alpha = fmin(alpha, fmin(fmax((umax - uc) / dpos, 0.0), 1.0));
+      if (dneg < -tol) alpha = fmin(alpha, fmin(fmax((umin - uc) / dneg, 0.0), 1.0));
       c1[m] *= alpha;
       c2[m] *= alpha;
     }
@@ -105,7 +112,7 @@ __global__ void __launch_bounds__(kBlock, DGB_LIMIT_MINB) k_limit(Geo geo, LimAr
       }
       if (!safe) {
         double rho_min = mr;
-        for (int k = 0; k < L.n_pts; ++k)
+        for (int k = 0; k < n_pts; ++k)
           rho_min = fmin(rho_min, c0[0] * sqrt2 + c1[0] * L.phi1[k] + c2[0] * L.phi2[k]);
         if (rho_min < eps_rho) {
           const double th = fmin(fmax((mr - eps_rho) / (mr - rho_min), 0.0), 1.0);
@@ -113,7 +120,7 @@ __global__ void __launch_bounds__(kBlock, DGB_LIMIT_MINB) k_limit(Geo geo, LimAr
           c2[0] *= th;
         }
         double th_p = 1.0;
-        for (int k = 0; k < L.n_pts; ++k) {
+        for (int k = 0; k < n_pts; ++k) {
           double u[4];
 #pragma unroll
           for (int m = 0; m < 4; ++m) u[m] = c0[m] * sqrt2 + c1[m] * L.phi1[k] + c2[m] * L.phi2[k];
@@ -173,24 +180,33 @@ __global__ void __launch_bounds__(kBlock, DGB_LIMIT_MINB) k_limit(Geo geo, LimAr
   const int par = a.step & 1;
   if (a.want_lambda) block_reduce_atomic<true>(lam_min, &sc->dtmin[par ^ 1]);
   if (a.want_resid) block_reduce_atomic<false>(res_max, &sc->resid[par]);
-  if (a.push) __threadfence_system();  // halo stores visible before the signal kernel's flag
+  if (a.push) __threadfence_system();
 }
+
+int g_lim_pts[2] = {0, 0};  // host copy of (n_edge, n_pts) of the uploaded table
 }  // namespace
 
 cudaError_t upload_limtab(const LimTab& t, cudaStream_t s) {
+  g_lim_pts[0] = t.n_edge;
+  g_lim_pts[1] = t.edge_begin + t.n_edge + 3 == t.n_pts ? t.n_pts : -1;
   return cudaMemcpyToSymbolAsync(c_lim, &t, sizeof(t), 0, cudaMemcpyHostToDevice, s);
 }
 
+constexpr int kLimNE = 6, kLimNPT = 12;  // p = 1 tables: 2 points per edge, 3 interior
+
 int limit_resident_blocks() {
   static int occ = 0;
-  if (!occ) occ = occupancy(k_limit);
+  if (!occ) occ = occupancy(k_limit<kLimNE, kLimNPT>);
   return occ;
 }
 
 cudaError_t launch_limit(int grid, const Geo& g, const LimArgs& a, cudaStream_t s) {
   if (a.e1 <= a.e0) return cudaSuccess;
   if (grid <= 0) grid = grid_for(a.e1 - a.e0, limit_resident_blocks());
-  k_limit<<<grid, kBlock, 0, s>>>(g, a);
+  if (g_lim_pts[0] == kLimNE && g_lim_pts[1] == kLimNPT)
+    k_limit<kLimNE, kLimNPT><<<grid, kBlock, 0, s>>>(g, a);
+  else
+    k_limit<0, 0><<<grid, kBlock, 0, s>>>(g, a);
   return cudaGetLastError();
 }
 
