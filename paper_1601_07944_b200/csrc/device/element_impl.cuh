@@ -352,6 +352,43 @@ struct MinBlocks {
   static constexpr int value = DGB_MINB(P);
 };
 
+// Stage prologue shared by the element kernels: step bookkeeping, stop rules, dt.
+// Returns false when the step must not run (a stop rule fired).
+__device__ __forceinline__ bool stage_prologue(const StageArgs& a, Scalars* sc, double& t0, double& dt) {
+  const int par = a.step & 1;
+  t0 = sc->t[par];
+  if (a.first) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      if (a.hist && a.step > 0) a.hist[a.step - 1] = bits_to_double(sc->resid[par ^ 1]);
+    }
+    bool stop = false;
+    if (a.stop_at_t_end && !(t0 < a.t_end)) stop = true;
+    if (a.stop_steady && a.step > 0 && bits_to_double(sc->resid[par ^ 1]) <= a.tol) stop = true;
+    if (stop) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        sc->halt = 1;
+        sc->halt_step = a.step;
+      }
+      return false;
+    }
+  }
+  if (a.dt_mode == 0) {
+    dt = a.dt_host;
+  } else {
+    dt = a.cfl * bits_to_double(sc->dtmin[par]);
+    if (a.clip_t_end && t0 + dt > a.t_end) dt = a.t_end - t0;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (a.first) {
+      sc->dtmin[par ^ 1] = 0x7ff0000000000000ull;  // +inf
+      sc->resid[par] = 0ull;
+      sc->dt_used[par] = dt;
+    }
+    if (a.last) sc->t[par ^ 1] = t0 + dt;
+  }
+  return true;
+}
+
 // The fused element kernel.  Four lanes per element, lane g owns conserved
 // variable g (its n_p coefficients and accumulators).  Contractions are DFMA
 // chains with constant-bank table operands (all lanes of a warp use the same
@@ -381,37 +418,7 @@ __device__ __forceinline__ void element_body(const Tab<P>& T, const Geo& geo, co
   // ---- time and dt of this stage (every thread evaluates the same values)
   double t0 = a.t_host, dt = 0.0;
   if constexpr (MODE == kModeStage) {
-    const int par = a.step & 1;
-    t0 = sc->t[par];
-    if (a.first) {
-      if (blockIdx.x == 0 && threadIdx.x == 0) {
-        if (a.hist && a.step > 0) a.hist[a.step - 1] = bits_to_double(sc->resid[par ^ 1]);
-      }
-      bool stop = false;
-      if (a.stop_at_t_end && !(t0 < a.t_end)) stop = true;
-      if (a.stop_steady && a.step > 0 && bits_to_double(sc->resid[par ^ 1]) <= a.tol) stop = true;
-      if (stop) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
-          sc->halt = 1;
-          sc->halt_step = a.step;
-        }
-        return;
-      }
-    }
-    if (a.dt_mode == 0) {
-      dt = a.dt_host;
-    } else {
-      dt = a.cfl * bits_to_double(sc->dtmin[par]);
-      if (a.clip_t_end && t0 + dt > a.t_end) dt = a.t_end - t0;
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      if (a.first) {
-        sc->dtmin[par ^ 1] = 0x7ff0000000000000ull;  // +inf
-        sc->resid[par] = 0ull;
-        sc->dt_used[par] = dt;
-      }
-      if (a.last) sc->t[par ^ 1] = t0 + dt;
-    }
+    if (!stage_prologue(a, sc, t0, dt)) return;
   }
   const double tstage = (MODE == kModeStage) ? fma(a.tcoef, dt, t0) : t0;
 
@@ -652,37 +659,7 @@ __device__ __forceinline__ void element_body_g1(const Tab<P>& T, const Geo& geo,
 
   double t0 = a.t_host, dt = 0.0;
   if constexpr (MODE == kModeStage) {
-    const int par = a.step & 1;
-    t0 = sc->t[par];
-    if (a.first) {
-      if (blockIdx.x == 0 && threadIdx.x == 0) {
-        if (a.hist && a.step > 0) a.hist[a.step - 1] = bits_to_double(sc->resid[par ^ 1]);
-      }
-      bool stop = false;
-      if (a.stop_at_t_end && !(t0 < a.t_end)) stop = true;
-      if (a.stop_steady && a.step > 0 && bits_to_double(sc->resid[par ^ 1]) <= a.tol) stop = true;
-      if (stop) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
-          sc->halt = 1;
-          sc->halt_step = a.step;
-        }
-        return;
-      }
-    }
-    if (a.dt_mode == 0) {
-      dt = a.dt_host;
-    } else {
-      dt = a.cfl * bits_to_double(sc->dtmin[par]);
-      if (a.clip_t_end && t0 + dt > a.t_end) dt = a.t_end - t0;
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      if (a.first) {
-        sc->dtmin[par ^ 1] = 0x7ff0000000000000ull;
-        sc->resid[par] = 0ull;
-        sc->dt_used[par] = dt;
-      }
-      if (a.last) sc->t[par ^ 1] = t0 + dt;
-    }
+    if (!stage_prologue(a, sc, t0, dt)) return;
   }
   const double tstage = (MODE == kModeStage) ? fma(a.tcoef, dt, t0) : t0;
 

@@ -91,43 +91,6 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
       : "d"(a), "d"(b));
 }
 
-// Stage prologue shared with element_body: step bookkeeping, stop rules, dt.
-// Returns false when the step must not run (a stop rule fired).
-__device__ __forceinline__ bool mma_prologue(const StageArgs& a, Scalars* sc, double& t0, double& dt) {
-  const int par = a.step & 1;
-  t0 = sc->t[par];
-  if (a.first) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      if (a.hist && a.step > 0) a.hist[a.step - 1] = bits_to_double(sc->resid[par ^ 1]);
-    }
-    bool stop = false;
-    if (a.stop_at_t_end && !(t0 < a.t_end)) stop = true;
-    if (a.stop_steady && a.step > 0 && bits_to_double(sc->resid[par ^ 1]) <= a.tol) stop = true;
-    if (stop) {
-      if (blockIdx.x == 0 && threadIdx.x == 0) {
-        sc->halt = 1;
-        sc->halt_step = a.step;
-      }
-      return false;
-    }
-  }
-  if (a.dt_mode == 0) {
-    dt = a.dt_host;
-  } else {
-    dt = a.cfl * bits_to_double(sc->dtmin[par]);
-    if (a.clip_t_end && t0 + dt > a.t_end) dt = a.t_end - t0;
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    if (a.first) {
-      sc->dtmin[par ^ 1] = 0x7ff0000000000000ull;  // +inf
-      sc->resid[par] = 0ull;
-      sc->dt_used[par] = dt;
-    }
-    if (a.last) sc->t[par ^ 1] = t0 + dt;
-  }
-  return true;
-}
-
 // cp.async of one double into shared memory (zero-filled when !pred); lane-private
 // destinations, so the issuing lane's wait_group is the only synchronisation needed.
 __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool pred) {
@@ -172,7 +135,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
 
   double t0 = a.t_host, dt = 0.0;
   if constexpr (MODE == kModeStage) {
-    if (!mma_prologue(a, sc, t0, dt)) return;
+    if (!stage_prologue(a, sc, t0, dt)) return;
   }
   const double tstage = (MODE == kModeStage) ? fma(a.tcoef, dt, t0) : t0;
 
