@@ -332,6 +332,19 @@ constexpr int kG1SideUnroll = DGB_G1_SIDE_UNROLL;
 #ifndef DGB_G1_MAXP
 #define DGB_G1_MAXP 2
 #endif
+#ifndef DGB_G1_RELOAD_MINP
+// one-thread kernel, degrees >= this: re-read the coefficients after the volume integral
+// instead of keeping them in registers (measured per stage: p=2 0.428 vs 0.446 ms, fewer
+// spills; p=1 0.189 vs 0.182 ms, so p=1 keeps them)
+#define DGB_G1_RELOAD_MINP 2
+#endif
+// Read-only global load the compiler may not merge with an earlier load of the same
+// address (so a value can be re-read instead of being kept live in registers).
+__device__ __forceinline__ double ld_nc(const double* p) {
+  double r;
+  asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(r) : "l"(p));
+  return r;
+}
 // Degrees up to DGB_G1_MAXP use one thread per element, higher ones four lanes.
 template <int P>
 struct Lanes {
@@ -738,15 +751,33 @@ __device__ __forceinline__ void element_body_g1(const Tab<P>& T, const Geo& geo,
             for (int j = 0; j < NP; ++j) acc[m][j] = 0.0;
         }
         const double* __restrict__ phq = &T.phe[q][0][0];  // own side, uniform runtime offset
+        constexpr bool kReload = P >= DGB_G1_RELOAD_MINP;
+        // own trace of the side from a fresh (L1) read of the coefficients, so that they
+        // need not stay in registers past the volume integral
+        double uoa[K][4];
+        if constexpr (kReload) {
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+#pragma unroll
+          for (int j = 0; j < NP; ++j) {
+            const double cj = ld_nc(a.in + (static_cast<long long>(m) * NP + j) * ld + e);
+#pragma unroll
+            for (int ko = 0; ko < K; ++ko) uoa[ko][m] = j == 0 ? phq[ko * NP] * cj : fma(phq[ko * NP + j], cj, uoa[ko][m]);
+          }
+        }
 #pragma unroll
         for (int ko = 0; ko < K; ++ko) {
           double uo[4];
 #pragma unroll
           for (int m = 0; m < 4; ++m) {
-            double s = phq[ko * NP] * c[m][0];
+            if constexpr (kReload) {
+              uo[m] = uoa[ko][m];
+            } else {
+              double s = phq[ko * NP] * c[m][0];
 #pragma unroll
-            for (int j = 1; j < NP; ++j) s = fma(phq[ko * NP + j], c[m][j], s);
-            uo[m] = s;
+              for (int j = 1; j < NP; ++j) s = fma(phq[ko * NP + j], c[m][j], s);
+              uo[m] = s;
+            }
           }
           double UL[4], UR[4];
 #pragma unroll
@@ -811,7 +842,8 @@ __device__ __forceinline__ void element_body_g1(const Tab<P>& T, const Geo& geo,
           if (a.kmode == 3) {
             o = fma(dt6, __ldg(a.kacc + idx) + d, uu);
           } else {
-            const double base = (a.alpha != 0.0) ? fma(a.alpha, uu, a.beta * c[m][j]) : a.beta * c[m][j];
+            const double cmj = (P >= DGB_G1_RELOAD_MINP) ? ld_nc(a.in + idx) : c[m][j];
+            const double base = (a.alpha != 0.0) ? fma(a.alpha, uu, a.beta * cmj) : a.beta * cmj;
             o = fma(gdt, d, base);
             if (a.kmode == 1) a.kacc[idx] = d;
             if (a.kmode == 2) a.kacc[idx] = fma(2.0, d, a.kacc[idx]);
