@@ -43,6 +43,11 @@ constexpr int kMmaSideUnroll = DGB_MMA_SIDE_UNROLL;
 #define DGB_MMA_PACK_UNROLL 2  // packed surface tile loop (p = 3, 4)
 #endif
 constexpr int kMmaPackUnroll = DGB_MMA_PACK_UNROLL;
+#ifndef DGB_MMA_C_SMEM_MINP
+// degrees >= this read the stage input for the RK epilogue from the own fragment buffer
+// (measured per stage: p=5 1.739 vs 1.846 ms, p=4 1.089 vs 1.108, p=3 0.870 vs 0.866)
+#define DGB_MMA_C_SMEM_MINP 4
+#endif
 #ifndef DGB_MMA_PACK_MAXK
 #define DGB_MMA_PACK_MAXK 5  // largest edge-point count K that uses the packed surface
 #endif
@@ -150,6 +155,9 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
   double* __restrict__ w_nbr = w_own + FR;
   // packed surface (p = 3, 4): a second neighbour buffer, side q lives in buffer q & 1
   constexpr bool kPk = D::kPacked && (MODE == kModeRhs || MODE == kModeStage);
+  // stage mode: the epilogue reads the stage input from the own fragment buffer (shared
+  // memory) instead of global memory; the next tile's own prefetch waits until then
+  constexpr bool kCSmem = P >= DGB_MMA_C_SMEM_MINP && MODE == kModeStage;
   double* __restrict__ w_nbr2 = w_own + 2 * FR;
 
   double lam_min = __longlong_as_double(0x7ff0000000000000ll);
@@ -356,7 +364,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
         } else {
           fetch_frag<NP, KS>(w_nbr, a.in, ld, nbn[0], nvalid && nbn[0] >= 0, lane, t);
           fetch_frag<NP, KS>(w_nbr2, a.in, ld, nbn[1], nvalid && nbn[1] >= 0, lane, t);
-          fetch_frag<NP, KS>(w_own, a.in, ld, e_next, nvalid, lane, t);
+          if (!kCSmem) fetch_frag<NP, KS>(w_own, a.in, ld, e_next, nvalid, lane, t);
         }
         cp_async_commit();
         // numerical flux at this lane's two packed points, canonical orientation
@@ -463,7 +471,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
           fetch_frag<NP, KS>(w_nbr, a.in, ld, nbq[q + 1], valid && nbq[q + 1] >= 0, lane, t);
         } else {
           fetch_frag<NP, KS>(w_nbr, a.in, ld, nbn[0], nvalid && nbn[0] >= 0, lane, t);
-          fetch_frag<NP, KS>(w_own, a.in, ld, e_next, nvalid, lane, t);
+          if (!kCSmem) fetch_frag<NP, KS>(w_own, a.in, ld, e_next, nvalid, lane, t);
         }
         cp_async_commit();
         // numerical flux at points ko = 2t + i, canonical orientation
@@ -555,7 +563,11 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
             const int j = 8 * jt + 2 * t + ii;
             const long long idx = (static_cast<long long>(m) * NP + j) * ld + e;
             uv[jt][ii] = (need_u && j < NP) ? __ldg(a.u + idx) : 0.0;
-            cv[jt][ii] = (need_c && j < NP) ? __ldg(a.in + idx) : 0.0;
+            if constexpr (kCSmem) {  // element g's mode j from the tile's own fragment buffer
+              cv[jt][ii] = (need_c && j < NP) ? w_own[(m * KS + (j >> 2)) * 32 + (g << 2) + (j & 3)] : 0.0;
+            } else {
+              cv[jt][ii] = (need_c && j < NP) ? __ldg(a.in + idx) : 0.0;
+            }
             kv[jt][ii] = ((a.kmode == 2 || a.kmode == 3) && j < NP) ? a.kacc[idx] : 0.0;
           }
 #pragma unroll
@@ -639,6 +651,11 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
         lam = fmax(lam, __shfl_xor_sync(0xffffffffu, lam, 2));
         if (valid && t == 0) lam_min = fmin(lam_min, 2.0 * __ldg(geo.inradius + e) / ((2.0 * P + 1.0) * lam));
       }
+    }
+    if constexpr (kCSmem) {  // the own buffer is free only now
+      __syncwarp();
+      fetch_frag<NP, KS>(w_own, a.in, ld, e_next, nvalid, lane, t);
+      cp_async_commit();
     }
 #pragma unroll
     for (int q = 0; q < 3; ++q) nbq[q] = nbn[q];
