@@ -48,6 +48,9 @@ constexpr int kMmaPackUnroll = DGB_MMA_PACK_UNROLL;
 // (measured per stage: p=5 1.739 vs 1.846 ms, p=4 1.089 vs 1.108, p=3 0.870 vs 0.866)
 #define DGB_MMA_C_SMEM_MINP 4
 #endif
+#ifndef DGB_MMA_U_AHEAD
+#define DGB_MMA_U_AHEAD 1
+#endif
 #ifndef DGB_MMA_PACK_MAXK
 #define DGB_MMA_PACK_MAXK 5  // largest edge-point count K that uses the packed surface
 #endif
@@ -158,6 +161,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
   // stage mode: the epilogue reads the stage input from the own fragment buffer (shared
   // memory) instead of global memory; the next tile's own prefetch waits until then
   constexpr bool kCSmem = P >= DGB_MMA_C_SMEM_MINP && MODE == kModeStage;
+  constexpr bool kUAhead = DGB_MMA_U_AHEAD != 0;
   double* __restrict__ w_nbr2 = w_own + 2 * FR;
 
   double lam_min = __longlong_as_double(0x7ff0000000000000ll);
@@ -551,18 +555,36 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
       const double dt6 = dt / 6.0;
       const bool need_u = a.alpha != 0.0 || a.want_resid || a.kmode == 3;
       const bool need_c = a.kmode != 3 && a.beta != 0.0;
+      // u^n is loaded one variable ahead of the stores (the stores may alias for all the
+      // compiler knows, so it cannot hoist the loads itself)
+      auto load_u = [&](double(&dst)[JT][2], int m) {
+#pragma unroll
+        for (int jt = 0; jt < JT; ++jt)
+#pragma unroll
+          for (int ii = 0; ii < 2; ++ii) {
+            const int j = 8 * jt + 2 * t + ii;
+            dst[jt][ii] = (need_u && j < NP) ? __ldg(a.u + (static_cast<long long>(m) * NP + j) * ld + e) : 0.0;
+          }
+      };
+      double uv_next[JT][2];
+      if (kUAhead) load_u(uv_next, 0);
 #pragma unroll
       for (int m = 0; m < 4; ++m) {
         // this variable's u^n, stage input and RK4 accumulator: every load issued
         // before any store, so one memory latency per variable
         double uv[JT][2], cv[JT][2], kv[JT][2];
+        if (kUAhead) {
+#pragma unroll
+          for (int jt = 0; jt < JT; ++jt) uv[jt][0] = uv_next[jt][0], uv[jt][1] = uv_next[jt][1];
+          if (m + 1 < 4) load_u(uv_next, m + 1);
+        }
 #pragma unroll
         for (int jt = 0; jt < JT; ++jt)
 #pragma unroll
           for (int ii = 0; ii < 2; ++ii) {
             const int j = 8 * jt + 2 * t + ii;
             const long long idx = (static_cast<long long>(m) * NP + j) * ld + e;
-            uv[jt][ii] = (need_u && j < NP) ? __ldg(a.u + idx) : 0.0;
+            if (!kUAhead) uv[jt][ii] = (need_u && j < NP) ? __ldg(a.u + idx) : 0.0;
             if constexpr (kCSmem) {  // element g's mode j from the tile's own fragment buffer
               cv[jt][ii] = (need_c && j < NP) ? w_own[(m * KS + (j >> 2)) * 32 + (g << 2) + (j & 3)] : 0.0;
             } else {

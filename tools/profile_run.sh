@@ -14,4 +14,8 @@ for p in ${PROFILE_ORDERS:-1 5}; do
   ORDERS=$p timeout -s KILL 400 ncu --set full --clock-control none --import-source on -k regex:k_element -s 12 -c 1 \
     -o gpurun_out/prof_${TAG}_p$p python tools/stage_timing.py > gpurun_out/ncu_${TAG}_p$p.log 2>&1
 done
+# the p=1 limiter on the double-Mach mesh (bench DMR leg)
+timeout -s KILL 400 ncu --set full --clock-control none --import-source on -k regex:k_limit -s 6 -c 1 \
+  -o gpurun_out/prof_${TAG}_limit python bench.py --orders 1 --no-cpu --e2e-steps 0 --steps 2 --warmup 3 --box 64 \
+  > gpurun_out/ncu_${TAG}_limit.log 2>&1
 ls -la gpurun_out
