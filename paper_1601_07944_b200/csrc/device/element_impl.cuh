@@ -332,6 +332,9 @@ constexpr int kG1SideUnroll = DGB_G1_SIDE_UNROLL;
 #ifndef DGB_G1_MAXP
 #define DGB_G1_MAXP 2
 #endif
+#ifndef DGB_G1_SIDE_PREFETCH
+#define DGB_G1_SIDE_PREFETCH 1
+#endif
 #ifndef DGB_G1_RELOAD_MINP
 // one-thread kernel, degrees >= this: re-read the coefficients after the volume integral
 // instead of keeping them in registers (measured per stage: p=2 0.428 vs 0.446 ms, fewer
@@ -690,6 +693,19 @@ __device__ __forceinline__ void element_body_g1(const Tab<P>& T, const Geo& geo,
     for (int m = 0; m < 4; ++m)
 #pragma unroll
       for (int j = 0; j < NP; ++j) acc[m][j] = 0.0;
+#if DGB_G1_SIDE_PREFETCH
+    // connectivity of the three sides, requested with the coefficients so that the side
+    // loop's neighbour-column and normal loads do not wait for a dependent index load
+    int nb3[3] = {0, 0, 0}, ed3[3] = {0, 0, 0}, inf0 = 0;
+    if constexpr (MODE != kModeVolume) {
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        nb3[q] = __ldg(geo.nbr + q * ld + e);
+        ed3[q] = __ldg(geo.eid + q * ld + e);
+      }
+      inf0 = __ldg(geo.info + e);
+    }
+#endif
 
     // ------------------------------------------------------------ volume
     if constexpr (MODE != kModeSurface) {
@@ -722,11 +738,20 @@ __device__ __forceinline__ void element_body_g1(const Tab<P>& T, const Geo& geo,
 
     // ------------------------------------------------------------ surface
     if constexpr (MODE != kModeVolume) {
+#if DGB_G1_SIDE_PREFETCH
+      const int inf = inf0;
+#else
       const int inf = __ldg(geo.info + e);
+#endif
 #pragma unroll kG1SideUnroll
       for (int q = 0; q < 3; ++q) {
+#if DGB_G1_SIDE_PREFETCH
+        const int nb = q == 0 ? nb3[0] : (q == 1 ? nb3[1] : nb3[2]);
+        const int ed = q == 0 ? ed3[0] : (q == 1 ? ed3[1] : ed3[2]);
+#else
         const int nb = __ldg(geo.nbr + q * ld + e);
         const int ed = __ldg(geo.eid + q * ld + e);
+#endif
         const int snb = (inf >> (2 * q)) & 3;
         const bool left = (inf >> (6 + q)) & 1;
         const double nx = __ldg(geo.enx + ed), ny = __ldg(geo.eny + ed), h = __ldg(geo.eh + ed);
