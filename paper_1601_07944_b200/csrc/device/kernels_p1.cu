@@ -21,6 +21,9 @@ namespace {
 #ifndef DGB_LIMIT_MINB
 #define DGB_LIMIT_MINB 8  // 64 registers: 0.149 ms per stage on the 2M DMR vs 0.206 at 116 (measured)
 #endif
+#ifndef DGB_LIMIT_CFL_PREFETCH
+#define DGB_LIMIT_CFL_PREFETCH 1
+#endif
 template <int NE, int NPT>
 __global__ void __launch_bounds__(kBlock, DGB_LIMIT_MINB) k_limit(Geo geo, LimArgs a) {
   constexpr int NP = 3;
@@ -52,6 +55,16 @@ __global__ void __launch_bounds__(kBlock, DGB_LIMIT_MINB) k_limit(Geo geo, LimAr
     int nb[3];
 #pragma unroll
     for (int q = 0; q < 3; ++q) nb[q] = __ldg(geo.nbr + q * ld + e);
+#if DGB_LIMIT_CFL_PREFETCH
+    // the CFL epilogue's edge normals and inradius, requested with the neighbour means
+    int ed3[3] = {0, 0, 0};
+    double enx3[3] = {0.0, 0.0, 0.0}, eny3[3] = {0.0, 0.0, 0.0}, rin = 0.0;
+    if (a.want_lambda) {
+#pragma unroll
+      for (int q = 0; q < 3; ++q) ed3[q] = __ldg(geo.eid + q * ld + e);
+      rin = __ldg(geo.inradius + e);
+    }
+#endif
     // the neighbours' means, all requested at once (mode 0 is never written here,
     // so the read-only path is safe)
     double nm[3][4];
@@ -59,6 +72,15 @@ __global__ void __launch_bounds__(kBlock, DGB_LIMIT_MINB) k_limit(Geo geo, LimAr
     for (int q = 0; q < 3; ++q)
 #pragma unroll
       for (int m = 0; m < 4; ++m) nm[q][m] = nb[q] >= 0 ? __ldg(a.c + (m * NP) * ld + nb[q]) : 0.0;
+#if DGB_LIMIT_CFL_PREFETCH
+    if (a.want_lambda) {
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        enx3[q] = __ldg(geo.enx + ed3[q]);
+        eny3[q] = __ldg(geo.eny + ed3[q]);
+      }
+    }
+#endif
 
     // Barth-Jespersen per conserved variable against the neighbours' centroid range
 #pragma unroll
@@ -170,11 +192,17 @@ __global__ void __launch_bounds__(kBlock, DGB_LIMIT_MINB) k_limit(Geo geo, LimAr
           record_error(sc, err_key(a.seq, kPassDt, __ldg(geo.ref_id + e), q + 1));
           continue;
         }
+#if DGB_LIMIT_CFL_PREFETCH
+        lam = fmax(lam, fabs(w.vx * enx3[q] + w.vy * eny3[q]) + sqrt_nr(geo.gamma * w.p * w.inv));
+      }
+      lam_min = fmin(lam_min, 2.0 * rin / (3.0 * lam));
+#else
         const int ed = __ldg(geo.eid + q * ld + e);
         lam = fmax(lam, fabs(w.vx * __ldg(geo.enx + ed) + w.vy * __ldg(geo.eny + ed)) +
                             sqrt_nr(geo.gamma * w.p * w.inv));
       }
       lam_min = fmin(lam_min, 2.0 * __ldg(geo.inradius + e) / (3.0 * lam));
+#endif
     }
   }
   const int par = a.step & 1;
