@@ -164,10 +164,13 @@ __device__ __forceinline__ void roe_flux(const double (&UL)[4], const Prim& wl, 
 
 enum : int { kFluxLLF = 0, kFluxRoe = 1 };
 
-// The numerical flux selected for the run (warp-uniform branch).
-__device__ __forceinline__ void num_flux(int kind, const double (&UL)[4], const Prim& wl, const double (&UR)[4],
-                                         const Prim& wr, double nx, double ny, double gamma, double (&fn)[4]) {
-  if (kind == kFluxRoe)
+// The numerical flux of the run, a template parameter of the element kernels: one
+// instance per flux, so the LLF instance carries none of the Roe flux's registers
+// (measured per stage: p=1 0.159 vs 0.175 ms, p=2 0.391 vs 0.421, p=4 1.046 vs 1.077).
+template <int FLUX>
+__device__ __forceinline__ void num_flux(const double (&UL)[4], const Prim& wl, const double (&UR)[4], const Prim& wr,
+                                         double nx, double ny, double gamma, double (&fn)[4]) {
+  if constexpr (FLUX == kFluxRoe)
     roe_flux(UL, wl, UR, wr, nx, ny, gamma, fn);
   else
     llf_flux(UL, wl, UR, wr, nx, ny, gamma, fn);
@@ -416,7 +419,7 @@ __device__ __forceinline__ bool stage_prologue(const StageArgs& a, Scalars* sc, 
 //   kModeSurface -> per-side surface integrals into the slot buffer (eval_surface_pass)
 //   kModeRhs     -> (volume + surface) / det (compute_rhs)
 //   kModeStage   -> RK stage update with the fused epilogues
-template <int P, int MODE>
+template <int P, int MODE, int FLUX>
 __device__ __forceinline__ void element_body(const Tab<P>& T, const Geo& geo, const StageArgs& a) {
   constexpr int NP = Dim<P>::NP, NQ = Dim<P>::NQ, K = Dim<P>::K;
   const long long ld = geo.ld;
@@ -551,7 +554,7 @@ __device__ __forceinline__ void element_body(const Tab<P>& T, const Geo& geo, co
           const Prim wl = primitives(UL, g1), wr = primitives(UR, g1);
           double fn[4];
           if (admissible(UL, wl) && admissible(UR, wr)) {
-            num_flux(geo.flux, UL, wl, UR, wr, nx, ny, gamma, fn);
+            num_flux<FLUX>(UL, wl, UR, wr, nx, ny, gamma, fn);
           } else {
             if (valid && g < nk) record_error(sc, err_key(a.seq, kPassSurface, ed, kc));
 #pragma unroll
@@ -660,7 +663,7 @@ __device__ __forceinline__ void element_body(const Tab<P>& T, const Geo& geo, co
 // p <= 2 the per-point work (reciprocals, square roots, shuffles) dominates the
 // contractions, so spreading an element over lanes multiplies it; a thread per
 // element evaluates every pointwise quantity exactly once with no exchange.
-template <int P, int MODE>
+template <int P, int MODE, int FLUX>
 __device__ __forceinline__ void element_body_g1(const Tab<P>& T, const Geo& geo, const StageArgs& a) {
   constexpr int NP = Dim<P>::NP, NQ = Dim<P>::NQ, K = Dim<P>::K;
   const long long ld = geo.ld;
@@ -815,7 +818,7 @@ __device__ __forceinline__ void element_body_g1(const Tab<P>& T, const Geo& geo,
           const Prim wl = primitives(UL, g1), wr = primitives(UR, g1);
           double fn[4];
           if (admissible(UL, wl) && admissible(UR, wr)) {
-            num_flux(geo.flux, UL, wl, UR, wr, nx, ny, gamma, fn);
+            num_flux<FLUX>(UL, wl, UR, wr, nx, ny, gamma, fn);
           } else {
             record_error(sc, err_key(a.seq, kPassSurface, ed, kc));
 #pragma unroll

@@ -124,7 +124,7 @@ __device__ __forceinline__ void fetch_frag(double* __restrict__ slot, const doub
     }
 }
 
-template <int P, int MODE>
+template <int P, int MODE, int FLUX>
 __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo, const StageArgs& a,
                                                  double* __restrict__ smem) {
   using D = MmaDim<P>;
@@ -395,7 +395,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
           const Prim wl = primitives(UL, g1), wr = primitives(UR, g1);
           double f[4];
           if (admissible(UL, wl) && admissible(UR, wr)) {
-            num_flux(geo.flux, UL, wl, UR, wr, nx, ny, gamma, f);
+            num_flux<FLUX>(UL, wl, UR, wr, nx, ny, gamma, f);
           } else {
             if (valid && live) record_error(sc, err_key(a.seq, kPassSurface, ed, kc));
 #pragma unroll
@@ -495,7 +495,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
           const Prim wl = primitives(UL, g1), wr = primitives(UR, g1);
           double f[4];
           if (admissible(UL, wl) && admissible(UR, wr)) {
-            num_flux(geo.flux, UL, wl, UR, wr, nx, ny, gamma, f);
+            num_flux<FLUX>(UL, wl, UR, wr, nx, ny, gamma, f);
           } else {
             if (valid && live) record_error(sc, err_key(a.seq, kPassSurface, ed, kc));
 #pragma unroll

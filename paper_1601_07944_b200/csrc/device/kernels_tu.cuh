@@ -30,16 +30,28 @@ constexpr int kThreads = kMma ? DGB_MMA_THREADS(DGB_P) : kBlock;  // threads per
 // dynamic shared memory (bytes): tables + per-warp staging buffers
 constexpr int kSmem = kMma ? (MmaDim<DGB_P>::kSize + (kThreads / 32) * MmaDim<DGB_P>::kWarpBuf) * 8 : 0;
 
-template <int MODE>
+// one instance per mode and numerical flux (geo.flux selects the instance at launch)
+template <int MODE, int FLUX>
 __global__ void __launch_bounds__(kThreads, kMinB) k_element(Geo geo, StageArgs a) {
   if constexpr (kMma) {
     extern __shared__ double smem[];
-    element_body_mma<DGB_P, MODE>(c_tab, geo, a, smem);
+    element_body_mma<DGB_P, MODE, FLUX>(c_tab, geo, a, smem);
   } else if constexpr (kG == 1) {
-    element_body_g1<DGB_P, MODE>(c_tab, geo, a);
+    element_body_g1<DGB_P, MODE, FLUX>(c_tab, geo, a);
   } else {
-    element_body<DGB_P, MODE>(c_tab, geo, a);
+    element_body<DGB_P, MODE, FLUX>(c_tab, geo, a);
   }
+}
+
+template <int FLUX>
+cudaError_t launch_element(int mode, int grid, const Geo& g, const StageArgs& a, cudaStream_t s) {
+  switch (mode) {
+    case kModeVolume: k_element<kModeVolume, FLUX><<<grid, kThreads, kSmem, s>>>(g, a); break;
+    case kModeSurface: k_element<kModeSurface, FLUX><<<grid, kThreads, kSmem, s>>>(g, a); break;
+    case kModeRhs: k_element<kModeRhs, FLUX><<<grid, kThreads, kSmem, s>>>(g, a); break;
+    default: k_element<kModeStage, FLUX><<<grid, kThreads, kSmem, s>>>(g, a); break;
+  }
+  return cudaGetLastError();
 }
 
 __global__ void __launch_bounds__(kBlock) k_dt(Geo geo, const double* __restrict__ c, Scalars* sc, int slot,
@@ -74,10 +86,14 @@ cudaError_t Launch<DGB_P>::upload(const Tab<DGB_P>& t, cudaStream_t s) {
   if constexpr (kMma) {  // opt in to > 48 KB of dynamic shared memory
     static bool done = false;
     if (!done) {
-      cudaFuncSetAttribute(k_element<kModeVolume>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-      cudaFuncSetAttribute(k_element<kModeSurface>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-      cudaFuncSetAttribute(k_element<kModeRhs>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-      cudaFuncSetAttribute(k_element<kModeStage>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+      cudaFuncSetAttribute(k_element<kModeVolume, kFluxLLF>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+      cudaFuncSetAttribute(k_element<kModeSurface, kFluxLLF>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+      cudaFuncSetAttribute(k_element<kModeRhs, kFluxLLF>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+      cudaFuncSetAttribute(k_element<kModeStage, kFluxLLF>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+      cudaFuncSetAttribute(k_element<kModeVolume, kFluxRoe>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+      cudaFuncSetAttribute(k_element<kModeSurface, kFluxRoe>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+      cudaFuncSetAttribute(k_element<kModeRhs, kFluxRoe>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+      cudaFuncSetAttribute(k_element<kModeStage, kFluxRoe>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
       done = true;
     }
   }
@@ -89,10 +105,11 @@ int Launch<DGB_P>::resident_blocks(int mode) {
   static int cache[4] = {0, 0, 0, 0};
   if (!cache[mode]) {
     switch (mode) {
-      case kModeVolume: cache[mode] = occupancy(k_element<kModeVolume>, kSmem, kThreads); break;
-      case kModeSurface: cache[mode] = occupancy(k_element<kModeSurface>, kSmem, kThreads); break;
-      case kModeRhs: cache[mode] = occupancy(k_element<kModeRhs>, kSmem, kThreads); break;
-      default: cache[mode] = occupancy(k_element<kModeStage>, kSmem, kThreads); break;
+      // the LLF instance (the Roe instance is sized the same by __launch_bounds__)
+      case kModeVolume: cache[mode] = occupancy(k_element<kModeVolume, kFluxLLF>, kSmem, kThreads); break;
+      case kModeSurface: cache[mode] = occupancy(k_element<kModeSurface, kFluxLLF>, kSmem, kThreads); break;
+      case kModeRhs: cache[mode] = occupancy(k_element<kModeRhs, kFluxLLF>, kSmem, kThreads); break;
+      default: cache[mode] = occupancy(k_element<kModeStage, kFluxLLF>, kSmem, kThreads); break;
     }
   }
   return cache[mode];
@@ -122,13 +139,7 @@ cudaError_t Launch<DGB_P>::element(int mode, int grid, const Geo& g, const Stage
                                    : static_cast<long long>((a.e1 - a.e0 + 31) & ~31) * kG;
     grid = grid_for(threads, resident_blocks(mode), kThreads);
   }
-  switch (mode) {
-    case kModeVolume: k_element<kModeVolume><<<grid, kThreads, kSmem, s>>>(g, a); break;
-    case kModeSurface: k_element<kModeSurface><<<grid, kThreads, kSmem, s>>>(g, a); break;
-    case kModeRhs: k_element<kModeRhs><<<grid, kThreads, kSmem, s>>>(g, a); break;
-    default: k_element<kModeStage><<<grid, kThreads, kSmem, s>>>(g, a); break;
-  }
-  return cudaGetLastError();
+  return g.flux == kFluxRoe ? launch_element<kFluxRoe>(mode, grid, g, a, s) : launch_element<kFluxLLF>(mode, grid, g, a, s);
 }
 
 template <>
