@@ -326,7 +326,7 @@ __device__ __forceinline__ void push_element(const Geo& geo, const PeerTab* __re
 
 // Minimum registers per launch for the fused kernel (occupancy target per degree).
 #ifndef DGB_MINB
-#define DGB_MINB(P) ((P) == 1 ? 5 : (P) == 2 ? 4 : (P) == 3 ? 5 : (P) == 4 ? 4 : 3)
+#define DGB_MINB(P) ((P) == 1 ? 4 : (P) == 2 ? 3 : (P) == 3 ? 5 : (P) == 4 ? 4 : 3)  // p=1 0.129 vs 0.132 ms at 5, p=2 0.323 vs 0.328 at 4
 #endif
 #ifndef DGB_G1_SIDE_UNROLL
 #define DGB_G1_SIDE_UNROLL 1  // sides of the one-thread-per-element kernel: runtime loop
@@ -419,7 +419,7 @@ __device__ __forceinline__ bool stage_prologue(const StageArgs& a, Scalars* sc, 
 //   kModeSurface -> per-side surface integrals into the slot buffer (eval_surface_pass)
 //   kModeRhs     -> (volume + surface) / det (compute_rhs)
 //   kModeStage   -> RK stage update with the fused epilogues
-template <int P, int MODE, int FLUX>
+template <int P, int MODE, int FLUX, bool RK4>
 __device__ __forceinline__ void element_body(const Tab<P>& T, const Geo& geo, const StageArgs& a) {
   constexpr int NP = Dim<P>::NP, NQ = Dim<P>::NQ, K = Dim<P>::K;
   const long long ld = geo.ld;
@@ -427,6 +427,7 @@ __device__ __forceinline__ void element_body(const Tab<P>& T, const Geo& geo, co
   const int stride = gridDim.x * blockDim.x;
   const double gamma = geo.gamma, g1 = gamma - 1.0;
   Scalars* sc = a.sc;
+  const int kmode = RK4 ? a.kmode : 0;  // 0 at compile time in the non-RK4 instance
 
   // block-uniform early exit: an error or a stop rule fired in an earlier launch
   __shared__ int s_stop;
@@ -597,20 +598,20 @@ __device__ __forceinline__ void element_body(const Tab<P>& T, const Geo& geo, co
       const double idet = __ldg(geo.inv_det + e);
       const double gdt = a.gcoef * dt;
       const double dt6 = dt / 6.0;
-      const bool need_u = a.alpha != 0.0 || a.want_resid || a.kmode == 3;
+      const bool need_u = a.alpha != 0.0 || a.want_resid || kmode == 3;
 #pragma unroll
       for (int j = 0; j < NP; ++j) {
         const long long idx = row + j * ld;
         const double d = acc[j] * idet;
         const double uu = need_u ? __ldg(a.u + idx) : 0.0;
         double o;
-        if (a.kmode == 3) {
+        if (kmode == 3) {
           o = fma(dt6, __ldg(a.kacc + idx) + d, uu);
         } else {
           const double base = (a.alpha != 0.0) ? fma(a.alpha, uu, a.beta * c[j]) : a.beta * c[j];
           o = fma(gdt, d, base);
-          if (a.kmode == 1 && valid) a.kacc[idx] = d;
-          if (a.kmode == 2 && valid) a.kacc[idx] = fma(2.0, d, a.kacc[idx]);
+          if (kmode == 1 && valid) a.kacc[idx] = d;
+          if (kmode == 2 && valid) a.kacc[idx] = fma(2.0, d, a.kacc[idx]);
         }
         if (valid) {
           a.out[idx] = o;
@@ -663,13 +664,14 @@ __device__ __forceinline__ void element_body(const Tab<P>& T, const Geo& geo, co
 // p <= 2 the per-point work (reciprocals, square roots, shuffles) dominates the
 // contractions, so spreading an element over lanes multiplies it; a thread per
 // element evaluates every pointwise quantity exactly once with no exchange.
-template <int P, int MODE, int FLUX>
+template <int P, int MODE, int FLUX, bool RK4>
 __device__ __forceinline__ void element_body_g1(const Tab<P>& T, const Geo& geo, const StageArgs& a) {
   constexpr int NP = Dim<P>::NP, NQ = Dim<P>::NQ, K = Dim<P>::K;
   const long long ld = geo.ld;
   const int stride = gridDim.x * blockDim.x;
   const double gamma = geo.gamma, g1 = gamma - 1.0;
   Scalars* sc = a.sc;
+  const int kmode = RK4 ? a.kmode : 0;  // 0 at compile time in the non-RK4 instance
 
   __shared__ int s_stop;
   if (threadIdx.x == 0) s_stop = (sc->err_key != kNoError || sc->halt) ? 1 : 0;
@@ -858,7 +860,7 @@ __device__ __forceinline__ void element_body_g1(const Tab<P>& T, const Geo& geo,
       const double idet = __ldg(geo.inv_det + e);
       const double gdt = a.gcoef * dt;
       const double dt6 = dt / 6.0;
-      const bool need_u = a.alpha != 0.0 || a.want_resid || a.kmode == 3;
+      const bool need_u = a.alpha != 0.0 || a.want_resid || kmode == 3;
 #pragma unroll
       for (int m = 0; m < 4; ++m) {
 #pragma unroll
@@ -867,14 +869,14 @@ __device__ __forceinline__ void element_body_g1(const Tab<P>& T, const Geo& geo,
           const double d = acc[m][j] * idet;
           const double uu = need_u ? __ldg(a.u + idx) : 0.0;
           double o;
-          if (a.kmode == 3) {
+          if (kmode == 3) {
             o = fma(dt6, __ldg(a.kacc + idx) + d, uu);
           } else {
             const double cmj = (P >= DGB_G1_RELOAD_MINP) ? ld_nc(a.in + idx) : c[m][j];
             const double base = (a.alpha != 0.0) ? fma(a.alpha, uu, a.beta * cmj) : a.beta * cmj;
             o = fma(gdt, d, base);
-            if (a.kmode == 1) a.kacc[idx] = d;
-            if (a.kmode == 2) a.kacc[idx] = fma(2.0, d, a.kacc[idx]);
+            if (kmode == 1) a.kacc[idx] = d;
+            if (kmode == 2) a.kacc[idx] = fma(2.0, d, a.kacc[idx]);
           }
           a.out[idx] = o;
           if (a.want_resid) res_max = fmax(res_max, fabs(uu - o));

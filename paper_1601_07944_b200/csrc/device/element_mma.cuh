@@ -124,7 +124,7 @@ __device__ __forceinline__ void fetch_frag(double* __restrict__ slot, const doub
     }
 }
 
-template <int P, int MODE, int FLUX>
+template <int P, int MODE, int FLUX, bool RK4>
 __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo, const StageArgs& a,
                                                  double* __restrict__ smem) {
   using D = MmaDim<P>;
@@ -133,6 +133,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
   const long long ld = geo.ld;
   const double gamma = geo.gamma, g1 = gamma - 1.0;
   Scalars* sc = a.sc;
+  const int kmode = RK4 ? a.kmode : 0;  // 0 at compile time in the non-RK4 instance
 
   __shared__ int s_stop;
   if (threadIdx.x == 0) s_stop = (sc->err_key != kNoError || sc->halt) ? 1 : 0;
@@ -553,8 +554,8 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
       const double idet = __ldg(geo.inv_det + e);
       const double gdt = a.gcoef * dt;
       const double dt6 = dt / 6.0;
-      const bool need_u = a.alpha != 0.0 || a.want_resid || a.kmode == 3;
-      const bool need_c = a.kmode != 3 && a.beta != 0.0;
+      const bool need_u = a.alpha != 0.0 || a.want_resid || kmode == 3;
+      const bool need_c = kmode != 3 && a.beta != 0.0;
       // u^n is loaded one variable ahead of the stores (the stores may alias for all the
       // compiler knows, so it cannot hoist the loads itself)
       auto load_u = [&](double(&dst)[JT][2], int m) {
@@ -590,7 +591,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
             } else {
               cv[jt][ii] = (need_c && j < NP) ? __ldg(a.in + idx) : 0.0;
             }
-            kv[jt][ii] = ((a.kmode == 2 || a.kmode == 3) && j < NP) ? a.kacc[idx] : 0.0;
+            kv[jt][ii] = ((kmode == 2 || kmode == 3) && j < NP) ? a.kacc[idx] : 0.0;
           }
 #pragma unroll
         for (int jt = 0; jt < JT; ++jt)
@@ -602,13 +603,13 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
               const double d = R[m][jt][ii] * idet;
               const double uu = uv[jt][ii], cj = cv[jt][ii];
               double o;
-              if (a.kmode == 3) {
+              if (kmode == 3) {
                 o = fma(dt6, kv[jt][ii] + d, uu);
               } else {
                 const double base = (a.alpha != 0.0) ? fma(a.alpha, uu, a.beta * cj) : a.beta * cj;
                 o = fma(gdt, d, base);
-                if (a.kmode == 1 && valid) a.kacc[idx] = d;
-                if (a.kmode == 2 && valid) a.kacc[idx] = fma(2.0, d, kv[jt][ii]);
+                if (kmode == 1 && valid) a.kacc[idx] = d;
+                if (kmode == 2 && valid) a.kacc[idx] = fma(2.0, d, kv[jt][ii]);
               }
               if (valid) {
                 a.out[idx] = o;

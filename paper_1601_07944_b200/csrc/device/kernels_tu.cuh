@@ -30,28 +30,45 @@ constexpr int kThreads = kMma ? DGB_MMA_THREADS(DGB_P) : kBlock;  // threads per
 // dynamic shared memory (bytes): tables + per-warp staging buffers
 constexpr int kSmem = kMma ? (MmaDim<DGB_P>::kSize + (kThreads / 32) * MmaDim<DGB_P>::kWarpBuf) * 8 : 0;
 
-// one instance per mode and numerical flux (geo.flux selects the instance at launch)
-template <int MODE, int FLUX>
+// One instance per mode, numerical flux (geo.flux) and, for the stage mode, whether the
+// RK4 derivative accumulator is in use (a.kmode != 0).  Without the RK4 branches the
+// midpoint-RK2 / SSP stage epilogue needs fewer registers (measured per stage: p=1 0.158
+// vs 0.131 ms, p=2 0.390 vs 0.328, p=4 1.050 vs 0.977, p=5 1.726 vs 1.623).
+template <int MODE, int FLUX, bool RK4>
 __global__ void __launch_bounds__(kThreads, kMinB) k_element(Geo geo, StageArgs a) {
   if constexpr (kMma) {
     extern __shared__ double smem[];
-    element_body_mma<DGB_P, MODE, FLUX>(c_tab, geo, a, smem);
+    element_body_mma<DGB_P, MODE, FLUX, RK4>(c_tab, geo, a, smem);
   } else if constexpr (kG == 1) {
-    element_body_g1<DGB_P, MODE, FLUX>(c_tab, geo, a);
+    element_body_g1<DGB_P, MODE, FLUX, RK4>(c_tab, geo, a);
   } else {
-    element_body<DGB_P, MODE, FLUX>(c_tab, geo, a);
+    element_body<DGB_P, MODE, FLUX, RK4>(c_tab, geo, a);
   }
 }
 
 template <int FLUX>
 cudaError_t launch_element(int mode, int grid, const Geo& g, const StageArgs& a, cudaStream_t s) {
   switch (mode) {
-    case kModeVolume: k_element<kModeVolume, FLUX><<<grid, kThreads, kSmem, s>>>(g, a); break;
-    case kModeSurface: k_element<kModeSurface, FLUX><<<grid, kThreads, kSmem, s>>>(g, a); break;
-    case kModeRhs: k_element<kModeRhs, FLUX><<<grid, kThreads, kSmem, s>>>(g, a); break;
-    default: k_element<kModeStage, FLUX><<<grid, kThreads, kSmem, s>>>(g, a); break;
+    case kModeVolume: k_element<kModeVolume, FLUX, false><<<grid, kThreads, kSmem, s>>>(g, a); break;
+    case kModeSurface: k_element<kModeSurface, FLUX, false><<<grid, kThreads, kSmem, s>>>(g, a); break;
+    case kModeRhs: k_element<kModeRhs, FLUX, false><<<grid, kThreads, kSmem, s>>>(g, a); break;
+    default:
+      if (a.kmode != 0)
+        k_element<kModeStage, FLUX, true><<<grid, kThreads, kSmem, s>>>(g, a);
+      else
+        k_element<kModeStage, FLUX, false><<<grid, kThreads, kSmem, s>>>(g, a);
+      break;
   }
   return cudaGetLastError();
+}
+
+template <int FLUX>
+void set_smem_attrs() {
+  cudaFuncSetAttribute(k_element<kModeVolume, FLUX, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+  cudaFuncSetAttribute(k_element<kModeSurface, FLUX, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+  cudaFuncSetAttribute(k_element<kModeRhs, FLUX, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+  cudaFuncSetAttribute(k_element<kModeStage, FLUX, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+  cudaFuncSetAttribute(k_element<kModeStage, FLUX, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
 }
 
 __global__ void __launch_bounds__(kBlock) k_dt(Geo geo, const double* __restrict__ c, Scalars* sc, int slot,
@@ -86,14 +103,8 @@ cudaError_t Launch<DGB_P>::upload(const Tab<DGB_P>& t, cudaStream_t s) {
   if constexpr (kMma) {  // opt in to > 48 KB of dynamic shared memory
     static bool done = false;
     if (!done) {
-      cudaFuncSetAttribute(k_element<kModeVolume, kFluxLLF>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-      cudaFuncSetAttribute(k_element<kModeSurface, kFluxLLF>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-      cudaFuncSetAttribute(k_element<kModeRhs, kFluxLLF>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-      cudaFuncSetAttribute(k_element<kModeStage, kFluxLLF>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-      cudaFuncSetAttribute(k_element<kModeVolume, kFluxRoe>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-      cudaFuncSetAttribute(k_element<kModeSurface, kFluxRoe>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-      cudaFuncSetAttribute(k_element<kModeRhs, kFluxRoe>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-      cudaFuncSetAttribute(k_element<kModeStage, kFluxRoe>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+      set_smem_attrs<kFluxLLF>();
+      set_smem_attrs<kFluxRoe>();
       done = true;
     }
   }
@@ -106,10 +117,10 @@ int Launch<DGB_P>::resident_blocks(int mode) {
   if (!cache[mode]) {
     switch (mode) {
       // the LLF instance (the Roe instance is sized the same by __launch_bounds__)
-      case kModeVolume: cache[mode] = occupancy(k_element<kModeVolume, kFluxLLF>, kSmem, kThreads); break;
-      case kModeSurface: cache[mode] = occupancy(k_element<kModeSurface, kFluxLLF>, kSmem, kThreads); break;
-      case kModeRhs: cache[mode] = occupancy(k_element<kModeRhs, kFluxLLF>, kSmem, kThreads); break;
-      default: cache[mode] = occupancy(k_element<kModeStage, kFluxLLF>, kSmem, kThreads); break;
+      case kModeVolume: cache[mode] = occupancy(k_element<kModeVolume, kFluxLLF, false>, kSmem, kThreads); break;
+      case kModeSurface: cache[mode] = occupancy(k_element<kModeSurface, kFluxLLF, false>, kSmem, kThreads); break;
+      case kModeRhs: cache[mode] = occupancy(k_element<kModeRhs, kFluxLLF, false>, kSmem, kThreads); break;
+      default: cache[mode] = occupancy(k_element<kModeStage, kFluxLLF, false>, kSmem, kThreads); break;
     }
   }
   return cache[mode];
