@@ -96,6 +96,7 @@ struct Geo {
   const double* __restrict__ bwn;      // [n_bnd][K][2] exact wall normals
   const double* __restrict__ bx;       // [n_bnd][K][2] boundary Gauss points
   int has_dir, has_wn, has_shock;
+  int has_bnd;                         // some owned element has a physical-boundary side
   double inflow[4];
   double sh_x0, sh_cos, sh_sin, sh_speed;
   double sh_post[4], sh_pre[4];
@@ -112,6 +113,12 @@ struct Geo {
 
 // Modes of the fused element kernel.
 enum : int { kModeVolume = 0, kModeSurface = 1, kModeRhs = 2, kModeStage = 3 };
+
+// Instance variants of the element kernel (bit set): the RK4 derivative accumulator is in
+// use, the CFL wave speeds are wanted (last stage of a step), the partition has elements
+// on the physical boundary.  Each unused path is compiled out of its instance, which
+// frees registers in the common case (SSP / midpoint stages, periodic meshes).
+enum : int { kVarRk4 = 1, kVarLambda = 2, kVarBoundary = 4 };
 
 struct StageArgs {
   const double* __restrict__ in;  // stage input coefficients

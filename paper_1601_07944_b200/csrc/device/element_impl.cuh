@@ -419,7 +419,7 @@ __device__ __forceinline__ bool stage_prologue(const StageArgs& a, Scalars* sc, 
 //   kModeSurface -> per-side surface integrals into the slot buffer (eval_surface_pass)
 //   kModeRhs     -> (volume + surface) / det (compute_rhs)
 //   kModeStage   -> RK stage update with the fused epilogues
-template <int P, int MODE, int FLUX, bool RK4>
+template <int P, int MODE, int FLUX, int VAR>
 __device__ __forceinline__ void element_body(const Tab<P>& T, const Geo& geo, const StageArgs& a) {
   constexpr int NP = Dim<P>::NP, NQ = Dim<P>::NQ, K = Dim<P>::K;
   const long long ld = geo.ld;
@@ -427,7 +427,10 @@ __device__ __forceinline__ void element_body(const Tab<P>& T, const Geo& geo, co
   const int stride = gridDim.x * blockDim.x;
   const double gamma = geo.gamma, g1 = gamma - 1.0;
   Scalars* sc = a.sc;
-  const int kmode = RK4 ? a.kmode : 0;  // 0 at compile time in the non-RK4 instance
+  // instance variant (kernels_tu.cuh): paths the launch knows are unused compile away
+  constexpr bool RK4 = VAR & kVarRk4, LAM = VAR & kVarLambda, BND = VAR & kVarBoundary;
+  const int kmode = RK4 ? a.kmode : 0;
+  const bool want_lambda = LAM && a.want_lambda;
 
   // block-uniform early exit: an error or a stop rule fired in an earlier launch
   __shared__ int s_stop;
@@ -551,7 +554,7 @@ __device__ __forceinline__ void element_body(const Tab<P>& T, const Geo& geo, co
           transpose4(UR, g);
           const int ko = (g < nk) ? k0 + g : k0;
           const int kc = left ? ko : K - 1 - ko;  // canonical (left-element) point index
-          if (bnd) ghost_state<K>(UL, nb, ed, kc, nx, ny, tstage, geo, UR);
+          if (BND && bnd) ghost_state<K>(UL, nb, ed, kc, nx, ny, tstage, geo, UR);
           const Prim wl = primitives(UL, g1), wr = primitives(UR, g1);
           double fn[4];
           if (admissible(UL, wl) && admissible(UR, wr)) {
@@ -623,7 +626,7 @@ __device__ __forceinline__ void element_body(const Tab<P>& T, const Geo& geo, co
         const double(&v)[1][NP] = reinterpret_cast<const double(&)[1][NP]>(acc);
         push_element<NP, 1>(geo, a.peers, a.out_buf, e, g, v);
       }
-      if (a.want_lambda) {
+      if (want_lambda) {
         double v[4];
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
@@ -653,7 +656,7 @@ __device__ __forceinline__ void element_body(const Tab<P>& T, const Geo& geo, co
 
   if constexpr (MODE == kModeStage) {
     const int par = a.step & 1;
-    if (a.want_lambda) block_reduce_atomic<true>(lam_min, &sc->dtmin[par ^ 1]);
+    if (want_lambda) block_reduce_atomic<true>(lam_min, &sc->dtmin[par ^ 1]);
     if (a.want_resid) block_reduce_atomic<false>(res_max, &sc->resid[par]);
     if (a.push) __threadfence_system();  // halo stores visible before the signal kernel's flag
   }
@@ -664,14 +667,17 @@ __device__ __forceinline__ void element_body(const Tab<P>& T, const Geo& geo, co
 // p <= 2 the per-point work (reciprocals, square roots, shuffles) dominates the
 // contractions, so spreading an element over lanes multiplies it; a thread per
 // element evaluates every pointwise quantity exactly once with no exchange.
-template <int P, int MODE, int FLUX, bool RK4>
+template <int P, int MODE, int FLUX, int VAR>
 __device__ __forceinline__ void element_body_g1(const Tab<P>& T, const Geo& geo, const StageArgs& a) {
   constexpr int NP = Dim<P>::NP, NQ = Dim<P>::NQ, K = Dim<P>::K;
   const long long ld = geo.ld;
   const int stride = gridDim.x * blockDim.x;
   const double gamma = geo.gamma, g1 = gamma - 1.0;
   Scalars* sc = a.sc;
-  const int kmode = RK4 ? a.kmode : 0;  // 0 at compile time in the non-RK4 instance
+  // instance variant (kernels_tu.cuh): paths the launch knows are unused compile away
+  constexpr bool RK4 = VAR & kVarRk4, LAM = VAR & kVarLambda, BND = VAR & kVarBoundary;
+  const int kmode = RK4 ? a.kmode : 0;
+  const bool want_lambda = LAM && a.want_lambda;
 
   __shared__ int s_stop;
   if (threadIdx.x == 0) s_stop = (sc->err_key != kNoError || sc->halt) ? 1 : 0;
@@ -816,7 +822,7 @@ __device__ __forceinline__ void element_body_g1(const Tab<P>& T, const Geo& geo,
             UR[m] = left ? un[ko][m] : uo[m];
           }
           const int kc = left ? ko : K - 1 - ko;
-          if (bnd) ghost_state<K>(UL, nb, ed, kc, nx, ny, tstage, geo, UR);
+          if (BND && bnd) ghost_state<K>(UL, nb, ed, kc, nx, ny, tstage, geo, UR);
           const Prim wl = primitives(UL, g1), wr = primitives(UR, g1);
           double fn[4];
           if (admissible(UL, wl) && admissible(UR, wr)) {
@@ -884,7 +890,7 @@ __device__ __forceinline__ void element_body_g1(const Tab<P>& T, const Geo& geo,
         }
       }
       if (a.push && e >= geo.send_begin) push_element<NP, 4>(geo, a.peers, a.out_buf, e, 0, acc);
-      if (a.want_lambda) {
+      if (want_lambda) {
         double lam = 0.0;
 #pragma unroll 1
         for (int q = 0; q < 3; ++q) {
@@ -911,7 +917,7 @@ __device__ __forceinline__ void element_body_g1(const Tab<P>& T, const Geo& geo,
 
   if constexpr (MODE == kModeStage) {
     const int par = a.step & 1;
-    if (a.want_lambda) block_reduce_atomic<true>(lam_min, &sc->dtmin[par ^ 1]);
+    if (want_lambda) block_reduce_atomic<true>(lam_min, &sc->dtmin[par ^ 1]);
     if (a.want_resid) block_reduce_atomic<false>(res_max, &sc->resid[par]);
     if (a.push) __threadfence_system();  // halo stores visible before the signal kernel's flag
   }

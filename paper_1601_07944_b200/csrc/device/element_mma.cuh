@@ -124,7 +124,7 @@ __device__ __forceinline__ void fetch_frag(double* __restrict__ slot, const doub
     }
 }
 
-template <int P, int MODE, int FLUX, bool RK4>
+template <int P, int MODE, int FLUX, int VAR>
 __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo, const StageArgs& a,
                                                  double* __restrict__ smem) {
   using D = MmaDim<P>;
@@ -133,7 +133,10 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
   const long long ld = geo.ld;
   const double gamma = geo.gamma, g1 = gamma - 1.0;
   Scalars* sc = a.sc;
-  const int kmode = RK4 ? a.kmode : 0;  // 0 at compile time in the non-RK4 instance
+  // instance variant (kernels_tu.cuh): paths the launch knows are unused compile away
+  constexpr bool RK4 = VAR & kVarRk4, LAM = VAR & kVarLambda, BND = VAR & kVarBoundary;
+  const int kmode = RK4 ? a.kmode : 0;
+  const bool want_lambda = LAM && a.want_lambda;
 
   __shared__ int s_stop;
   if (threadIdx.x == 0) s_stop = (sc->err_key != kNoError || sc->halt) ? 1 : 0;
@@ -392,7 +395,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
             UR[m] = left ? Tn[m][i] : Tw[m][i];
           }
           const int kc = left ? ko : K - 1 - ko;  // canonical (left-element) point index
-          if (bnd && live) ghost_state<K>(UL, nb, ed, kc, nx, ny, tstage, geo, UR);
+          if (BND && bnd && live) ghost_state<K>(UL, nb, ed, kc, nx, ny, tstage, geo, UR);
           const Prim wl = primitives(UL, g1), wr = primitives(UR, g1);
           double f[4];
           if (admissible(UL, wl) && admissible(UR, wr)) {
@@ -492,7 +495,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
           }
           const int kc = left ? ko : K - 1 - ko;  // canonical (left-element) point index
           const bool live = ko < K;
-          if (bnd && live) ghost_state<K>(UL, nb, ed, kc, nx, ny, tstage, geo, UR);
+          if (BND && bnd && live) ghost_state<K>(UL, nb, ed, kc, nx, ny, tstage, geo, UR);
           const Prim wl = primitives(UL, g1), wr = primitives(UR, g1);
           double f[4];
           if (admissible(UL, wl) && admissible(UR, wr)) {
@@ -639,7 +642,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
               }
         }
       }
-      if (a.want_lambda) {
+      if (want_lambda) {
         // states at the 3 side midpoints: partial sums over this lane's modes, then
         // reduced over the 4 lanes of the element
         double v[3][4];
@@ -687,7 +690,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
 
   if constexpr (MODE == kModeStage) {
     const int par = a.step & 1;
-    if (a.want_lambda) block_reduce_atomic<true>(lam_min, &sc->dtmin[par ^ 1]);
+    if (want_lambda) block_reduce_atomic<true>(lam_min, &sc->dtmin[par ^ 1]);
     if (a.want_resid) block_reduce_atomic<false>(res_max, &sc->resid[par]);
     if (a.push) __threadfence_system();
   }

@@ -30,45 +30,66 @@ constexpr int kThreads = kMma ? DGB_MMA_THREADS(DGB_P) : kBlock;  // threads per
 // dynamic shared memory (bytes): tables + per-warp staging buffers
 constexpr int kSmem = kMma ? (MmaDim<DGB_P>::kSize + (kThreads / 32) * MmaDim<DGB_P>::kWarpBuf) * 8 : 0;
 
-// One instance per mode, numerical flux (geo.flux) and, for the stage mode, whether the
-// RK4 derivative accumulator is in use (a.kmode != 0).  Without the RK4 branches the
-// midpoint-RK2 / SSP stage epilogue needs fewer registers (measured per stage: p=1 0.158
-// vs 0.131 ms, p=2 0.390 vs 0.328, p=4 1.050 vs 0.977, p=5 1.726 vs 1.623).
-template <int MODE, int FLUX, bool RK4>
+// One instance per mode, numerical flux (geo.flux) and variant (kVar* bits, dg_kernels.cuh):
+// the stage mode with or without the RK4 accumulator (a.kmode != 0) and the CFL epilogue
+// (a.want_lambda), and every surface mode with or without physical-boundary code
+// (geo.has_bnd).  Without the RK4 branches the midpoint-RK2 / SSP stage needs fewer
+// registers (measured per stage: p=1 0.158 vs 0.131 ms, p=2 0.390 vs 0.328, p=4 1.050 vs
+// 0.977, p=5 1.726 vs 1.623).
+template <int MODE, int FLUX, int VAR>
 __global__ void __launch_bounds__(kThreads, kMinB) k_element(Geo geo, StageArgs a) {
   if constexpr (kMma) {
     extern __shared__ double smem[];
-    element_body_mma<DGB_P, MODE, FLUX, RK4>(c_tab, geo, a, smem);
+    element_body_mma<DGB_P, MODE, FLUX, VAR>(c_tab, geo, a, smem);
   } else if constexpr (kG == 1) {
-    element_body_g1<DGB_P, MODE, FLUX, RK4>(c_tab, geo, a);
+    element_body_g1<DGB_P, MODE, FLUX, VAR>(c_tab, geo, a);
   } else {
-    element_body<DGB_P, MODE, FLUX, RK4>(c_tab, geo, a);
+    element_body<DGB_P, MODE, FLUX, VAR>(c_tab, geo, a);
   }
 }
 
-template <int FLUX>
-cudaError_t launch_element(int mode, int grid, const Geo& g, const StageArgs& a, cudaStream_t s) {
+// Calls f(kernel) for the instance that serves (mode, flux, var).
+template <int FLUX, class F>
+void with_instance(int mode, int var, F&& f) {
   switch (mode) {
-    case kModeVolume: k_element<kModeVolume, FLUX, false><<<grid, kThreads, kSmem, s>>>(g, a); break;
-    case kModeSurface: k_element<kModeSurface, FLUX, false><<<grid, kThreads, kSmem, s>>>(g, a); break;
-    case kModeRhs: k_element<kModeRhs, FLUX, false><<<grid, kThreads, kSmem, s>>>(g, a); break;
+    case kModeVolume: f(k_element<kModeVolume, FLUX, 0>); break;
+    case kModeSurface:
+      if (var & kVarBoundary) f(k_element<kModeSurface, FLUX, kVarBoundary>); else f(k_element<kModeSurface, FLUX, 0>);
+      break;
+    case kModeRhs:
+      if (var & kVarBoundary) f(k_element<kModeRhs, FLUX, kVarBoundary>); else f(k_element<kModeRhs, FLUX, 0>);
+      break;
     default:
-      if (a.kmode != 0)
-        k_element<kModeStage, FLUX, true><<<grid, kThreads, kSmem, s>>>(g, a);
-      else
-        k_element<kModeStage, FLUX, false><<<grid, kThreads, kSmem, s>>>(g, a);
+      switch (var & 7) {
+        case 0: f(k_element<kModeStage, FLUX, 0>); break;
+        case 1: f(k_element<kModeStage, FLUX, 1>); break;
+        case 2: f(k_element<kModeStage, FLUX, 2>); break;
+        case 3: f(k_element<kModeStage, FLUX, 3>); break;
+        case 4: f(k_element<kModeStage, FLUX, 4>); break;
+        case 5: f(k_element<kModeStage, FLUX, 5>); break;
+        case 6: f(k_element<kModeStage, FLUX, 6>); break;
+        default: f(k_element<kModeStage, FLUX, 7>); break;
+      }
       break;
   }
-  return cudaGetLastError();
 }
-
-template <int FLUX>
-void set_smem_attrs() {
-  cudaFuncSetAttribute(k_element<kModeVolume, FLUX, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-  cudaFuncSetAttribute(k_element<kModeSurface, FLUX, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-  cudaFuncSetAttribute(k_element<kModeRhs, FLUX, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-  cudaFuncSetAttribute(k_element<kModeStage, FLUX, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-  cudaFuncSetAttribute(k_element<kModeStage, FLUX, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+template <class F>
+void with_instance(int flux, int mode, int var, F&& f) {
+  if (flux == kFluxRoe)
+    with_instance<kFluxRoe>(mode, var, f);
+  else
+    with_instance<kFluxLLF>(mode, var, f);
+}
+#ifndef DGB_VAR_MASK
+// variant bits specialised per degree (the others take the full path); measured per stage on the
+// periodic box: p=2 0.307 ms with the boundary code kept vs 0.341 without (register allocation)
+#define DGB_VAR_MASK(P) ((P) == 2 ? (kVarRk4 | kVarLambda) : 7)
+#endif
+int variant_of(int mode, const Geo& g, const StageArgs& a) {
+  constexpr int mask = DGB_VAR_MASK(DGB_P);
+  int v = g.has_bnd ? kVarBoundary : 0;
+  if (mode == kModeStage) v |= (a.kmode != 0 ? kVarRk4 : 0) | (a.want_lambda ? kVarLambda : 0);
+  return (v & mask) | (7 & ~mask);
 }
 
 __global__ void __launch_bounds__(kBlock) k_dt(Geo geo, const double* __restrict__ c, Scalars* sc, int slot,
@@ -103,8 +124,12 @@ cudaError_t Launch<DGB_P>::upload(const Tab<DGB_P>& t, cudaStream_t s) {
   if constexpr (kMma) {  // opt in to > 48 KB of dynamic shared memory
     static bool done = false;
     if (!done) {
-      set_smem_attrs<kFluxLLF>();
-      set_smem_attrs<kFluxRoe>();
+      for (int flux = 0; flux < 2; ++flux)
+        for (int mode = 0; mode < 4; ++mode)
+          for (int var = 0; var < 8; ++var)
+            with_instance(flux, mode, var, [](auto k) {
+              cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+            });
       done = true;
     }
   }
@@ -113,16 +138,10 @@ cudaError_t Launch<DGB_P>::upload(const Tab<DGB_P>& t, cudaStream_t s) {
 
 template <>
 int Launch<DGB_P>::resident_blocks(int mode) {
+  // the LLF instance of the full variant (the others are sized the same by __launch_bounds__)
   static int cache[4] = {0, 0, 0, 0};
-  if (!cache[mode]) {
-    switch (mode) {
-      // the LLF instance (the Roe instance is sized the same by __launch_bounds__)
-      case kModeVolume: cache[mode] = occupancy(k_element<kModeVolume, kFluxLLF, false>, kSmem, kThreads); break;
-      case kModeSurface: cache[mode] = occupancy(k_element<kModeSurface, kFluxLLF, false>, kSmem, kThreads); break;
-      case kModeRhs: cache[mode] = occupancy(k_element<kModeRhs, kFluxLLF, false>, kSmem, kThreads); break;
-      default: cache[mode] = occupancy(k_element<kModeStage, kFluxLLF, false>, kSmem, kThreads); break;
-    }
-  }
+  if (!cache[mode])
+    with_instance(kFluxLLF, mode, 7, [&](auto k) { cache[mode] = occupancy(k, kSmem, kThreads); });
   return cache[mode];
 }
 
@@ -150,7 +169,12 @@ cudaError_t Launch<DGB_P>::element(int mode, int grid, const Geo& g, const Stage
                                    : static_cast<long long>((a.e1 - a.e0 + 31) & ~31) * kG;
     grid = grid_for(threads, resident_blocks(mode), kThreads);
   }
-  return g.flux == kFluxRoe ? launch_element<kFluxRoe>(mode, grid, g, a, s) : launch_element<kFluxLLF>(mode, grid, g, a, s);
+  cudaError_t err = cudaSuccess;
+  with_instance(g.flux, mode, variant_of(mode, g, a), [&](auto k) {
+    k<<<grid, kThreads, kSmem, s>>>(g, a);
+    err = cudaGetLastError();
+  });
+  return err;
 }
 
 template <>

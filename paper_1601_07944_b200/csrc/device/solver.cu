@@ -1159,6 +1159,10 @@ int dgb_part_create(const dgb_mesh_view* m, const dgb_tables_view* t, const dgb_
     c->d_inv_det.upload(inv_det.data(), ld, c->stream);
     c->d_inradius.upload(inr.data(), ld, c->stream);
     c->d_nbr.upload(nbr.data(), nbr.size(), c->stream);
+    c->geo.has_bnd = 0;  // any owned element with a boundary code (padding columns hold -4 too)
+    for (int q = 0; q < 3; ++q)
+      for (int d = 0; d < N; ++d)
+        if (nbr[static_cast<size_t>(q) * ld + d] < 0) c->geo.has_bnd = 1;
     c->d_eid.upload(eid.data(), eid.size(), c->stream);
     c->d_info.upload(info.data(), ld, c->stream);
     c->d_ref_id.upload(ref_id.data(), ld, c->stream);
