@@ -124,6 +124,22 @@ __device__ __forceinline__ void fetch_frag(double* __restrict__ slot, const doub
     }
 }
 
+// Projection k-step of a half-live 8-point tile (live points 2t+i only for t < 2): the
+// two k-steps (slot t <- point 2t+i, i = 0, 1) collapse into one whose slot t < 2 takes
+// this lane's point i=0 and slot t >= 2 the point i=1 of lane t-2 (one shuffle per value).
+// The B fragment of that slot is the existing table entry of k-step i=1 at lane-2, so the
+// caller offsets its table index by the returned flag * (one k-step of fragments - 2).
+__device__ __forceinline__ int half_operands(const double (&v)[4][2], double (&a)[4], int lane, int t) {
+  const bool hi = t >= 2;
+  const int src = (lane + 30) & 31;
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    const double o = __shfl_sync(0xffffffffu, v[m][1], src);
+    a[m] = hi ? o : v[m][0];
+  }
+  return hi ? 1 : 0;
+}
+
 template <int P, int MODE, int FLUX, int VAR>
 __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo, const StageArgs& a,
                                                  double* __restrict__ smem) {
@@ -162,6 +178,10 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
   double* __restrict__ w_nbr = w_own + FR;
   // packed surface (p = 3, 4): a second neighbour buffer, side q lives in buffer q & 1
   constexpr bool kPk = D::kPacked && (MODE == kModeRhs || MODE == kModeStage);
+  // last point tile / last packed surface tile with only slots t < 2 live (p = 3: Q = 12,
+  // 3K = 12): its projection is one compacted k-step (half_operands)
+  constexpr bool kHalfQ = NQ % 8 == 4 && !D::kTail1;
+  constexpr bool kHalfS = kPk && (3 * K) % 8 == 4;
   // stage mode: the epilogue reads the stage input from the own fragment buffer (shared
   // memory) instead of global memory; the next tile's own prefetch waits until then
   constexpr bool kCSmem = P >= DGB_MMA_C_SMEM_MINP && MODE == kModeStage;
@@ -267,6 +287,22 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
           }
         }
         __syncwarp();
+        if (kHalfQ && nt == NTD - 1) {
+          // half-live last tile (p = 3: points 8..11): one compacted k-step instead of two
+          double ar[4], as[4];
+          const int boff = half_operands(fr, ar, lane, t) * (JT * 32 - 2);
+          half_operands(fs, as, lane, t);
+#pragma unroll
+          for (int jt = 0; jt < JT; ++jt) {
+            const double br = smem[D::kDr + (nt * 2 * JT + jt) * 32 + lane + boff];
+            const double bs = smem[D::kDs + (nt * 2 * JT + jt) * 32 + lane + boff];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) dmma(R[m][jt], ar[m], br);
+#pragma unroll
+            for (int m = 0; m < 4; ++m) dmma(R[m][jt], as[m], bs);
+          }
+          continue;
+        }
 #pragma unroll
         for (int i = 0; i < 2; ++i)
 #pragma unroll
@@ -410,6 +446,17 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
           for (int m = 0; m < 4; ++m) fn[m][i] = left ? -(wh * f[m]) : (wh * f[m]);
         }
         __syncwarp();
+        if (kHalfS && sp == D::NSP - 1) {  // half-live last packed tile (p = 3): one k-step
+          double an[4];
+          const int boff = half_operands(fn, an, lane, t) * (JT * 32 - 2);
+#pragma unroll
+          for (int jt = 0; jt < JT; ++jt) {
+            const double b = smem[D::kPkProj + (sp * 2 * JT + jt) * 32 + lane + boff];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) dmma(R[m][jt], an[m], b);
+          }
+          continue;
+        }
 #pragma unroll
         for (int i = 0; i < 2; ++i)
 #pragma unroll
