@@ -23,6 +23,13 @@ __device__ __forceinline__ unsigned long long err_key(unsigned long long seq, in
 
 __device__ __forceinline__ void record_error(Scalars* sc, unsigned long long key) { atomicMin(&sc->err_key, key); }
 
+// std::max / std::min / std::clamp(x, 0, 1) as the reference evaluates them (plain
+// compare-and-select): fmax/fmin carry NaN-propagation fix-ups (~6 instructions each on
+// sm_100a), and the limiter's extreme searches are most of its instruction stream.
+__device__ __forceinline__ double std_max(double a, double b) { return a < b ? b : a; }
+__device__ __forceinline__ double std_min(double a, double b) { return b < a ? b : a; }
+__device__ __forceinline__ double std_clamp01(double x) { return x < 0.0 ? 0.0 : (1.0 < x ? 1.0 : x); }
+
 // Select variable m of a full state without local-memory indexing.
 __device__ __forceinline__ double pick4(const double (&v)[4], int m) {
   double r = v[0];
@@ -121,7 +128,7 @@ __device__ __forceinline__ void llf_flux(const double (&UL)[4], const Prim& wl, 
   normal_flux(UR, wr, nx, ny, vnr, fr);
   const double sl = fabs(vnl) + sqrt_nr(gamma * wl.p * wl.inv);
   const double sr = fabs(vnr) + sqrt_nr(gamma * wr.p * wr.inv);
-  const double hs = 0.5 * fmax(sl, sr);
+  const double hs = 0.5 * std_max(sl, sr);  // std::max as euler.hpp:64
 #pragma unroll
   for (int m = 0; m < 4; ++m) fn[m] = fma(0.5, fl[m] + fr[m], -hs * (UR[m] - UL[m]));
 }
@@ -618,7 +625,7 @@ __device__ __forceinline__ void element_body(const Tab<P>& T, const Geo& geo, co
         }
         if (valid) {
           a.out[idx] = o;
-          if (a.want_resid) res_max = fmax(res_max, fabs(uu - o));
+          if (a.want_resid) res_max = std_max(res_max, fabs(uu - o));
         }
         acc[j] = o;  // keep the new stage for the CFL epilogue
       }
@@ -885,7 +892,7 @@ __device__ __forceinline__ void element_body_g1(const Tab<P>& T, const Geo& geo,
             if (kmode == 2) a.kacc[idx] = fma(2.0, d, a.kacc[idx]);
           }
           a.out[idx] = o;
-          if (a.want_resid) res_max = fmax(res_max, fabs(uu - o));
+          if (a.want_resid) res_max = std_max(res_max, fabs(uu - o));
           acc[m][j] = o;
         }
       }

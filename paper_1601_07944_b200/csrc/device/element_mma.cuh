@@ -663,7 +663,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
               }
               if (valid) {
                 a.out[idx] = o;
-                if (a.want_resid) res_max = fmax(res_max, fabs(uu - o));
+                if (a.want_resid) res_max = std_max(res_max, fabs(uu - o));
               }
               R[m][jt][ii] = o;  // keep the new stage for the CFL epilogue / halo push
             } else {

@@ -24,8 +24,11 @@ namespace {
 #ifndef DGB_LIMIT_CFL_PREFETCH
 #define DGB_LIMIT_CFL_PREFETCH 1
 #endif
-template <int NE, int NPT>
+// EPI: epilogues compiled into the instance (1: CFL bound, 2: residual), the launch passes
+// a.want_lambda / a.want_resid; the intermediate-stage instance carries neither.
+template <int NE, int NPT, int EPI>
 __global__ void __launch_bounds__(kBlock, DGB_LIMIT_MINB) k_limit(Geo geo, LimArgs a) {
+  const bool want_lambda = (EPI & 1) && a.want_lambda, want_resid = (EPI & 2) && a.want_resid;
   constexpr int NP = 3;
   const long long ld = geo.ld;
   const double g1 = geo.gamma - 1.0;
@@ -59,7 +62,7 @@ __global__ void __launch_bounds__(kBlock, DGB_LIMIT_MINB) k_limit(Geo geo, LimAr
     // the CFL epilogue's edge normals and inradius, requested with the neighbour means
     int ed3[3] = {0, 0, 0};
     double enx3[3] = {0.0, 0.0, 0.0}, eny3[3] = {0.0, 0.0, 0.0}, rin = 0.0;
-    if (a.want_lambda) {
+    if (want_lambda) {
 #pragma unroll
       for (int q = 0; q < 3; ++q) ed3[q] = __ldg(geo.eid + q * ld + e);
       rin = __ldg(geo.inradius + e);
@@ -73,7 +76,7 @@ __global__ void __launch_bounds__(kBlock, DGB_LIMIT_MINB) k_limit(Geo geo, LimAr
 #pragma unroll
       for (int m = 0; m < 4; ++m) nm[q][m] = nb[q] >= 0 ? __ldg(a.c + (m * NP) * ld + nb[q]) : 0.0;
 #if DGB_LIMIT_CFL_PREFETCH
-    if (a.want_lambda) {
+    if (want_lambda) {
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
         enx3[q] = __ldg(geo.enx + ed3[q]);
@@ -91,8 +94,8 @@ __global__ void __launch_bounds__(kBlock, DGB_LIMIT_MINB) k_limit(Geo geo, LimAr
       for (int q = 0; q < 3; ++q) {
         if (nb[q] < 0) continue;
         const double un = nm[q][m] * sqrt2;
-        umax = fmax(umax, un);
-        umin = fmin(umin, un);
+        umax = std_max(umax, un);
+        umin = std_min(umin, un);
       }
       const double tol = 1e-13 * (fabs(uc) + (umax - umin));
       // min over the edge points of clamp((umax-uc)/d) for d > tol and clamp((umin-uc)/d) for
@@ -100,17 +103,17 @@ __global__ void __launch_bounds__(kBlock, DGB_LIMIT_MINB) k_limit(Geo geo, LimAr
       // division is monotone in the divisor, so the minimum is the quotient by the extreme d:
       // two divisions per variable instead of one per point.  tol >= 0, so the extreme d
       // beyond +-tol is the extreme of all d when that clears the threshold (and NaN d are
-      // skipped by fmax/fmin as by the comparisons): bit-identical.
+      // skipped by the selects as by the comparisons): bit-identical.
       double dpos = 0.0, dneg = 0.0;
 #pragma unroll
       for (int k = e_begin; k < e_begin + n_edge; ++k) {
         const double d = c1[m] * L.phi1[k] + c2[m] * L.phi2[k];
-        dpos = fmax(dpos, d);
-        dneg = fmin(dneg, d);
+        dpos = d > dpos ? d : dpos;  // a NaN d is skipped, as by the reference's comparisons
+        dneg = d < dneg ? d : dneg;
       }
       double alpha = 1.0;
-      if (dpos > tol) alpha = fmin(alpha, fmin(fmax((umax - uc) / dpos, 0.0), 1.0));
-      if (dneg < -tol) alpha = fmin(alpha, fmin(fmax((umin - uc) / dneg, 0.0), 1.0));
+      if (dpos > tol) alpha = std_min(alpha, std_clamp01((umax - uc) / dpos));
+      if (dneg < -tol) alpha = std_min(alpha, std_clamp01((umin - uc) / dneg));
       c1[m] *= alpha;
       c2[m] *= alpha;
     }
@@ -172,15 +175,15 @@ __global__ void __launch_bounds__(kBlock, DGB_LIMIT_MINB) k_limit(Geo geo, LimAr
       const double v[4][NP] = {{c0[0], c1[0], c2[0]}, {c0[1], c1[1], c2[1]}, {c0[2], c1[2], c2[2]}, {c0[3], c1[3], c2[3]}};
       push_element<NP, 4>(geo, a.peers, a.out_buf, e, 0, v);
     }
-    if (a.want_resid) {
+    if (want_resid) {
 #pragma unroll
       for (int m = 0; m < 4; ++m) {
-        res_max = fmax(res_max, fabs(__ldg(a.u + (m * NP + 0) * ld + e) - c0[m]));
-        res_max = fmax(res_max, fabs(__ldg(a.u + (m * NP + 1) * ld + e) - c1[m]));
-        res_max = fmax(res_max, fabs(__ldg(a.u + (m * NP + 2) * ld + e) - c2[m]));
+        res_max = std_max(res_max, fabs(__ldg(a.u + (m * NP + 0) * ld + e) - c0[m]));
+        res_max = std_max(res_max, fabs(__ldg(a.u + (m * NP + 1) * ld + e) - c1[m]));
+        res_max = std_max(res_max, fabs(__ldg(a.u + (m * NP + 2) * ld + e) - c2[m]));
       }
     }
-    if (a.want_lambda) {  // CFL bound of the limited state (solver.cpp:439-457)
+    if (want_lambda) {  // CFL bound of the limited state (solver.cpp:439-457)
       double lam = 0.0;
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
@@ -206,8 +209,8 @@ __global__ void __launch_bounds__(kBlock, DGB_LIMIT_MINB) k_limit(Geo geo, LimAr
     }
   }
   const int par = a.step & 1;
-  if (a.want_lambda) block_reduce_atomic<true>(lam_min, &sc->dtmin[par ^ 1]);
-  if (a.want_resid) block_reduce_atomic<false>(res_max, &sc->resid[par]);
+  if (want_lambda) block_reduce_atomic<true>(lam_min, &sc->dtmin[par ^ 1]);
+  if (want_resid) block_reduce_atomic<false>(res_max, &sc->resid[par]);
   if (a.push) __threadfence_system();
 }
 
@@ -224,17 +227,24 @@ constexpr int kLimNE = 6, kLimNPT = 12;  // p = 1 tables: 2 points per edge, 3 i
 
 int limit_resident_blocks() {
   static int occ = 0;
-  if (!occ) occ = occupancy(k_limit<kLimNE, kLimNPT>);
+  if (!occ) occ = occupancy(k_limit<kLimNE, kLimNPT, 3>);
   return occ;
 }
 
 cudaError_t launch_limit(int grid, const Geo& g, const LimArgs& a, cudaStream_t s) {
   if (a.e1 <= a.e0) return cudaSuccess;
   if (grid <= 0) grid = grid_for(a.e1 - a.e0, limit_resident_blocks());
-  if (g_lim_pts[0] == kLimNE && g_lim_pts[1] == kLimNPT)
-    k_limit<kLimNE, kLimNPT><<<grid, kBlock, 0, s>>>(g, a);
-  else
-    k_limit<0, 0><<<grid, kBlock, 0, s>>>(g, a);
+  const int epi = (a.want_lambda ? 1 : 0) | (a.want_resid ? 2 : 0);
+  if (g_lim_pts[0] == kLimNE && g_lim_pts[1] == kLimNPT) {
+    switch (epi) {
+      case 0: k_limit<kLimNE, kLimNPT, 0><<<grid, kBlock, 0, s>>>(g, a); break;
+      case 1: k_limit<kLimNE, kLimNPT, 1><<<grid, kBlock, 0, s>>>(g, a); break;
+      case 2: k_limit<kLimNE, kLimNPT, 2><<<grid, kBlock, 0, s>>>(g, a); break;
+      default: k_limit<kLimNE, kLimNPT, 3><<<grid, kBlock, 0, s>>>(g, a); break;
+    }
+  } else {
+    k_limit<0, 0, 3><<<grid, kBlock, 0, s>>>(g, a);
+  }
   return cudaGetLastError();
 }
 
