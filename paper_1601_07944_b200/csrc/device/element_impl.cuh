@@ -654,9 +654,9 @@ __device__ __forceinline__ void element_body(const Tab<P>& T, const Geo& geo, co
           record_error(sc, err_key(a.seq_next, kPassDt, __ldg(geo.ref_id + e), g + 1));
         }
         if (g == 3) lam = 0.0;
-        lam = fmax(lam, __shfl_xor_sync(kFull, lam, 1));
-        lam = fmax(lam, __shfl_xor_sync(kFull, lam, 2));
-        if (valid && g == 0) lam_min = fmin(lam_min, 2.0 * __ldg(geo.inradius + e) / ((2.0 * P + 1.0) * lam));
+        lam = std_max(lam, __shfl_xor_sync(kFull, lam, 1));
+        lam = std_max(lam, __shfl_xor_sync(kFull, lam, 2));
+        if (valid && g == 0) lam_min = std_min(lam_min, 2.0 * __ldg(geo.inradius + e) / ((2.0 * P + 1.0) * lam));
       }
     }
   }
@@ -912,12 +912,12 @@ __device__ __forceinline__ void element_body_g1(const Tab<P>& T, const Geo& geo,
           const Prim w = primitives(U, g1);
           if (admissible(U, w)) {
             const int ed = __ldg(geo.eid + q * ld + e);
-            lam = fmax(lam, fabs(w.vx * __ldg(geo.enx + ed) + w.vy * __ldg(geo.eny + ed)) + sqrt(gamma * w.p * w.inv));
+            lam = std_max(lam, fabs(w.vx * __ldg(geo.enx + ed) + w.vy * __ldg(geo.eny + ed)) + sqrt(gamma * w.p * w.inv));
           } else {
             record_error(sc, err_key(a.seq_next, kPassDt, __ldg(geo.ref_id + e), q + 1));
           }
         }
-        lam_min = fmin(lam_min, 2.0 * __ldg(geo.inradius + e) / ((2.0 * P + 1.0) * lam));
+        lam_min = std_min(lam_min, 2.0 * __ldg(geo.inradius + e) / ((2.0 * P + 1.0) * lam));
       }
     }
   }
@@ -957,9 +957,9 @@ __device__ __forceinline__ void dt_body(const Tab<P>& T, const Geo& geo, const d
         continue;
       }
       const int ed = __ldg(geo.eid + q * ld + e);
-      lam = fmax(lam, fabs(w.vx * __ldg(geo.enx + ed) + w.vy * __ldg(geo.eny + ed)) + sqrt(gamma * w.p * w.inv));
+      lam = std_max(lam, fabs(w.vx * __ldg(geo.enx + ed) + w.vy * __ldg(geo.eny + ed)) + sqrt(gamma * w.p * w.inv));
     }
-    lam_min = fmin(lam_min, 2.0 * __ldg(geo.inradius + e) / ((2.0 * P + 1.0) * lam));
+    lam_min = std_min(lam_min, 2.0 * __ldg(geo.inradius + e) / ((2.0 * P + 1.0) * lam));
   }
   block_reduce_atomic<true>(lam_min, &sc->dtmin[slot]);
 }

@@ -720,9 +720,9 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
           record_error(sc, err_key(a.seq_next, kPassDt, __ldg(geo.ref_id + e), t + 1));
         }
         if (t == 3) lam = 0.0;
-        lam = fmax(lam, __shfl_xor_sync(0xffffffffu, lam, 1));
-        lam = fmax(lam, __shfl_xor_sync(0xffffffffu, lam, 2));
-        if (valid && t == 0) lam_min = fmin(lam_min, 2.0 * __ldg(geo.inradius + e) / ((2.0 * P + 1.0) * lam));
+        lam = std_max(lam, __shfl_xor_sync(0xffffffffu, lam, 1));
+        lam = std_max(lam, __shfl_xor_sync(0xffffffffu, lam, 2));
+        if (valid && t == 0) lam_min = std_min(lam_min, 2.0 * __ldg(geo.inradius + e) / ((2.0 * P + 1.0) * lam));
       }
     }
     if constexpr (kCSmem) {  // the own buffer is free only now

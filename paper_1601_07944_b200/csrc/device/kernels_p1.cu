@@ -196,15 +196,15 @@ __global__ void __launch_bounds__(kBlock, DGB_LIMIT_MINB) k_limit(Geo geo, LimAr
           continue;
         }
 #if DGB_LIMIT_CFL_PREFETCH
-        lam = fmax(lam, fabs(w.vx * enx3[q] + w.vy * eny3[q]) + sqrt_nr(geo.gamma * w.p * w.inv));
+        lam = std_max(lam, fabs(w.vx * enx3[q] + w.vy * eny3[q]) + sqrt_nr(geo.gamma * w.p * w.inv));
       }
-      lam_min = fmin(lam_min, 2.0 * rin / (3.0 * lam));
+      lam_min = std_min(lam_min, 2.0 * rin / (3.0 * lam));
 #else
         const int ed = __ldg(geo.eid + q * ld + e);
-        lam = fmax(lam, fabs(w.vx * __ldg(geo.enx + ed) + w.vy * __ldg(geo.eny + ed)) +
+        lam = std_max(lam, fabs(w.vx * __ldg(geo.enx + ed) + w.vy * __ldg(geo.eny + ed)) +
                             sqrt_nr(geo.gamma * w.p * w.inv));
       }
-      lam_min = fmin(lam_min, 2.0 * __ldg(geo.inradius + e) / (3.0 * lam));
+      lam_min = std_min(lam_min, 2.0 * __ldg(geo.inradius + e) / (3.0 * lam));
 #endif
     }
   }
