@@ -119,6 +119,16 @@ enum dgb_slot {
 };
 int dgb_upload(dgb_ctx* ctx, int slot, const double* host_coeffs);
 int dgb_download(dgb_ctx* ctx, int slot, double* host_coeffs);
+/* Asynchronous forms of dgb_upload / dgb_download (no reference counterpart: the
+ * reference's arrays live in host memory).  They return once the copy is enqueued;
+ * `host_coeffs` should be pinned (cudaHostAlloc) and must stay untouched until
+ * dgb_sync.  Each direction has its own copy stream and staging buffer, so a result's
+ * device->host copy overlaps the next input's host->device copy; later calls on the
+ * context are ordered after them on the device. */
+int dgb_upload_async(dgb_ctx* ctx, int slot, const double* host_coeffs);
+int dgb_download_async(dgb_ctx* ctx, int slot, double* host_coeffs);
+/* Wait for every copy and kernel the context has enqueued. */
+int dgb_sync(dgb_ctx* ctx);
 /* Device-resident copies (no host round trip): dst <- src. */
 int dgb_copy_slot(dgb_ctx* ctx, int dst, int src);
 

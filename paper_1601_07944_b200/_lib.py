@@ -101,6 +101,9 @@ _sig("dgb_set_dirichlet", C.c_int, _vp, c_double_p)
 _sig("dgb_set_flux", C.c_int, _vp, C.c_int)
 _sig("dgb_upload", C.c_int, _vp, C.c_int, c_double_p)
 _sig("dgb_download", C.c_int, _vp, C.c_int, c_double_p)
+_sig("dgb_upload_async", C.c_int, _vp, C.c_int, c_double_p)
+_sig("dgb_download_async", C.c_int, _vp, C.c_int, c_double_p)
+_sig("dgb_sync", C.c_int, _vp)
 _sig("dgb_copy_slot", C.c_int, _vp, C.c_int, C.c_int)
 _sig("dgb_eval_volume_pass", C.c_int, _vp, C.c_int)
 _sig("dgb_eval_surface_pass", C.c_int, _vp, C.c_int, C.c_double)

@@ -308,6 +308,11 @@ struct dgb_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  // asynchronous host copies (dgb_upload_async / dgb_download_async): one copy stream per
+  // direction and a staging buffer each, so a result's device->host copy overlaps the
+  // next input's host->device copy (PCIe is full duplex)
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  cudaEvent_t ev_h2d = nullptr, ev_in_free = nullptr, ev_perm_out = nullptr, ev_out_free = nullptr;
   int p = 1, np = 3, nq = 3, K = 2;
   int N = 0, ld = 0, n_edges = 0, n_bnd = 0;
   double gamma = 1.4;
@@ -347,7 +352,7 @@ struct dgb_ctx {
   Geo geo{};
 
   // coefficient buffers (device order [4][np][ld])
-  DevBuf<double> state[2], input, volume, deriv, stage[2], kacc, slots, staging, hist;
+  DevBuf<double> state[2], input, volume, deriv, stage[2], kacc, slots, staging, hist, staging_in, staging_out;
   int cur = 0;
   Scalars* d_sc = nullptr;
   Scalars* h_sc = nullptr;  // pinned mirror
@@ -1318,6 +1323,13 @@ int dgb_destroy(dgb_ctx* c) {
     cudaEventDestroy(pd.b);
   }
   for (auto e : c->event_pool) cudaEventDestroy(e);
+  for (cudaStream_t cs : {c->s_h2d, c->s_d2h})
+    if (cs) {
+      cudaStreamSynchronize(cs);
+      cudaStreamDestroy(cs);
+    }
+  for (cudaEvent_t ev : {c->ev_h2d, c->ev_in_free, c->ev_perm_out, c->ev_out_free})
+    if (ev) cudaEventDestroy(ev);
   for (auto it = g_bank_owner.begin(); it != g_bank_owner.end();)
     it = it->second == c ? g_bank_owner.erase(it) : std::next(it);
   if (c->d_sc) cudaFree(c->d_sc);
@@ -1387,6 +1399,76 @@ int dgb_download(dgb_ctx* c, int slot, double* host) {
   return guarded([&] {
     set_device(c);
     download_dev(c, slot_ptr(c, slot), 4 * c->np, host);
+    return DGB_OK;
+  });
+}
+
+namespace {
+void ensure_copy_streams(dgb_ctx* c) {
+  if (c->s_h2d) return;
+  CU(cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking));
+  CU(cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking));
+  for (cudaEvent_t* ev : {&c->ev_h2d, &c->ev_in_free, &c->ev_perm_out, &c->ev_out_free})
+    CU(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
+}
+}  // namespace
+
+int dgb_upload_async(dgb_ctx* c, int slot, const double* host) {
+  return guarded([&] {
+    set_device(c);
+    ensure_copy_streams(c);
+    double* dev = slot_ptr(c, slot);
+    const int rows = 4 * c->np, nl = c->N + c->n_halo;
+    const size_t n = static_cast<size_t>(rows) * nl;
+    if (c->staging_in.n < n) {
+      sync(c);  // a resize must not free a buffer an enqueued permute still reads
+      c->staging_in.alloc(n);
+    }
+    // the previous upload's permute has consumed staging_in
+    CU(cudaStreamWaitEvent(c->s_h2d, c->ev_in_free, 0));
+    CU(cudaMemcpyAsync(c->staging_in.p, host, sizeof(double) * n, cudaMemcpyHostToDevice, c->s_h2d));
+    CU(cudaEventRecord(c->ev_h2d, c->s_h2d));
+    CU(cudaStreamWaitEvent(c->stream, c->ev_h2d, 0));
+    k_permute_in<<<small_grid(static_cast<long long>(rows) * c->ld), 256, 0, c->stream>>>(
+        dev, c->staging_in.p, c->d_cmp.p, nl, nl, c->ld, rows);
+    CU(cudaGetLastError());
+    ++c->launches;
+    CU(cudaEventRecord(c->ev_in_free, c->stream));
+    return DGB_OK;
+  });
+}
+
+int dgb_download_async(dgb_ctx* c, int slot, double* host) {
+  return guarded([&] {
+    set_device(c);
+    ensure_copy_streams(c);
+    const double* dev = slot_ptr(c, slot);
+    const int rows = 4 * c->np;
+    const size_t n = static_cast<size_t>(rows) * c->N;
+    if (c->staging_out.n < n) {
+      CU(cudaStreamSynchronize(c->s_d2h));
+      c->staging_out.alloc(n);
+    }
+    // the previous download's device->host copy has drained staging_out
+    CU(cudaStreamWaitEvent(c->stream, c->ev_out_free, 0));
+    k_permute_out<<<small_grid(static_cast<long long>(rows) * c->ld), 256, 0, c->stream>>>(
+        c->staging_out.p, dev, c->d_cmp.p, c->N, c->N, c->ld, rows);
+    CU(cudaGetLastError());
+    ++c->launches;
+    CU(cudaEventRecord(c->ev_perm_out, c->stream));
+    CU(cudaStreamWaitEvent(c->s_d2h, c->ev_perm_out, 0));
+    CU(cudaMemcpyAsync(host, c->staging_out.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->s_d2h));
+    CU(cudaEventRecord(c->ev_out_free, c->s_d2h));
+    return DGB_OK;
+  });
+}
+
+int dgb_sync(dgb_ctx* c) {
+  return guarded([&] {
+    set_device(c);
+    if (c->s_h2d) CU(cudaStreamSynchronize(c->s_h2d));
+    if (c->s_d2h) CU(cudaStreamSynchronize(c->s_d2h));
+    sync(c);
     return DGB_OK;
   });
 }

@@ -475,3 +475,37 @@ def test_roe_with_limiter_and_moving_shock_matches_oracle():
     assert rel_per_eq(st.coeffs, cr) <= RUN_TOL
     assert abs(st.t - tr) <= 1e-12 * tr
     ctx.close()
+
+
+def test_async_copies_pipeline_bitwise_equal_to_synchronous():
+    """dgb_upload_async / dgb_download_async / dgb_sync (the bench's end-to-end path): a
+    pipelined sequence of (upload, one step, download) requests from pinned buffers, each
+    download overlapping the next upload, returns exactly what the synchronous calls return."""
+    import ctypes as C
+
+    import torch
+
+    mesh, tb, bc, c, ctx, orc = build(CASES[2], 2, dg2d.SolverOptions(rk_order=2))
+    h = ctx.handle
+    res = C.c_double()
+    inputs = [np.ascontiguousarray(c * (1.0 + 1e-3 * k)) for k in range(3)]
+    want = []
+    for x in inputs:  # synchronous reference: upload, one step, download
+        ctx.upload(L.SLOT_STATE, x)
+        dg2d._check(L.lib.dgb_run_fixed_steps(h, 2, 0.3, 0, 1, C.byref(res), None))
+        want.append(ctx.download(L.SLOT_STATE))
+    ctx.close()
+    ctx = build(CASES[2], 2, dg2d.SolverOptions(rk_order=2))[4]  # same start time as above
+    h = ctx.handle
+    pins = [torch.empty(x.size, dtype=torch.float64, pin_memory=True) for x in inputs]
+    outs = [torch.empty(x.size, dtype=torch.float64, pin_memory=True) for x in inputs]
+    for pin, x in zip(pins, inputs):
+        pin.numpy()[...] = x.ravel()
+    for pin, out in zip(pins, outs):
+        dg2d._check(L.lib.dgb_upload_async(h, L.SLOT_STATE, pin.numpy().ctypes.data_as(L.c_double_p)))
+        dg2d._check(L.lib.dgb_run_fixed_steps(h, 2, 0.3, 0, 1, C.byref(res), None))
+        dg2d._check(L.lib.dgb_download_async(h, L.SLOT_STATE, out.numpy().ctypes.data_as(L.c_double_p)))
+    dg2d._check(L.lib.dgb_sync(h))
+    for out, w in zip(outs, want):
+        assert np.array_equal(out.numpy().reshape(w.shape), w)
+    ctx.close()
