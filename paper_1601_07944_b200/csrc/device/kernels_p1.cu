@@ -19,7 +19,7 @@ namespace {
 // NE / NPT: edge points and all check points as compile-time constants (0: read from c_lim),
 // so the point loops unroll onto immediate constant-bank operands.
 #ifndef DGB_LIMIT_MINB
-#define DGB_LIMIT_MINB 8  // 64 registers: 0.149 ms per stage on the 2M DMR vs 0.206 at 116 (measured)
+#define DGB_LIMIT_MINB 6  // 80 registers: 0.120 ms per stage on the 2M DMR vs 0.128 at 64, 0.126 at 72 (measured)
 #endif
 #ifndef DGB_LIMIT_CFL_PREFETCH
 #define DGB_LIMIT_CFL_PREFETCH 1
