@@ -33,7 +33,7 @@
 namespace dgbk {
 
 #ifndef DGB_MMA_VOL_PIPE
-#define DGB_MMA_VOL_PIPE 1  // interpolate the next point tile while this tile's fluxes run
+#define DGB_MMA_VOL_PIPE(P) 1  // interpolate the next point tile while this tile's fluxes run
 #endif
 #ifndef DGB_MMA_SIDE_UNROLL
 #define DGB_MMA_SIDE_UNROLL 1  // per-side surface loop (p = 5): runtime loop, 1.84 vs 1.91 ms unrolled
@@ -45,8 +45,9 @@ constexpr int kMmaSideUnroll = DGB_MMA_SIDE_UNROLL;
 constexpr int kMmaPackUnroll = DGB_MMA_PACK_UNROLL;
 #ifndef DGB_MMA_C_SMEM_MINP
 // degrees >= this read the stage input for the RK epilogue from the own fragment buffer
-// (measured per stage: p=5 1.739 vs 1.846 ms, p=4 1.089 vs 1.108, p=3 0.870 vs 0.866)
-#define DGB_MMA_C_SMEM_MINP 4
+// (measured per stage: p=5 1.739 vs 1.846 ms, p=4 1.089 vs 1.108, p=3 0.870 vs 0.866; after
+// the kernel-instance split p=3 0.730 vs 0.771)
+#define DGB_MMA_C_SMEM_MINP 3
 #endif
 #ifndef DGB_MMA_U_AHEAD
 #define DGB_MMA_U_AHEAD 1
@@ -255,12 +256,12 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
         }
       };
       constexpr int NTD = D::NTD;
-      if (DGB_MMA_VOL_PIPE) interp(U[0], 0);
+      if (DGB_MMA_VOL_PIPE(P)) interp(U[0], 0);
 #pragma unroll
       for (int nt = 0; nt < NTD; ++nt) {
         // software pipeline: the next tile of points is interpolated while this
         // tile's fluxes are evaluated
-        if (DGB_MMA_VOL_PIPE) {
+        if (DGB_MMA_VOL_PIPE(P)) {
           if (nt + 1 < NTD) interp(U[(nt + 1) & 1], nt + 1);
         } else {
           interp(U[nt & 1], nt);
