@@ -126,6 +126,13 @@ int dgb_download(dgb_ctx* ctx, int slot, double* host_coeffs);
  * device->host copy overlaps the next input's host->device copy; later calls on the
  * context are ordered after them on the device. */
 int dgb_upload_async(dgb_ctx* ctx, int slot, const double* host_coeffs);
+/* dgb_upload_async in two halves, so the next request's host->device copy can run while
+ * the current request computes: dgb_stage_input_async enqueues the copy into the
+ * context's input staging buffer (after the previous staged input was committed);
+ * dgb_commit_input(slot) orders, on the compute stream, the permutation of the staged
+ * input into `slot` after everything enqueued so far.  DGB_ERR_ARG if nothing is staged. */
+int dgb_stage_input_async(dgb_ctx* ctx, const double* host_coeffs);
+int dgb_commit_input(dgb_ctx* ctx, int slot);
 int dgb_download_async(dgb_ctx* ctx, int slot, double* host_coeffs);
 /* Wait for every copy and kernel the context has enqueued. */
 int dgb_sync(dgb_ctx* ctx);

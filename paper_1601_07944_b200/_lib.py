@@ -104,6 +104,8 @@ _sig("dgb_download", C.c_int, _vp, C.c_int, c_double_p)
 _sig("dgb_upload_async", C.c_int, _vp, C.c_int, c_double_p)
 _sig("dgb_download_async", C.c_int, _vp, C.c_int, c_double_p)
 _sig("dgb_sync", C.c_int, _vp)
+_sig("dgb_stage_input_async", C.c_int, _vp, c_double_p)
+_sig("dgb_commit_input", C.c_int, _vp, C.c_int)
 _sig("dgb_copy_slot", C.c_int, _vp, C.c_int, C.c_int)
 _sig("dgb_eval_volume_pass", C.c_int, _vp, C.c_int)
 _sig("dgb_eval_surface_pass", C.c_int, _vp, C.c_int, C.c_double)

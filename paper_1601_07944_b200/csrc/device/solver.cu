@@ -313,6 +313,7 @@ struct dgb_ctx {
   // next input's host->device copy (PCIe is full duplex)
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
   cudaEvent_t ev_h2d = nullptr, ev_in_free = nullptr, ev_perm_out = nullptr, ev_out_free = nullptr;
+  bool staged = false;  // an input is (being) copied into staging_in and not yet committed
   int p = 1, np = 3, nq = 3, K = 2;
   int N = 0, ld = 0, n_edges = 0, n_bnd = 0;
   double gamma = 1.4;
@@ -1413,29 +1414,46 @@ void ensure_copy_streams(dgb_ctx* c) {
 }
 }  // namespace
 
-int dgb_upload_async(dgb_ctx* c, int slot, const double* host) {
+int dgb_stage_input_async(dgb_ctx* c, const double* host) {
   return guarded([&] {
     set_device(c);
     ensure_copy_streams(c);
-    double* dev = slot_ptr(c, slot);
-    const int rows = 4 * c->np, nl = c->N + c->n_halo;
-    const size_t n = static_cast<size_t>(rows) * nl;
+    const size_t n = static_cast<size_t>(4 * c->np) * (c->N + c->n_halo);
     if (c->staging_in.n < n) {
       sync(c);  // a resize must not free a buffer an enqueued permute still reads
+      CU(cudaStreamSynchronize(c->s_h2d));
       c->staging_in.alloc(n);
     }
-    // the previous upload's permute has consumed staging_in
+    if (c->staged) throw Fail{DGB_ERR_ARG, "dgb_stage_input_async: an input is already staged (commit it first)"};
+    // the previous commit's permute has consumed staging_in
     CU(cudaStreamWaitEvent(c->s_h2d, c->ev_in_free, 0));
     CU(cudaMemcpyAsync(c->staging_in.p, host, sizeof(double) * n, cudaMemcpyHostToDevice, c->s_h2d));
     CU(cudaEventRecord(c->ev_h2d, c->s_h2d));
+    c->staged = true;
+    return DGB_OK;
+  });
+}
+
+int dgb_commit_input(dgb_ctx* c, int slot) {
+  return guarded([&] {
+    set_device(c);
+    if (!c->staged) throw Fail{DGB_ERR_ARG, "dgb_commit_input: no staged input (call dgb_stage_input_async)"};
+    double* dev = slot_ptr(c, slot);
+    const int rows = 4 * c->np, nl = c->N + c->n_halo;
     CU(cudaStreamWaitEvent(c->stream, c->ev_h2d, 0));
     k_permute_in<<<small_grid(static_cast<long long>(rows) * c->ld), 256, 0, c->stream>>>(
         dev, c->staging_in.p, c->d_cmp.p, nl, nl, c->ld, rows);
     CU(cudaGetLastError());
     ++c->launches;
     CU(cudaEventRecord(c->ev_in_free, c->stream));
+    c->staged = false;
     return DGB_OK;
   });
+}
+
+int dgb_upload_async(dgb_ctx* c, int slot, const double* host) {
+  const int rc = dgb_stage_input_async(c, host);
+  return rc != DGB_OK ? rc : dgb_commit_input(c, slot);
 }
 
 int dgb_download_async(dgb_ctx* c, int slot, double* host) {

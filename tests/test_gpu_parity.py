@@ -478,9 +478,10 @@ def test_roe_with_limiter_and_moving_shock_matches_oracle():
 
 
 def test_async_copies_pipeline_bitwise_equal_to_synchronous():
-    """dgb_upload_async / dgb_download_async / dgb_sync (the bench's end-to-end path): a
-    pipelined sequence of (upload, one step, download) requests from pinned buffers, each
-    download overlapping the next upload, returns exactly what the synchronous calls return."""
+    """dgb_upload_async / dgb_stage_input_async / dgb_commit_input / dgb_download_async /
+    dgb_sync (the bench's end-to-end path): a pipelined sequence of (upload, one step,
+    download) requests from pinned buffers — the next input's copy in flight while the current
+    request computes and downloads — returns exactly what the synchronous calls return."""
     import ctypes as C
 
     import torch
@@ -501,10 +502,18 @@ def test_async_copies_pipeline_bitwise_equal_to_synchronous():
     outs = [torch.empty(x.size, dtype=torch.float64, pin_memory=True) for x in inputs]
     for pin, x in zip(pins, inputs):
         pin.numpy()[...] = x.ravel()
-    for pin, out in zip(pins, outs):
-        dg2d._check(L.lib.dgb_upload_async(h, L.SLOT_STATE, pin.numpy().ctypes.data_as(L.c_double_p)))
+    ptr = lambda t: t.numpy().ctypes.data_as(L.c_double_p)  # noqa: E731
+    # request 0 in one call; request k+1 staged (host->device copy in flight) while request k
+    # computes and committed after request k's download was enqueued
+    dg2d._check(L.lib.dgb_upload_async(h, L.SLOT_STATE, ptr(pins[0])))
+    assert L.lib.dgb_commit_input(h, L.SLOT_STATE) == L.ERR_ARG  # nothing staged
+    for k, out in enumerate(outs):
+        if k + 1 < len(pins):
+            dg2d._check(L.lib.dgb_stage_input_async(h, ptr(pins[k + 1])))
         dg2d._check(L.lib.dgb_run_fixed_steps(h, 2, 0.3, 0, 1, C.byref(res), None))
-        dg2d._check(L.lib.dgb_download_async(h, L.SLOT_STATE, out.numpy().ctypes.data_as(L.c_double_p)))
+        dg2d._check(L.lib.dgb_download_async(h, L.SLOT_STATE, ptr(out)))
+        if k + 1 < len(pins):
+            dg2d._check(L.lib.dgb_commit_input(h, L.SLOT_STATE))
     dg2d._check(L.lib.dgb_sync(h))
     for out, w in zip(outs, want):
         assert np.array_equal(out.numpy().reshape(w.shape), w)
