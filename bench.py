@@ -490,7 +490,7 @@ def main():
     ap.add_argument("--orders", default="1,2,3,4,5")
     ap.add_argument("--scheme", default="ssp3", choices=list(SCHEMES))
     ap.add_argument("--cfl", type=float, default=0.3)
-    ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--e2e-steps", type=int, default=16)
     ap.add_argument("--cpu-box", dest="cpu_n", type=int, default=708, help="box size of the CPU sample")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--dmr-nx", type=int, default=2000, help="DMR channel cells in x (C4 leg; 0 = skip)")
