@@ -18,6 +18,21 @@ for p in (1, 2, 3, 4, 5):
         dg2d.run_fixed_steps(ctx, st, 2)
         dg2d.compute_rhs(ctx, c0, 0.0); dg2d.eval_volume_pass(ctx, c0); dg2d.eval_surface_pass(ctx, c0, 0.0)
         ctx.close()
+    # RK4 accumulator instances and the asynchronous copy path
+    ctx = dg2d.SolverContext(mesh, tb, options=dg2d.SolverOptions(rk_order=4))
+    dg2d.run_fixed_steps(ctx, dg2d.SolverState(c0.copy()), 2)
+    import ctypes as C, torch
+    pin = torch.empty(c0.size, dtype=torch.float64, pin_memory=True); pin.numpy()[...] = c0.ravel()
+    out = torch.empty(c0.size, dtype=torch.float64, pin_memory=True)
+    ptr = lambda t: t.numpy().ctypes.data_as(L.c_double_p)
+    res = C.c_double()
+    dg2d._check(L.lib.dgb_upload_async(ctx.handle, L.SLOT_STATE, ptr(pin)))
+    dg2d._check(L.lib.dgb_stage_input_async(ctx.handle, ptr(pin)))
+    dg2d._check(L.lib.dgb_run_fixed_steps(ctx.handle, 4, 0.3, 0, 1, C.byref(res), None))
+    dg2d._check(L.lib.dgb_download_async(ctx.handle, L.SLOT_STATE, ptr(out)))
+    dg2d._check(L.lib.dgb_commit_input(ctx.handle, L.SLOT_STATE))
+    dg2d._check(L.lib.dgb_sync(ctx.handle))
+    ctx.close()
     if not os.environ.get("SAN_SKIP_PART"):  # initcheck serialises kernels: the in-process
         # partitions' spin-wait kernels would wait on peers that cannot run concurrently
         parts = [D.PartContext(mesh, tb, r, 2, options=dg2d.SolverOptions(scheme=103)) for r in range(2)]
