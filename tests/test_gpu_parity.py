@@ -515,6 +515,11 @@ def test_async_copies_pipeline_bitwise_equal_to_synchronous():
         if k + 1 < len(pins):
             dg2d._check(L.lib.dgb_commit_input(h, L.SLOT_STATE))
     dg2d._check(L.lib.dgb_sync(h))
+    # staging twice without a commit is refused (the staging buffer holds one input)
+    dg2d._check(L.lib.dgb_stage_input_async(h, ptr(pins[0])))
+    assert L.lib.dgb_stage_input_async(h, ptr(pins[1])) == L.ERR_ARG
+    dg2d._check(L.lib.dgb_commit_input(h, L.SLOT_INPUT))
+    dg2d._check(L.lib.dgb_sync(h))
     for out, w in zip(outs, want):
         assert np.array_equal(out.numpy().reshape(w.shape), w)
     ctx.close()
