@@ -421,14 +421,16 @@ class RefArm:
         self.runs = []
         if self.kind == "reference":
             rm = bind.RefMesh.from_mesh(mesh)
-            self.cores = bind.ref_lib().ref_num_threads()
+            # every host thread, set through the reference's own SolverOptions::workers
+            # (solver.cpp:26-33): torchrun exports OMP_NUM_THREADS=1 to its ranks
+            self.cores = len(os.sched_getaffinity(0))
         else:
             rm, self.cores = None, 1
         for p in orders:
             tb = dg2d.build_tables(p)
             c0 = dg2d.project_initial(lambda xy: iv(xy), mesh, tb)
             if self.kind == "reference":
-                solver = bind.RefSolver(rm, bind.RefTables(p), rk_order=2, cfl=0.3)
+                solver = bind.RefSolver(rm, bind.RefTables(p), rk_order=2, cfl=0.3, workers=self.cores)
             else:
                 solver = bind.Oracle(mesh, tb)
             self.runs.append((p, solver, c0))
@@ -499,10 +501,13 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    rank, world, local, pg = dist_setup(args.gpus, args.same_device)
     if args.impl == "reference":
-        line = run_reference(args, rank, world)
+        # the reference arm is CPU-only: rank 0 runs it, the other ranks exit at once, and no
+        # rank touches CUDA or a process group
+        rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+        line, pg = run_reference(args, rank, world), None
     else:
+        rank, world, local, pg = dist_setup(args.gpus, args.same_device)
         line = run_b200(args, rank, world, local, pg)
     if rank == 0 and line is not None:
         print(json.dumps(line), flush=True)
