@@ -127,7 +127,7 @@ class Mesh:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and lib is not None:  # lib is None during interpreter shutdown
             lib.dgb_mesh_free(h)
             self._h = None
 
@@ -290,7 +290,7 @@ class BasisTables:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and lib is not None:  # lib is None during interpreter shutdown
             lib.dgb_tables_free(h)
             self._h = None
 
