@@ -318,7 +318,7 @@ def run_b200(args, rank, world, local, pg):
                        "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                        "note": "per step: pinned host state -> dgb_stage_input_async + dgb_commit_input -> one RK step -> dgb_download_async (one copy stream per direction: step k+1's upload overlaps step k's compute and download); wall clock incl. dgb_sync"}
     if rank == 0 and world == 1 and not args.no_cpu:
-        line["cpu_baseline"] = cpu_baseline(mesh, orders, args)
+        line["cpu_baseline"] = cpu_baseline(orders, args)
     if world == 1 and args.dmr_nx > 0:
         line["dmr"] = dmr_leg(args, local)
     return line
@@ -374,127 +374,71 @@ def dmr_leg(args, local):
 
 
 # ----------------------------------------------------------------------------- CPU reference
-def cpu_sample(mesh, orders, sample_n, steps=2):
-    """Time the reference solver's run_fixed_steps (RK2, its own driver with its
-    workspace reused across the steps of a call, all host threads) for `steps`
-    steps per order on the same mesh; returns DOF-updates/s/stage."""
-    from oracle import bind
-    from paper_1601_07944_b200 import _lib as L
-    from paper_1601_07944_b200 import dg2d
-    if mesh is None or mesh.n_elements() != 2 * sample_n * sample_n:
-        mesh = dg2d.generate_mesh(L.MESH_PERIODIC_BOX, sample_n, sample_n, 10.0, 10.0)
-    N = mesh.n_elements()
-    iv = dg2d.IsentropicVortex()
-    kind = "reference" if bind.ref_available() else "port"
-    upd, secs = 0.0, 0.0
-    if kind == "reference":
-        rm = bind.RefMesh.from_mesh(mesh)
-        cores = bind.ref_lib().ref_num_threads()
-    else:
-        cores = 1
-    for p in orders:
-        tb = dg2d.build_tables(p)
-        c0 = dg2d.project_initial(lambda xy: iv(xy), mesh, tb)
-        if kind == "reference":
-            rt = bind.RefTables(p)
-            rs = bind.RefSolver(rm, rt, rk_order=2, cfl=0.3)
-            t0 = time.perf_counter()
-            rs.run_fixed_steps(c0, 0.0, steps)
-            dt = time.perf_counter() - t0
-        else:
-            orc = bind.Oracle(mesh, tb)
-            t0 = time.perf_counter()
-            orc.run_fixed_steps(c0, 0.0, steps, 2, 0.3)
-            dt = time.perf_counter() - t0
-        upd += 4 * np_(p) * N * 2 * steps
-        secs += dt
-    return {"value": upd / secs, "unit": "DOF-updates/s/stage", "cores": cores, "kind": kind,
-            "seconds": secs,
-            "sample": f"{steps} RK2 (midpoint) steps per order p={','.join(map(str, orders))} on the "
-                      f"periodic {int(round(math.sqrt(N / 2)))}^2 box ({N} triangles), "
-                      f"reference run_fixed_steps with OpenMP over {cores} threads"}
+REF_CONFIG_NOTE = ("same mesh (the periodic 708x708 box built by the reference's own build_connectivity with "
+                   "the hull edges joined, array-identical to ours: tests/test_host_setup.py), same initial data "
+                   "(the reference's project_initial of the same isentropic vortex), same orders; the reference "
+                   "has no SSP-RK3, so it runs its RK2 midpoint scheme: a stage is one compute_rhs + the stage "
+                   "combination in both, and the metric is per stage")
 
 
-def cpu_baseline(mesh, orders, args):
+def cpu_sample(orders, n, steps=2):
+    """The reference solver (oracle/_ref, -march=native, OpenMP over every host core, bound
+    close) on the benchmark's own workload: one run_fixed_steps call of `steps` RK2 steps
+    per order.  Returns the cpu_baseline object."""
+    from oracle import refarm
+    if not refarm.available():
+        raise RuntimeError("oracle/_ref not built")
+    r = refarm.throughput(n, orders, calls_per_order=1, steps_per_call=steps, warmup_calls=0)
+    secs = sum(r["best_s"].values())
+    return {"value": r["value"], "unit": "DOF-updates/s/stage", "cores": r["threads"], "kind": "reference",
+            "seconds": secs, "library": r["so"],
+            "sample": f"one run_fixed_steps call of {steps} RK2 (midpoint) steps per order "
+                      f"p={','.join(map(str, orders))} on the periodic {n}^2 box ({r['N']} triangles), the "
+                      f"reference's own build (-O3 -march=native -fno-math-errno, OpenMP over {r['threads']} "
+                      "threads, OMP_PROC_BIND=close), no warm-up"}
+
+
+def cpu_baseline(orders, args):
     try:
-        return cpu_sample(mesh if args.cpu_n == args.n else None, orders, args.cpu_n)
+        return cpu_sample(orders, args.cpu_n)
     except Exception as e:  # the CPU leg must never break the GPU number
         return {"value": None, "unit": "DOF-updates/s/stage", "cores": None, "kind": None,
                 "sample": f"failed: {e}"}
 
 
-class RefArm:
-    """The reference solver (oracle/_ref: its own sources, unmodified, OpenMP over all host
-    cores) set up ONCE on the bench workload: mesh, tables, projected state per order."""
-
-    def __init__(self, orders, n):
-        from oracle import bind
-        from paper_1601_07944_b200 import _lib as L
-        from paper_1601_07944_b200 import dg2d
-        self.kind = "reference" if bind.ref_available() else "port"
-        mesh = dg2d.generate_mesh(L.MESH_PERIODIC_BOX, n, n, 10.0, 10.0)
-        self.N = mesh.n_elements()
-        iv = dg2d.IsentropicVortex()
-        self.runs = []
-        if self.kind == "reference":
-            rm = bind.RefMesh.from_mesh(mesh)
-            # every host thread, set through the reference's own SolverOptions::workers
-            # (solver.cpp:26-33): torchrun exports OMP_NUM_THREADS=1 to its ranks
-            self.cores = len(os.sched_getaffinity(0))
-        else:
-            rm, self.cores = None, 1
-        for p in orders:
-            tb = dg2d.build_tables(p)
-            c0 = dg2d.project_initial(lambda xy: iv(xy), mesh, tb)
-            if self.kind == "reference":
-                solver = bind.RefSolver(rm, bind.RefTables(p), rk_order=2, cfl=0.3, workers=self.cores)
-            else:
-                solver = bind.Oracle(mesh, tb)
-            self.runs.append((p, solver, c0))
-        self.mesh_keep = mesh
-
-    def step(self, steps=1):
-        """`steps` RK2 steps per order through the reference's run_fixed_steps; returns
-        (seconds, DOF updates)."""
-        secs, upd = 0.0, 0.0
-        for p, solver, c0 in self.runs:
-            t0 = time.perf_counter()
-            if self.kind == "reference":
-                solver.run_fixed_steps(c0, 0.0, steps)
-            else:
-                solver.run_fixed_steps(c0, 0.0, steps, 2, 0.3)
-            secs += time.perf_counter() - t0
-            upd += 4 * np_(p) * self.N * 2 * steps
-        return secs, upd
-
-
 def run_reference(args, rank, world):
+    """The reference arm: the UNMODIFIED reference's CPU solver (oracle/refarm.py; this
+    process never loads the B200 library).  A bench step is one run_fixed_steps call of
+    --ref-steps RK2 steps (the reference's own driver, its RkWorkspace reused across the
+    steps of the call, solver.cpp:600-613) at one order, the orders taken round robin; after
+    one untimed warm-up call per order.  value = sum over orders of the DOF updates of one call
+    / sum of each order's best timed call (best of >= 3 when --steps >= 3 x orders)."""
     if rank != 0:
         return None
+    from oracle import refarm
     orders = [int(x) for x in args.orders.split(",")]
-    arm = RefArm(orders, args.cpu_n)
-    for _ in range(args.warmup):
-        arm.step()
-    t_tot, upd_tot = 0.0, 0.0
-    for _ in range(args.steps):
-        sec, upd = arm.step()
-        t_tot += sec
-        upd_tot += upd
-    value = upd_tot / t_tot
-    N = arm.N
-    sample = (f"one RK2 (midpoint) step per order p={args.orders} per bench step on the periodic "
-              f"{args.cpu_n}^2 box ({N} triangles), reference run_fixed_steps, OpenMP over {arm.cores} threads")
+    sched = [orders[k % len(orders)] for k in range(args.steps)]
+    warm = max(1, -(-args.warmup // len(orders)))
+    r = refarm.throughput(args.cpu_n, orders, calls_per_order=0, steps_per_call=args.ref_steps,
+                          warmup_calls=warm, schedule=sched)
+    value, N = r["value"], r["N"]
+    t_tot = sum(sum(v) for v in r["all_s"].values())
+    sample = (f"one run_fixed_steps call of {args.ref_steps} RK2 (midpoint) steps per bench step, orders "
+              f"p={args.orders} round robin, on the periodic {args.cpu_n}^2 box ({N} triangles); per order the best "
+              f"of its {min(len(v) for v in r['all_s'].values())}+ timed calls; the reference's own build "
+              f"({r['so']}: -O3 -march=native -fno-math-errno) with OpenMP over {r['threads']} threads, "
+              "OMP_PROC_BIND=close")
     return {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "DOF-updates/s/stage",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": t_tot / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic: periodic isentropic vortex initial data",
+        "ms_per_step": t_tot / max(len(sched), 1) * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic: periodic isentropic vortex initial data (projected)",
         "config": {"workload": f"isentropic vortex, periodic {args.cpu_n}x{args.cpu_n} box ({N} triangles), "
-                               f"p={args.orders} sweep; reference RK2 (SSP-RK3 is not in the reference; "
-                               "per-stage cost is the same RHS + stage combination)",
-                   "orders": orders},
-        "cpu_baseline": {"value": value, "unit": "DOF-updates/s/stage", "cores": arm.cores,
-                         "kind": arm.kind, "sample": sample},
+                               f"p={args.orders} sweep, reference RK2 midpoint, cfl 0.3",
+                   "orders": orders, "same_config": REF_CONFIG_NOTE},
+        "per_order": {str(p): v for p, v in r["per_order"].items()},
+        "cpu_baseline": {"value": value, "unit": "DOF-updates/s/stage", "cores": r["threads"],
+                         "kind": "reference", "sample": sample},
         "e2e": {"value": value, "unit": "DOF-updates/s/stage", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
@@ -511,6 +455,7 @@ def main():
     ap.add_argument("--cfl", type=float, default=0.3)
     ap.add_argument("--e2e-steps", type=int, default=16)
     ap.add_argument("--cpu-box", dest="cpu_n", type=int, default=708, help="box size of the CPU sample")
+    ap.add_argument("--ref-steps", type=int, default=5, help="RK2 steps per reference run_fixed_steps call")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--dmr-nx", type=int, default=2000, help="DMR channel cells in x (C4 leg; 0 = skip)")
     ap.add_argument("--same-device", action="store_true",

@@ -190,7 +190,8 @@ _rlib = None
 
 
 def ref_available() -> bool:
-    return os.path.exists(REF_SO)
+    from . import refarm
+    return refarm.available()
 
 
 def ref_lib():
@@ -198,7 +199,8 @@ def ref_lib():
     if _rlib is None:
         if not ref_available():
             raise ImportError(f"{REF_SO} missing: run `make -C oracle ref` where /root/reference exists")
-        lib = C.CDLL(REF_SO)
+        from . import refarm
+        lib = refarm.lib()  # the -march=native build on the build host's CPU model, else x86-64-v3
         V = C.c_void_p
         sig = {
             "ref_last_error": (C.c_char_p, []), "ref_num_threads": (C.c_int, []),
@@ -235,6 +237,8 @@ def ref_lib():
             "ref_ssp_step": (C.c_int, [V, dp, dp, i64p, C.c_double, C.c_int, C.c_int, dp]),
             "ref_total_mass": (C.c_double, [V, dp]),
             "ref_project": (C.c_int, [V, V, C.c_double, C.c_int, dp, dp]),
+            "ref_mesh_periodic_box": (V, [C.c_int, C.c_int, C.c_double, C.c_double]),
+            "ref_project_isentropic_vortex": (C.c_int, [V, V] + [C.c_double] * 8 + [dp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(lib, name)

@@ -7,6 +7,8 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <map>
+#include <algorithm>
 #include <random>
 #include <sstream>
 #include <string>
@@ -53,6 +55,7 @@ struct RefCtx {
   const BoundaryConditions* bc;
   SolverContext ctx;
   RhsBuffers bufs;
+  SolverState held;  // persistent state of the ref_hold_* entries (benchmark arm)
 };
 
 CoefficientArray make_coeffs(const RefCtx* r, const double* c) {
@@ -587,6 +590,129 @@ int ref_export(void* mp, void* tp, double gamma, const double* c, int csv, const
       export_csv(a, mesh, tb, GasModel{gamma}, path);
     else
       export_vtk(a, mesh, tb, GasModel{gamma}, path);
+  });
+}
+
+
+// --------------------------------------------------------------- benchmark arm (no B200 code)
+// The periodic box of BASELINE.json's configs, built with the reference's own code: the
+// n x n box of gen_box_msh (same vertex expression, split_quads triangles, outflow tag) goes
+// through the reference's build_connectivity, then each bottom/left hull edge is joined to
+// its top/right partner (the lower element id stays the left element, whose side gives v0,
+// v1, the normal and the half length exactly as build_connectivity computed them for the
+// hull edge), and the edges are re-sorted into build_connectivity's order (all interior:
+// by (left, side_left)).  Identical to dgb_mesh_generate(DGB_MESH_PERIODIC_BOX) (tested).
+void* ref_mesh_periodic_box(int nx, int ny, double width, double height) {
+  Mesh* out = nullptr;
+  if (guard([&] {
+        if (nx < 2 || ny < 2) throw std::invalid_argument("periodic box needs nx, ny >= 2");
+        MeshPrecursor pre;
+        for (int j = 0; j <= ny; ++j)
+          for (int i = 0; i <= nx; ++i) pre.vertices.push_back({width * i / nx, height * j / ny});
+        auto vid = [nx](int i, int j) { return j * (nx + 1) + i; };
+        for (int j = 0; j < ny; ++j)
+          for (int i = 0; i < nx; ++i) {  // problems.cpp:31-40
+            pre.triangles.push_back({vid(i, j), vid(i + 1, j), vid(i, j + 1)});
+            pre.triangles.push_back({vid(i + 1, j), vid(i + 1, j + 1), vid(i, j + 1)});
+          }
+        for (int i = 0; i < nx; ++i) {
+          pre.boundary_lines.push_back({vid(i, 0), vid(i + 1, 0), 4});
+          pre.boundary_lines.push_back({vid(i, ny), vid(i + 1, ny), 4});
+        }
+        for (int j = 0; j < ny; ++j) {
+          pre.boundary_lines.push_back({vid(0, j), vid(0, j + 1), 4});
+          pre.boundary_lines.push_back({vid(nx, j), vid(nx, j + 1), 4});
+        }
+        Mesh m = build_connectivity(pre);
+        // hull edge of each (wrapped) vertex pair
+        auto wrap = [&](int v) { return vid((v % (nx + 1)) % nx, (v / (nx + 1)) % ny); };
+        std::map<std::pair<int, int>, int> first;
+        std::vector<Edge> edges;
+        for (const Edge& e : m.edges) {
+          if (!e.is_boundary()) {
+            edges.push_back(e);
+            continue;
+          }
+          const int w0 = wrap(e.v0), w1 = wrap(e.v1);
+          const std::pair<int, int> key(std::min(w0, w1), std::max(w0, w1));
+          auto it = first.find(key);
+          if (it == first.end()) {
+            first.emplace(key, static_cast<int>(edges.size()));
+            edges.push_back(e);
+            continue;
+          }
+          Edge& a = edges[it->second];
+          Edge b = e;
+          if (b.left < a.left) std::swap(a, b);
+          a.right = b.left;
+          a.side_right = b.side_left;
+        }
+        for (const Edge& e : edges)
+          if (e.is_boundary()) throw MeshError("periodic box: unmatched hull edge");
+        std::sort(edges.begin(), edges.end(), [](const Edge& a, const Edge& b) {
+          return a.left != b.left ? a.left < b.left : a.side_left < b.side_left;
+        });
+        m.edges = std::move(edges);
+        m.n_boundary_edges = 0;
+        for (int ei = 0; ei < m.n_edges(); ++ei) {
+          const Edge& e = m.edges[ei];
+          m.elements[e.left].edge[e.side_left - 1] = ei;
+          m.elements[e.right].edge[e.side_right - 1] = ei;
+        }
+        out = new Mesh(std::move(m));
+      }))
+    return nullptr;
+  return out;
+}
+
+// Shu's isentropic vortex (the initial data of the benchmark's periodic box; the same
+// formula as dgb_isentropic_vortex), projected with the reference's project_initial.
+int ref_project_isentropic_vortex(void* mp, void* tp, double gamma, double xc, double yc, double beta, double u_inf,
+                                  double v_inf, double width, double height, double* out) {
+  const Mesh& mesh = *static_cast<Mesh*>(mp);
+  const BasisTables& tb = *static_cast<BasisTables*>(tp);
+  return guard([&] {
+    const double g = gamma;
+    auto f = [=](Vec2 x) {
+      double dx = x.x - xc, dy = x.y - yc;
+      if (width > 0.0) dx -= width * std::floor(dx / width + 0.5);
+      if (height > 0.0) dy -= height * std::floor(dy / height + 0.5);
+      const double r2 = dx * dx + dy * dy;
+      const double e = std::exp(0.5 * (1.0 - r2));
+      const double du = -beta / (2.0 * M_PI) * e * dy;
+      const double dv = beta / (2.0 * M_PI) * e * dx;
+      const double temp = 1.0 - (g - 1.0) * beta * beta / (8.0 * g * M_PI * M_PI) * e * e;
+      const double rho = std::pow(temp, 1.0 / (g - 1.0));
+      const double p = rho * temp;
+      const double vx = u_inf + du, vy = v_inf + dv;
+      return EulerState{rho, rho * vx, rho * vy, p / (g - 1.0) + 0.5 * rho * (vx * vx + vy * vy)};
+    };
+    CoefficientArray c = project_initial(f, mesh, tb, GasModel{gamma});
+    std::memcpy(out, c.data.data(), c.data.size() * 8);
+  });
+}
+
+// A state held inside the context, so a timed run_fixed_steps call copies nothing in or
+// out: the reference driver exactly as proj/tools and its tests call it (one RkWorkspace
+// per call, solver.cpp:600-613).
+int ref_hold_set(void* rp, const double* c, double t) {
+  RefCtx* r = static_cast<RefCtx*>(rp);
+  return guard([&] {
+    r->held.coeffs = make_coeffs(r, c);
+    r->held.t = t;
+    r->held.step_count = 0;
+  });
+}
+int ref_hold_run_fixed_steps(void* rp, int64_t n, double* resid) {
+  RefCtx* r = static_cast<RefCtx*>(rp);
+  return guard([&] { *resid = run_fixed_steps(r->ctx, r->held, n); });
+}
+int ref_hold_get(void* rp, double* c, double* t, int64_t* step) {
+  RefCtx* r = static_cast<RefCtx*>(rp);
+  return guard([&] {
+    std::memcpy(c, r->held.coeffs.data.data(), r->held.coeffs.data.size() * 8);
+    if (t) *t = r->held.t;
+    if (step) *step = r->held.step_count;
   });
 }
 

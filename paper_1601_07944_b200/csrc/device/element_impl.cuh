@@ -92,6 +92,18 @@ __device__ __forceinline__ Prim primitives(const double (&U)[4], double g1) {
 
 __device__ __forceinline__ bool admissible(const double (&U)[4], const Prim& w) { return U[0] > 0.0 && w.p > 0.0; }
 
+// CFL wave speed |v.n| + c at a side midpoint with the reference's own operations
+// (max_wave_speed / sound_speed / pressure, euler.hpp:29-55): IEEE division and square
+// root, no Newton approximations, so the time step carries no approximation error
+// relative to stable_dt (solver.cpp:427-461).  `ok` = admissible(u) as the reference
+// tests it before the wave speed.
+__device__ __forceinline__ double wave_speed_ieee(const double (&U)[4], double nx, double ny, double gamma, bool& ok) {
+  const double p = (gamma - 1.0) * (U[3] - 0.5 * (U[1] * U[1] + U[2] * U[2]) / U[0]);
+  ok = U[0] > 0.0 && p > 0.0;
+  const double vn = (U[1] * nx + U[2] * ny) / U[0];
+  return fabs(vn) + sqrt(gamma * p / U[0]);
+}
+
 // Contravariant fluxes fr = ta F1 + tb F2, fs = tc F1 + td F2 of the analytic flux
 // (euler.hpp:43-50) through the contravariant velocities: 16 FP64 operations instead of
 // forming F1, F2 and rotating them (26).
@@ -644,12 +656,13 @@ __device__ __forceinline__ void element_body(const Tab<P>& T, const Geo& geo, co
         }
         v[3] = v[0];
         transpose4(v, g);  // lane q < 3: state at the midpoint of side q
-        const Prim w = primitives(v, g1);
         const double nxq = g == 0 ? snx[0] : (g == 1 ? snx[1] : snx[2]);
         const double nyq = g == 0 ? sny[0] : (g == 1 ? sny[1] : sny[2]);
         double lam = 0.0;
-        if (admissible(v, w)) {
-          lam = fabs(w.vx * nxq + w.vy * nyq) + sqrt(gamma * w.p * w.inv);
+        bool ok;
+        const double ws = wave_speed_ieee(v, nxq, nyq, gamma, ok);
+        if (ok) {
+          lam = ws;
         } else if (valid && g < 3) {
           record_error(sc, err_key(a.seq_next, kPassDt, __ldg(geo.ref_id + e), g + 1));
         }
@@ -909,10 +922,11 @@ __device__ __forceinline__ void element_body_g1(const Tab<P>& T, const Geo& geo,
             for (int j = 1; j < NP; ++j) s = fma(T.phm[q][j], acc[m][j], s);
             U[m] = s;
           }
-          const Prim w = primitives(U, g1);
-          if (admissible(U, w)) {
-            const int ed = __ldg(geo.eid + q * ld + e);
-            lam = std_max(lam, fabs(w.vx * __ldg(geo.enx + ed) + w.vy * __ldg(geo.eny + ed)) + sqrt(gamma * w.p * w.inv));
+          const int ed = __ldg(geo.eid + q * ld + e);
+          bool ok;
+          const double ws = wave_speed_ieee(U, __ldg(geo.enx + ed), __ldg(geo.eny + ed), gamma, ok);
+          if (ok) {
+            lam = std_max(lam, ws);
           } else {
             record_error(sc, err_key(a.seq_next, kPassDt, __ldg(geo.ref_id + e), q + 1));
           }
@@ -936,7 +950,7 @@ __device__ __forceinline__ void dt_body(const Tab<P>& T, const Geo& geo, const d
                                         int slot, unsigned long long seq) {
   constexpr int NP = Dim<P>::NP;
   const long long ld = geo.ld;
-  const double gamma = geo.gamma, g1 = gamma - 1.0;
+  const double gamma = geo.gamma;
   double lam_min = __longlong_as_double(0x7ff0000000000000ll);
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < geo.ld; e += gridDim.x * blockDim.x) {
     if (e >= geo.N) continue;
@@ -951,13 +965,14 @@ __device__ __forceinline__ void dt_body(const Tab<P>& T, const Geo& geo, const d
         for (int j = 1; j < NP; ++j) s = fma(T.phm[q][j], __ldg(c + (static_cast<long long>(m) * NP + j) * ld + e), s);
         U[m] = s;
       }
-      const Prim w = primitives(U, g1);
-      if (!admissible(U, w)) {
+      const int ed = __ldg(geo.eid + q * ld + e);
+      bool ok;
+      const double ws = wave_speed_ieee(U, __ldg(geo.enx + ed), __ldg(geo.eny + ed), gamma, ok);
+      if (!ok) {
         record_error(sc, err_key(seq, kPassDt, __ldg(geo.ref_id + e), q + 1));
         continue;
       }
-      const int ed = __ldg(geo.eid + q * ld + e);
-      lam = std_max(lam, fabs(w.vx * __ldg(geo.enx + ed) + w.vy * __ldg(geo.eny + ed)) + sqrt(gamma * w.p * w.inv));
+      lam = std_max(lam, ws);
     }
     lam_min = std_min(lam_min, 2.0 * __ldg(geo.inradius + e) / ((2.0 * P + 1.0) * lam));
   }

@@ -713,10 +713,11 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
         for (int m = 0; m < 4; ++m) U[m] = t == 0 ? v[0][m] : (t == 1 ? v[1][m] : v[2][m]);
         const int qq = t < 3 ? t : 2;
         const int edq = __ldg(geo.eid + qq * ld + e);
-        const Prim w = primitives(U, g1);
         double lam = 0.0;
-        if (admissible(U, w)) {
-          lam = fabs(w.vx * __ldg(geo.enx + edq) + w.vy * __ldg(geo.eny + edq)) + sqrt(gamma * w.p * w.inv);
+        bool ok;
+        const double ws = wave_speed_ieee(U, __ldg(geo.enx + edq), __ldg(geo.eny + edq), gamma, ok);
+        if (ok) {
+          lam = ws;
         } else if (valid && t < 3) {
           record_error(sc, err_key(a.seq_next, kPassDt, __ldg(geo.ref_id + e), t + 1));
         }

@@ -190,20 +190,23 @@ __global__ void __launch_bounds__(kBlock, DGB_LIMIT_MINB) k_limit(Geo geo, LimAr
         double U[4];
 #pragma unroll
         for (int m = 0; m < 4; ++m) U[m] = fma(T.phm[q][2], c2[m], fma(T.phm[q][1], c1[m], T.phm[q][0] * c0[m]));
-        const Prim w = primitives(U, g1);
-        if (!admissible(U, w)) {
+#if DGB_LIMIT_CFL_PREFETCH
+        const double nxq = enx3[q], nyq = eny3[q];
+#else
+        const int ed = __ldg(geo.eid + q * ld + e);
+        const double nxq = __ldg(geo.enx + ed), nyq = __ldg(geo.eny + ed);
+#endif
+        bool ok;
+        const double ws = wave_speed_ieee(U, nxq, nyq, geo.gamma, ok);
+        if (!ok) {
           record_error(sc, err_key(a.seq, kPassDt, __ldg(geo.ref_id + e), q + 1));
           continue;
         }
-#if DGB_LIMIT_CFL_PREFETCH
-        lam = std_max(lam, fabs(w.vx * enx3[q] + w.vy * eny3[q]) + sqrt_nr(geo.gamma * w.p * w.inv));
+        lam = std_max(lam, ws);
       }
+#if DGB_LIMIT_CFL_PREFETCH
       lam_min = std_min(lam_min, 2.0 * rin / (3.0 * lam));
 #else
-        const int ed = __ldg(geo.eid + q * ld + e);
-        lam = std_max(lam, fabs(w.vx * __ldg(geo.enx + ed) + w.vy * __ldg(geo.eny + ed)) +
-                            sqrt_nr(geo.gamma * w.p * w.inv));
-      }
       lam_min = std_min(lam_min, 2.0 * __ldg(geo.inradius + e) / (3.0 * lam));
 #endif
     }
@@ -214,28 +217,31 @@ __global__ void __launch_bounds__(kBlock, DGB_LIMIT_MINB) k_limit(Geo geo, LimAr
   if (a.push) __threadfence_system();
 }
 
-int g_lim_pts[2] = {0, 0};  // host copy of (n_edge, n_pts) of the uploaded table
+// host copy of (n_edge, n_pts) of the table uploaded to each device's bank (packed in one
+// atomic word: the limiter may be launched from several host threads)
+std::atomic<int> g_lim_pts[kMaxDevices];
 }  // namespace
 
 cudaError_t upload_limtab(const LimTab& t, cudaStream_t s) {
-  g_lim_pts[0] = t.n_edge;
-  g_lim_pts[1] = t.edge_begin + t.n_edge + 3 == t.n_pts ? t.n_pts : -1;
+  const int npt = t.edge_begin + t.n_edge + 3 == t.n_pts ? t.n_pts : 0;
+  g_lim_pts[current_device()].store(t.n_edge | (npt << 16));
   return cudaMemcpyToSymbolAsync(c_lim, &t, sizeof(t), 0, cudaMemcpyHostToDevice, s);
 }
 
 constexpr int kLimNE = 6, kLimNPT = 12;  // p = 1 tables: 2 points per edge, 3 interior
 
 int limit_resident_blocks() {
-  static int occ = 0;
-  if (!occ) occ = occupancy(k_limit<kLimNE, kLimNPT, 3>);
-  return occ;
+  static std::atomic<int> occ{0};
+  int o = occ.load(std::memory_order_relaxed);
+  if (!o) occ.store(o = occupancy(k_limit<kLimNE, kLimNPT, 3>), std::memory_order_relaxed);
+  return o;
 }
 
 cudaError_t launch_limit(int grid, const Geo& g, const LimArgs& a, cudaStream_t s) {
   if (a.e1 <= a.e0) return cudaSuccess;
   if (grid <= 0) grid = grid_for(a.e1 - a.e0, limit_resident_blocks());
   const int epi = (a.want_lambda ? 1 : 0) | (a.want_resid ? 2 : 0);
-  if (g_lim_pts[0] == kLimNE && g_lim_pts[1] == kLimNPT) {
+  if (g_lim_pts[current_device()].load() == (kLimNE | (kLimNPT << 16))) {
     switch (epi) {
       case 0: k_limit<kLimNE, kLimNPT, 0><<<grid, kBlock, 0, s>>>(g, a); break;
       case 1: k_limit<kLimNE, kLimNPT, 1><<<grid, kBlock, 0, s>>>(g, a); break;

@@ -1,6 +1,8 @@
 // One translation unit per polynomial degree: its constant bank, the four
 // element-kernel modes and the CFL kernel.  Included by kernels_pN.cu with
 // DGB_P defined.
+#include <atomic>
+
 #include "element_mma.cuh"
 #include "launch.hpp"
 
@@ -97,14 +99,25 @@ __global__ void __launch_bounds__(kBlock) k_dt(Geo geo, const double* __restrict
   dt_body<DGB_P>(c_tab, geo, c, sc, slot, seq);
 }
 
-int g_sms = 0;
+// Per-device caches: contexts on several devices may launch from several host threads
+// (dist.run_group), so every entry is an atomic indexed by the current device.
+constexpr int kMaxDevices = 64;
+std::atomic<int> g_sms[kMaxDevices];
+int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev & (kMaxDevices - 1);
+}
 int sm_count() {
-  if (!g_sms) {
+  std::atomic<int>& s = g_sms[current_device()];
+  int v = s.load(std::memory_order_relaxed);
+  if (!v) {
     int dev = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    s.store(v, std::memory_order_relaxed);
   }
-  return g_sms;
+  return v;
 }
 template <class Kern>
 int occupancy(Kern k, int smem = 0, int threads = kBlock) {
@@ -121,16 +134,20 @@ int grid_for(long long threads, int blocks_per_sm, int block = kBlock) {
 
 template <>
 cudaError_t Launch<DGB_P>::upload(const Tab<DGB_P>& t, cudaStream_t s) {
-  if constexpr (kMma) {  // opt in to > 48 KB of dynamic shared memory
-    static bool done = false;
-    if (!done) {
+  if constexpr (kMma) {  // opt in to > 48 KB of dynamic shared memory: a per-device function attribute
+    static std::atomic<unsigned long long> done{0};
+    const unsigned long long bit = 1ull << current_device();
+    if (!(done.load() & bit)) {
+      cudaError_t err = cudaSuccess;
       for (int flux = 0; flux < 2; ++flux)
         for (int mode = 0; mode < 4; ++mode)
           for (int var = 0; var < 8; ++var)
-            with_instance(flux, mode, var, [](auto k) {
-              cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+            with_instance(flux, mode, var, [&](auto k) {
+              const cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+              if (e != cudaSuccess) err = e;
             });
-      done = true;
+      if (err != cudaSuccess) return err;
+      done.fetch_or(bit);
     }
   }
   return cudaMemcpyToSymbolAsync(c_tab, &t, sizeof(t), 0, cudaMemcpyHostToDevice, s);
@@ -139,10 +156,13 @@ cudaError_t Launch<DGB_P>::upload(const Tab<DGB_P>& t, cudaStream_t s) {
 template <>
 int Launch<DGB_P>::resident_blocks(int mode) {
   // the LLF instance of the full variant (the others are sized the same by __launch_bounds__)
-  static int cache[4] = {0, 0, 0, 0};
-  if (!cache[mode])
-    with_instance(kFluxLLF, mode, 7, [&](auto k) { cache[mode] = occupancy(k, kSmem, kThreads); });
-  return cache[mode];
+  static std::atomic<int> cache[4];
+  int v = cache[mode].load(std::memory_order_relaxed);
+  if (!v) {
+    with_instance(kFluxLLF, mode, 7, [&](auto k) { v = occupancy(k, kSmem, kThreads); });
+    cache[mode].store(v, std::memory_order_relaxed);
+  }
+  return v;
 }
 
 template <>
@@ -180,9 +200,10 @@ cudaError_t Launch<DGB_P>::element(int mode, int grid, const Geo& g, const Stage
 template <>
 cudaError_t Launch<DGB_P>::dt(int grid, const Geo& g, const double* c, Scalars* sc, int slot, unsigned long long seq,
                               cudaStream_t s) {
-  static int occ = 0;
-  if (!occ) occ = occupancy(k_dt);
-  if (grid <= 0) grid = grid_for(g.ld, occ);
+  static std::atomic<int> occ{0};
+  int o = occ.load(std::memory_order_relaxed);
+  if (!o) occ.store(o = occupancy(k_dt), std::memory_order_relaxed);
+  if (grid <= 0) grid = grid_for(g.ld, o);
   k_dt<<<grid, kBlock, 0, s>>>(g, c, sc, slot, seq);
   return cudaGetLastError();
 }

@@ -13,6 +13,7 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -389,8 +390,24 @@ struct dgb_ctx {
 
 namespace {
 
-// Which context's tables currently sit in each degree's constant bank, per device.
-std::map<std::pair<int, int>, const dgb_ctx*> g_bank_owner;
+// Contents of each degree's constant bank, per (device, degree): a context uploads its
+// tables only when the bank holds different bytes (contexts built from the same tables
+// share the bank, so partitions driven from several host threads never rewrite it under
+// each other's kernels).  When the content does change, the device is drained first so no
+// kernel of another context still reads the old tables.  Guarded by g_bank_mutex: contexts
+// may run from several host threads (dist.run_group).
+std::mutex g_bank_mutex;
+std::map<std::pair<int, int>, std::vector<char>> g_bank_content;
+
+template <class T>
+bool bank_claim(int device, int key, const T& tab) {  // caller holds g_bank_mutex
+  std::vector<char>& cur = g_bank_content[std::make_pair(device, key)];
+  const char* b = reinterpret_cast<const char*>(&tab);
+  if (cur.size() == sizeof(T) && std::memcmp(cur.data(), b, sizeof(T)) == 0) return false;
+  if (!cur.empty()) CU(cudaDeviceSynchronize());
+  cur.assign(b, b + sizeof(T));
+  return true;
+}
 
 void set_device(dgb_ctx* c) { CU(cudaSetDevice(c->device)); }
 
@@ -455,10 +472,9 @@ void sync(dgb_ctx* c) {
 
 template <int P>
 void upload_tab(dgb_ctx* c, dgbk::Tab<P>& tab) {
-  auto key = std::make_pair(c->device, P);
-  if (g_bank_owner[key] != c) {
+  if (bank_claim(c->device, P, tab)) {
     CU(dgbk::Launch<P>::upload(tab, c->stream));
-    g_bank_owner[key] = c;
+    CU(cudaStreamSynchronize(c->stream));  // the bank is in place before any other stream launches
   }
   if (!c->d_mma.p) {  // DMMA fragment-ordered copy (global memory, staged to smem per block)
     const int n = dgbk::Launch<P>::mma_table(tab, nullptr);
@@ -475,15 +491,13 @@ void upload_tab(dgb_ctx* c, dgbk::Tab<P>& tab) {
 }
 
 void ensure_tables(dgb_ctx* c) {
+  std::lock_guard<std::mutex> lock(g_bank_mutex);
   switch (c->p) {
     case 1:
       upload_tab<1>(c, c->tab1);
-      {
-        auto key = std::make_pair(c->device, 100);
-        if (g_bank_owner[key] != c) {
-          CU(dgbk::upload_limtab(c->lim, c->stream));
-          g_bank_owner[key] = c;
-        }
+      if (bank_claim(c->device, 100, c->lim)) {
+        CU(dgbk::upload_limtab(c->lim, c->stream));
+        CU(cudaStreamSynchronize(c->stream));
       }
       break;
     case 2: upload_tab<2>(c, c->tab2); break;
@@ -1262,6 +1276,7 @@ int dgb_part_create(const dgb_mesh_view* m, const dgb_tables_view* t, const dgb_
       default: fill_tab<5>(c->tab5, t); break;
     }
     if (c->p == 1) {  // limiter evaluation points (solver.cpp:296-321)
+      std::memset(&c->lim, 0, sizeof c->lim);  // the bank is compared bytewise (bank_claim)
       dgbk::LimTab& L = c->lim;
       int idx = 0;
       for (int k = 0; k < c->nq; ++k, ++idx) {
@@ -1309,6 +1324,9 @@ int dgb_part_create(const dgb_mesh_view* m, const dgb_tables_view* t, const dgb_
       CU(cudaMemsetAsync(c->d_peers, 0, sizeof(dgbk::PeerTab), c->stream));
     }
     reset_scalars(c.get(), 0.0);
+    // constant banks and the kernels' shared-memory opt-in for this device, now rather than
+    // at the first launch (partitions may first launch from several host threads at once)
+    ensure_tables(c.get());
     sync(c.get());
     *out = c.release();
     return DGB_OK;
@@ -1331,8 +1349,6 @@ int dgb_destroy(dgb_ctx* c) {
     }
   for (cudaEvent_t ev : {c->ev_h2d, c->ev_in_free, c->ev_perm_out, c->ev_out_free})
     if (ev) cudaEventDestroy(ev);
-  for (auto it = g_bank_owner.begin(); it != g_bank_owner.end();)
-    it = it->second == c ? g_bank_owner.erase(it) : std::next(it);
   if (c->d_sc) cudaFree(c->d_sc);
   if (c->h_sc) cudaFreeHost(c->h_sc);
   if (c->d_red) cudaFree(c->d_red);
@@ -1971,14 +1987,37 @@ int dgb_part_peer_view(dgb_ctx* c, dgb_peer_view* out) {
   });
 }
 
-int dgb_part_attach_peer(dgb_ctx* c, int peer, const dgb_peer_view* v) {
-  return guarded([&] {
-    if (!c->partitioned || peer < 0 || peer >= c->world || peer == c->rank || !v)
-      throw Fail{DGB_ERR_ARG, "bad peer"};
-    for (int k = 0; k < 4; ++k) c->h_peers.buf[peer][k] = static_cast<double*>(v->buf[k]);
+namespace {
+void attach_view(dgb_ctx* c, int peer, const dgb_peer_view* v) {
+  if (!c->partitioned || peer < 0 || peer >= c->world || peer == c->rank || !v) throw Fail{DGB_ERR_ARG, "bad peer"};
+  for (int k = 0; k < 4; ++k) c->h_peers.buf[peer][k] = static_cast<double*>(v->buf[k]);
     c->h_peers.ld[peer] = v->ld;
     c->h_peers.flag[peer] = static_cast<unsigned long long*>(v->flags);
     c->h_peers.scal[peer] = static_cast<unsigned long long*>(v->scal);
+}
+}  // namespace
+
+int dgb_part_attach_peer(dgb_ctx* c, int peer, const dgb_peer_view* v) {
+  return guarded([&] {
+    if (!v || !v->buf[0]) throw Fail{DGB_ERR_ARG, "bad peer view"};
+    // a peer on another device of this process: this context's kernels store into the peer's
+    // buffers, so this device needs peer access to the peer's device (NVLink P2P)
+    cudaPointerAttributes pa{};
+    CU(cudaPointerGetAttributes(&pa, v->buf[0]));
+    if (pa.type == cudaMemoryTypeDevice && pa.device != c->device) {
+      int can = 0;
+      CU(cudaDeviceCanAccessPeer(&can, c->device, pa.device));
+      if (!can)
+        throw Fail{DGB_ERR_ARG, "device " + std::to_string(c->device) + " cannot access peer device " +
+                                    std::to_string(pa.device) + " (no P2P path)"};
+      set_device(c);
+      const cudaError_t e = cudaDeviceEnablePeerAccess(pa.device, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled)
+        cudaGetLastError();  // clear the sticky-free "already enabled" status
+      else
+        CU(e);
+    }
+    attach_view(c, peer, v);
     return DGB_OK;
   });
 }
@@ -2009,7 +2048,8 @@ int dgb_part_attach_peer_ipc(dgb_ctx* c, int peer, const void* handles, int32_t 
     v.flags = ptrs[4];
     v.scal = static_cast<unsigned long long*>(ptrs[4]) + dgbk::kMaxRanks;
     v.ld = peer_ld;
-    return dgb_part_attach_peer(c, peer, &v);
+    attach_view(c, peer, &v);  // cudaIpcMemLazyEnablePeerAccess already enabled the P2P mapping
+    return DGB_OK;
   });
 }
 

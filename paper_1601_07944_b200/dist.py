@@ -18,7 +18,9 @@ Two ways to wire the ranks:
   CUDA IPC handles exchanged with ``torch.distributed.all_gather_object``.
 
 Coefficient arrays cross the ABI in "compact" order: owned ids then halo ids
-(``local_ids``); ``PartContext.upload_global`` slices a reference-layout global array.
+(``local_ids``).  ``PartContext.upload`` takes compact arrays only and
+``PartContext.upload_global`` takes a reference-layout global array (it gathers the
+rank's columns); the shapes are checked, never guessed.
 """
 from __future__ import annotations
 
@@ -100,12 +102,21 @@ class PartContext(SolverContext):
         return (kEq, self.tables.n_p, self.info.n_owned + self.info.n_halo)
 
     def upload(self, slot, coeffs):
+        """Compact-order array [4][n_p][n_owned + n_halo] (owned ids, then halo ids)."""
         c = np.asarray(coeffs, np.float64)
-        if c.shape[-1] == self.mesh.n_elements() and c.shape[-1] != self._shape()[-1]:
-            c = c[:, :, self.local_ids]
+        if c.shape != self._shape():
+            raise ValueError(f"PartContext.upload takes a compact array of shape {self._shape()}, got {c.shape} "
+                             "(use upload_global for a reference-layout global array)")
         super().upload(slot, np.ascontiguousarray(c))
 
-    upload_global = upload
+    def upload_global(self, slot, coeffs):
+        """Reference-layout global array [4][n_p][n_elements]: the rank's owned and halo
+        columns are gathered in compact order."""
+        c = np.asarray(coeffs, np.float64)
+        if c.shape != (kEq, self.tables.n_p, self.mesh.n_elements()):
+            raise ValueError(f"PartContext.upload_global takes a global array of shape "
+                             f"{(kEq, self.tables.n_p, self.mesh.n_elements())}, got {c.shape}")
+        self.upload(slot, c[:, :, self.local_ids])
 
     def download(self, slot):
         out = np.empty((kEq, self.tables.n_p, self.info.n_owned))
@@ -220,7 +231,7 @@ def run_fixed_steps_group(parts: Sequence[PartContext], state: SolverState, n_st
     """run_fixed_steps over an in-process partition group; gathers the owned results back
     into ``state`` (reference layout) and returns the global residual."""
     for p in parts:
-        p.upload(L.SLOT_STATE, state.coeffs)
+        p.upload_global(L.SLOT_STATE, state.coeffs)
         _check(lib.dgb_set_time(p.handle, state.t, state.step_count))
 
     def go(p):

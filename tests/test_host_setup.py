@@ -105,6 +105,28 @@ def test_periodic_box_connectivity():
     assert abs(m.total_area() - 1.0) < 1e-12
 
 
+@pytest.mark.skipif(not bind.ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("n", [3, 7, 40])
+def test_periodic_box_identical_to_reference_built(n):
+    """The reference arm's periodic box (ref_mesh_periodic_box: the reference's own
+    build_connectivity with the hull edges joined) is our DGB_MESH_PERIODIC_BOX, array for
+    array, and the reference's project_initial of the isentropic vortex equals ours: both
+    arms of the benchmark run the identical workload."""
+    mine = dg2d.generate_mesh(L.MESH_PERIODIC_BOX, n, n, 10.0, 10.0)
+    ref = bind.RefMesh(bind.ref_lib().ref_mesh_periodic_box(n, n, 10.0, 10.0))
+    assert ref.nb == 0
+    for k, v in ref.export().items():
+        a = np.asarray(getattr(mine, k)).reshape(v.shape)
+        assert np.array_equal(a, v), k
+    for p in (1, 3):
+        rt = bind.RefTables(p)
+        c_ref = np.empty((4, rt.n_p, ref.ne))
+        assert bind.ref_lib().ref_project_isentropic_vortex(ref.h, rt.h, 1.4, 5.0, 5.0, 5.0, 1.0, 1.0, 10.0, 10.0,
+                                                             c_ref.ctypes.data_as(bind.dp)) == 0
+        c = dg2d.project_initial(dg2d.IsentropicVortex(), mine, dg2d.build_tables(p))
+        assert np.max(np.abs(c - c_ref)) <= 1e-15 * np.max(np.abs(c_ref))
+
+
 # ----------------------------------------------------------------------------- basis (test_basis.cpp)
 def test_table_sizes_and_counts():
     for p, nq in zip(range(1, 6), (3, 6, 12, 16, 25)):

@@ -187,6 +187,45 @@ def test_in_process_partitions_bit_identical_to_whole_mesh(name, p, scheme, worl
 
 
 @pytest.mark.gpu
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs in this process")
+@pytest.mark.parametrize("p,limiting", [(1, True), (3, False)])
+def test_partitions_on_different_devices_bit_identical(p, limiting):
+    """connect_local across devices: dgb_part_attach_peer enables P2P access between the
+    devices, and the halo stores cross NVLink; bit-identical to the whole-mesh solve."""
+    ndev = min(torch.cuda.device_count(), 4)
+    name = "dmr" if limiting else "periodic"
+    mesh, tb, bc, c0 = _problem(name, p)
+    opts = dg2d.SolverOptions(scheme=L.SSP_RK3, cfl=0.3, limiting=limiting)
+    ref, res_ref = _whole(mesh, tb, bc, c0, opts, 10)
+    parts = [D.PartContext(mesh, tb, r, ndev, bc=bc, options=opts, device=r) for r in range(ndev)]
+    for q in parts:
+        q.set_timeout(30.0)
+    D.connect_local(parts)
+    st = dg2d.SolverState(c0.copy())
+    res = D.run_fixed_steps_group(parts, st, 10)
+    assert np.array_equal(st.coeffs, ref.coeffs)
+    assert res == res_ref and st.t == ref.t
+    for q in parts:
+        q.close()
+
+
+@pytest.mark.gpu
+def test_partition_upload_layout_is_explicit():
+    """upload takes compact arrays only, upload_global reference-layout ones (a
+    shape guess passes a global array through unpermuted whenever n_owned + n_halo equals
+    n_elements, e.g. rank 1 of the two-element mesh, whose compact order is [1, 0])."""
+    mesh, tb, bc, c0 = _problem("periodic", 1)
+    parts = [D.PartContext(mesh, tb, r, 2, device=0) for r in range(2)]
+    q = parts[1]
+    with pytest.raises(ValueError):
+        q.upload(L.SLOT_STATE, c0)  # global array through the compact entry
+    q.upload_global(L.SLOT_STATE, c0)
+    q.upload(L.SLOT_STATE, c0[:, :, q.local_ids])
+    for r in parts:
+        r.close()
+
+
+@pytest.mark.gpu
 def test_partition_run_to_time_halts_together():
     mesh, tb, bc, c0 = _problem("periodic", 2)
     opts = dg2d.SolverOptions(scheme=L.SSP_RK3, cfl=0.3)
@@ -196,7 +235,7 @@ def test_partition_run_to_time_halts_together():
     parts = [D.PartContext(mesh, tb, r, 3, options=opts, device=0) for r in range(3)]
     D.connect_local(parts)
     for q in parts:
-        q.upload(L.SLOT_STATE, c0)
+        q.upload_global(L.SLOT_STATE, c0)
 
     def go(q):
         import ctypes as C
@@ -221,7 +260,7 @@ def _ipc_worker(rank, world, port, q):
         part.set_timeout(60.0)
         D.connect_process_group(part)
         st = dg2d.SolverState(c0.copy())
-        part.upload(L.SLOT_STATE, st.coeffs)
+        part.upload_global(L.SLOT_STATE, st.coeffs)
         import ctypes as C
         r = C.c_double()
         dg2d._check(L.lib.dgb_run_fixed_steps(part.handle, L.SSP_RK3, 0.3, 0, 6, C.byref(r), None))
@@ -291,7 +330,7 @@ def test_partition_run_to_steady_matches_whole_mesh():
     parts = [D.PartContext(mesh, tb, r, 3, bc=bc, options=opts, device=0) for r in range(3)]
     D.connect_local(parts)
     for q in parts:
-        q.upload(L.SLOT_STATE, c0)
+        q.upload_global(L.SLOT_STATE, c0)
 
     def go(q):
         import ctypes as C
