@@ -152,6 +152,12 @@ class Oracle:
         self._chk(self.lib.or_rhs(C.byref(self.prob), _d(c), t, _d(out), C.byref(f)), f)
         return out
 
+    def term_scale(self, c, t=0.0):
+        """Per-equation max of (|vol| + sum_q |slot_q|) / detJ (the per-RHS parity scale)."""
+        out = np.zeros(4)
+        _rchk(self.lib.ref_term_scale(self.h, _d(np.ascontiguousarray(c)), t, _d(out)))
+        return out
+
     def limit(self, c):
         c = np.array(c, np.float64, order="C")
         if self.lib.or_limit(C.byref(self.prob), _d(c)):
@@ -238,6 +244,7 @@ def ref_lib():
             "ref_total_mass": (C.c_double, [V, dp]),
             "ref_project": (C.c_int, [V, V, C.c_double, C.c_int, dp, dp]),
             "ref_mesh_periodic_box": (V, [C.c_int, C.c_int, C.c_double, C.c_double]),
+            "ref_term_scale": (C.c_int, [V, dp, C.c_double, dp]),
             "ref_project_isentropic_vortex": (C.c_int, [V, V] + [C.c_double] * 8 + [dp]),
         }
         for name, (res, args) in sig.items():
@@ -410,6 +417,12 @@ class RefSolver:
     def serial_rhs(self, c, t=0.0):
         out = np.zeros(self.shape)
         _rchk(self.lib.ref_serial_rhs(self.h, _d(np.ascontiguousarray(c)), t, _d(out)))
+        return out
+
+    def term_scale(self, c, t=0.0):
+        """Per-equation max of (|vol| + sum_q |slot_q|) / detJ (the per-RHS parity scale)."""
+        out = np.zeros(4)
+        _rchk(self.lib.ref_term_scale(self.h, _d(np.ascontiguousarray(c)), t, _d(out)))
         return out
 
     def limit(self, c):

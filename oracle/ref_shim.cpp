@@ -716,4 +716,34 @@ int ref_hold_get(void* rp, double* c, double* t, int64_t* step) {
   });
 }
 
+
+// Per-equation term scale of the per-RHS parity metric:
+// scale[m] = max_i,j (|vol| + sum_q |slot_q|)(m, j, i) / det_jac_i, from the reference's own
+// volume and surface passes (kept in C++ so a 1M-element p=5 check needs no host copies of
+// the six slot arrays).
+int ref_term_scale(void* rp, const double* c, double t, double* scale) {
+  RefCtx* r = static_cast<RefCtx*>(rp);
+  return guard([&] {
+    CoefficientArray a = make_coeffs(r, c);
+    eval_volume_pass(r->ctx, a, r->bufs.volume);
+    std::fill(r->bufs.surface_left.begin(), r->bufs.surface_left.end(), 0.0);
+    std::fill(r->bufs.surface_right.begin(), r->bufs.surface_right.end(), 0.0);
+    eval_surface_pass(r->ctx, a, t, r->bufs);
+    const int n = r->mesh->n_elements(), np = r->tables->n_p;
+    const size_t per = static_cast<size_t>(kEq) * np * n;
+    for (int m = 0; m < kEq; ++m) {
+      double mx = 0.0;
+      for (int j = 0; j < np; ++j)
+        for (int i = 0; i < n; ++i) {
+          const size_t idx = (static_cast<size_t>(m) * np + j) * n + i;
+          double s = std::abs(r->bufs.volume.data[idx]);
+          for (int q = 0; q < 3; ++q)
+            s += std::abs(r->bufs.surface_left[q * per + idx]) + std::abs(r->bufs.surface_right[q * per + idx]);
+          mx = std::max(mx, s / r->mesh->elements[i].det_jac);
+        }
+      scale[m] = mx;
+    }
+  });
+}
+
 }  // extern "C"
