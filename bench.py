@@ -154,6 +154,63 @@ def barrier(pg):
 
 
 # ----------------------------------------------------------------------------- our arm
+def samples(h, category):
+    """Per-launch device ms of a timer category (3 limiter, 5 stage kernel) since the reset."""
+    from paper_1601_07944_b200 import _lib as L
+    n = C.c_int64()
+    L.lib.dgb_timer_samples(h, category, None, 0, C.byref(n))
+    out = np.zeros(max(n.value, 1))
+    L.lib.dgb_timer_samples(h, category, out.ctypes.data_as(L.c_double_p), n.value, C.byref(n))
+    return out[:n.value]
+
+
+def timed_run(h, stream, scheme, cfl, limiting, steps, pg=None, local=0, kernel_stages=100, stages=3):
+    """Device-timed runs of the resident solver (dgb_run_fixed_steps):
+      * throughput pass: exactly `steps` steps, no per-kernel events (an event record costs
+        ~4 us of GPU time between kernels, tools/gap_probe.py), CUDA events on the launch
+        stream around the whole call, max over ranks;
+      * kernel pass: enough steps for >= `kernel_stages` stages with CUDA events around every
+        stage-kernel (and limiter) launch on the same stream; the medians come from it.
+    Returns (ms of the throughput pass, launches in it, stage-kernel ms samples, limiter ms samples)."""
+    import torch
+    from paper_1601_07944_b200 import _lib as L
+    from paper_1601_07944_b200 import dg2d
+    res = C.c_double()
+
+    def one(n, timers):
+        L.lib.dgb_enable_timers(h, timers)
+        L.lib.dgb_reset_timers(h)
+        l0 = L.lib.dgb_launch_count(h)
+        barrier(pg)
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        dg2d._check(L.lib.dgb_run_fixed_steps(h, scheme, cfl, int(limiting), n, C.byref(res), None))
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier(pg)
+        return max_over_ranks(ev0.elapsed_time(ev1), pg, local), L.lib.dgb_launch_count(h) - l0
+
+    ms, launches = one(steps, 0)
+    one(max(steps, -(-kernel_stages // stages)), 1)
+    st, lim = samples(h, 5), samples(h, 3)
+    L.lib.dgb_enable_timers(h, 0)
+    return ms, launches, st, lim
+
+
+def roofline(p, e_ratio, n_elem, kernel_ms, hbm_gbs, fp64_tf, extra_bytes=0.0):
+    """SURVEY.md 8(d) algorithmic bytes / flops per element per stage x elements, over the
+    median stage-kernel duration; the binding roof is the larger of the two times."""
+    b = alg_bytes(p, e_ratio) * n_elem + extra_bytes
+    f = alg_flops(p, e_ratio) * n_elem
+    bound = "hbm" if b / (hbm_gbs * 1e9) >= f / (fp64_tf * 1e12) else "fp64"
+    ach = b / (kernel_ms * 1e-3) / 1e9 if bound == "hbm" else f / (kernel_ms * 1e-3) / 1e12
+    peak = hbm_gbs if bound == "hbm" else fp64_tf
+    return {"bound": bound, "achieved": ach, "peak": peak, "unit": "GB/s" if bound == "hbm" else "TFLOP/s",
+            "frac": ach / peak, "traffic": ncu_traffic(p), "kernel_ms": kernel_ms,
+            "alg_bytes_per_launch": b, "alg_flops_per_launch": f}
+
+
 def run_b200(args, rank, world, local, pg):
     import torch
     from paper_1601_07944_b200 import _lib as L
@@ -182,6 +239,7 @@ def run_b200(args, rank, world, local, pg):
     e2e_dof, e2e_ms, h2d, d2h = 0.0, 0.0, 0, 0
     stream = torch.cuda.Stream(device=local)
     sampler = ClockSampler(local)
+    legs = {}
     with sampler:
         for p in orders:
             tb = dg2d.build_tables(p)
@@ -198,47 +256,16 @@ def run_b200(args, rank, world, local, pg):
             ctx.upload(L.SLOT_STATE, c0)
             res = C.c_double()
             dg2d._check(L.lib.dgb_run_fixed_steps(h, scheme, args.cfl, 0, args.warmup, C.byref(res), None))
-
-            def timed_steps(timers):
-                # timers=1 brackets every stage-kernel launch with CUDA events on the launch
-                # stream (the roofline's kernel duration); the event records themselves cost
-                # ~4 us of GPU time each between kernels (tools/gap_probe.py), so the
-                # throughput pass runs without them
-                L.lib.dgb_enable_timers(h, timers)
-                L.lib.dgb_reset_timers(h)
-                l0 = L.lib.dgb_launch_count(h)
-                barrier(pg)
-                torch.cuda.synchronize()
-                ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                ev0.record(stream)
-                dg2d._check(L.lib.dgb_run_fixed_steps(h, scheme, args.cfl, 0, args.steps, C.byref(res), None))
-                ev1.record(stream)
-                torch.cuda.synchronize()
-                barrier(pg)
-                return max_over_ranks(ev0.elapsed_time(ev1), pg, local), L.lib.dgb_launch_count(h) - l0
-
-            ms, launches = timed_steps(0)  # throughput: `value`
-            ms_k, _ = timed_steps(1)  # the same K steps again with per-kernel events
-            kms, kn = C.c_double(), C.c_int64()
-            L.lib.dgb_stage_kernel_ms(h, C.byref(kms), C.byref(kn))
-            L.lib.dgb_enable_timers(h, 0)
-            k_avg = kms.value / max(kn.value, 1)
+            ms, launches, st_ms, _ = timed_run(h, stream, scheme, args.cfl, False, args.steps, pg, local,
+                                               stages=stages)
+            k_med = float(np.median(st_ms))
             dof = 4 * np_(p) * N_glob
             upd = dof * stages * args.steps
-            b, f = alg_bytes(p, e_ratio) * N, alg_flops(p, e_ratio) * N
-            ach_bw, ach_fl = b / (k_avg * 1e-3) / 1e9, f / (k_avg * 1e-3) / 1e12
-            bound = "hbm" if b / (hbm_gbs * 1e9) >= f / (fp64_tf * 1e12) else "fp64"
-            roof = {"bound": bound,
-                    "achieved": ach_bw if bound == "hbm" else ach_fl,
-                    "peak": hbm_gbs if bound == "hbm" else fp64_tf,
-                    "unit": "GB/s" if bound == "hbm" else "TFLOP/s",
-                    "traffic": ncu_traffic(p)}
-            roof["frac"] = roof["achieved"] / roof["peak"]
-            roof["kernel_ms"] = k_avg
-            roof["alg_bytes_per_launch"] = b
-            roof["alg_flops_per_launch"] = f
+            roof = roofline(p, e_ratio, N, k_med, hbm_gbs, fp64_tf)
             per_order.append({"p": p, "value": upd / (ms * 1e-3), "ms_per_step": ms / args.steps,
-                              "stage_kernel_ms": k_avg, "kernel_share": kms.value / ms_k if ms_k else None,
+                              "stage_kernel_ms_median": k_med, "stage_kernel_ms_mean": float(np.mean(st_ms)),
+                              "stage_kernel_samples": int(st_ms.size),
+                              "kernel_share": float(np.sum(st_ms)) / (ms / args.steps * st_ms.size / stages),
                               "dof": dof, "roofline": roof, "launches_per_step": launches / args.steps})
             tot_dof_upd += upd
             tot_ms += ms
@@ -288,8 +315,14 @@ def run_b200(args, rank, world, local, pg):
                 d2h += n_out * 8 * world
                 per_order[-1]["e2e_value"] = dof * stages * args.e2e_steps / (ms_e * 1e-3)
             ctx.close()
+        if world == 1 and not args.no_legs:
+            for name, fn in (("c3", leg_c3), ("c4", leg_c4), ("c5", leg_c5), ("limiter_overhead", leg_limiter_overhead)):
+                try:
+                    legs[name] = fn(args, local, stream, hbm_gbs, fp64_tf)
+                except Exception as e:  # an informational leg must never break the headline
+                    legs[name] = {"failed": repr(e)}
 
-    dom = max(per_order, key=lambda r: r["stage_kernel_ms"] * stages)
+    dom = max(per_order, key=lambda r: r["stage_kernel_ms_median"] * stages)
     line = {
         "metric": METRIC, "value": tot_dof_upd / (tot_ms * 1e-3), "unit": "DOF-updates/s/stage",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -298,15 +331,18 @@ def run_b200(args, rank, world, local, pg):
         "data": "synthetic: periodic isentropic vortex initial data (projected), no dataset",
         "config": {"workload": f"isentropic vortex, periodic {n}x{n * world} box ({N_glob} triangles), "
                                f"p={','.join(map(str, orders))} sweep, {args.scheme.upper()}, cfl {args.cfl}",
+                   "blend": "value = sum over the orders of the DOF updates (4 Np N x stages x K steps) / sum "
+                            "over the orders of the device time of their K-step runs (each order weighs by its "
+                            "own time; per-order values in per_order)",
                    "triangles_per_gpu": N, "edges_per_gpu": mesh.n_edges() // world, "orders": orders,
                    "scheme": args.scheme, "stages_per_step": stages,
                    "l2": "inputs larger than L2 (>=288 MB of coefficients per stage)",
-                   "timing": "value: K steps without per-kernel events; roofline kernel_ms: the same K "
-                             "steps again with CUDA events around every stage kernel on its stream",
+                   "timing": "value: K steps without per-kernel events; roofline kernel_ms: median over >= 100 "
+                             "stage-kernel launches timed with CUDA events on their stream in a second pass",
                    "parallelism": (f"element partition x{world} (contiguous strips), peer-memory halo "
                                    "exchange fused into the stage kernel") if world > 1 else "single GPU"},
         "roofline": dict(dom["roofline"], p=dom["p"],
-                         note=f"dominant kernel = fused stage kernel at p={dom['p']}; "
+                         note=f"dominant kernel = fused stage kernel at p={dom['p']} (median launch); "
                               f"HBM peak {hbm_src}; FP64 peak measured in-run (DFMA loop) {fp64_tf:.1f} TF/s"),
         "per_order": per_order,
         "gpu_launches": tot_launch,
@@ -319,58 +355,146 @@ def run_b200(args, rank, world, local, pg):
                        "note": "per step: pinned host state -> dgb_stage_input_async + dgb_commit_input -> one RK step -> dgb_download_async (one copy stream per direction: step k+1's upload overlaps step k's compute and download); wall clock incl. dgb_sync"}
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(orders, args)
-    if world == 1 and args.dmr_nx > 0:
-        line["dmr"] = dmr_leg(args, local)
+    line.update(legs)
     return line
 
 
-def dmr_leg(args, local):
-    """BASELINE.json configs[3] (C4): double Mach reflection, p=1, Barth-Jespersen limiter on
+def _leg_context(mesh, p, bc, opts, local, stream, c0):
+    from paper_1601_07944_b200 import _lib as L
+    from paper_1601_07944_b200 import dg2d
+    ctx = dg2d.SolverContext(mesh, dg2d.build_tables(p), bc=bc, options=opts, device=local)
+    dg2d._check(L.lib.dgb_set_stream(ctx.handle, C.c_void_p(stream.cuda_stream)))
+    ctx.upload(L.SLOT_STATE, c0)
+    return ctx
+
+
+def leg_c3(args, local, stream, hbm_gbs, fp64_tf):
+    """BASELINE configs[2] (C3): supersonic vortex / channel with wall BCs, p = 3, ~1M
+    triangles (vortex level 6: 737,280 triangles; curved reflecting walls, Dirichlet inflow,
+    outflow), SSP-RK3, cfl 0.3.  Exercises the boundary-code instance of the DMMA kernel."""
+    from paper_1601_07944_b200 import _lib as L
+    from paper_1601_07944_b200 import dg2d
+    mesh = dg2d.generate_mesh(L.MESH_VORTEX, args.c3_level, 0, 1.0, 1.384)
+    N, e = mesh.n_elements(), mesh.n_edges() / mesh.n_elements()
+    c0 = dg2d.project_initial(lambda xy: dg2d.vortex_exact(xy), mesh, dg2d.build_tables(3))
+    ctx = _leg_context(mesh, 3, dg2d.vortex_boundary(), dg2d.SolverOptions(scheme=L.SSP_RK3, cfl=0.3), local,
+                       stream, c0)
+    res = C.c_double()
+    dg2d._check(L.lib.dgb_run_fixed_steps(ctx.handle, L.SSP_RK3, 0.3, 0, args.warmup, C.byref(res), None))
+    ms, launches, st, _ = timed_run(ctx.handle, stream, L.SSP_RK3, 0.3, False, args.steps)
+    ctx.close()
+    k = float(np.median(st))
+    upd = 4 * np_(3) * N * 3 * args.steps
+    return {"workload": f"supersonic vortex level {args.c3_level} ({N} triangles, walls + inflow + outflow), p=3, "
+                        "SSP-RK3, cfl 0.3", "steps": args.steps, "value": upd / (ms * 1e-3),
+            "unit": "DOF-updates/s/stage", "ms_per_step": ms / args.steps, "stage_kernel_ms_median": k,
+            "stage_kernel_samples": int(st.size), "roofline": roofline(3, e, N, k, hbm_gbs, fp64_tf)}
+
+
+def leg_c4(args, local, stream, hbm_gbs, fp64_tf):
+    """BASELINE configs[3] (C4): double Mach reflection, p = 1, Barth-Jespersen limiter on
     every stage, midpoint RK2 (dmr_desk.cfg), on the 2000x500 channel (2M triangles): the
-    paper's own headline path (GTX 580 mesh C: 1.31e8 DOF-updates/s/stage).
-    Informational; not part of `value`."""
-    import torch
+    paper's own headline path (GTX 580 mesh C: 1.31e8 DOF-updates/s/stage)."""
     from paper_1601_07944_b200 import _lib as L
     from paper_1601_07944_b200 import dg2d
     nx, ny = args.dmr_nx, args.dmr_nx // 4
     mesh = dg2d.generate_mesh(L.MESH_DOUBLE_MACH, nx, ny, 1.0 / 6.0)
+    N, e = mesh.n_elements(), mesh.n_edges() / mesh.n_elements()
     tb = dg2d.build_tables(1)
     setup = dg2d.DoubleMachSetup()
-    ctx = dg2d.SolverContext(mesh, tb, bc=dg2d.double_mach_boundary(setup),
-                             options=dg2d.SolverOptions(rk_order=2, cfl=0.3, limiting=True), device=local)
-    c0 = dg2d.limit(ctx, dg2d.project_initial(lambda xy: dg2d.double_mach_initial(xy, setup), mesh, tb))
-    h = ctx.handle
-    stream = torch.cuda.Stream(device=local)
-    dg2d._check(L.lib.dgb_set_stream(h, C.c_void_p(stream.cuda_stream)))
-    ctx.upload(L.SLOT_STATE, c0)
+    bc = dg2d.double_mach_boundary(setup)
+    opts = dg2d.SolverOptions(rk_order=2, cfl=0.3, limiting=True)
+    lim = dg2d.SolverContext(mesh, tb, bc=bc, options=opts, device=local)
+    c0 = dg2d.limit(lim, dg2d.project_initial(lambda xy: dg2d.double_mach_initial(xy, setup), mesh, tb))
+    lim.close()
+    ctx = _leg_context(mesh, 1, bc, opts, local, stream, c0)
     res = C.c_double()
-    dg2d._check(L.lib.dgb_run_fixed_steps(h, 2, 0.3, 1, args.warmup, C.byref(res), None))
-
-    def timed_steps(timers):  # as run_b200: throughput without, the split with per-kernel events
-        L.lib.dgb_enable_timers(h, timers)
-        L.lib.dgb_reset_timers(h)
-        torch.cuda.synchronize()
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ev0.record(stream)
-        dg2d._check(L.lib.dgb_run_fixed_steps(h, 2, 0.3, 1, args.steps, C.byref(res), None))
-        ev1.record(stream)
-        torch.cuda.synchronize()
-        return ev0.elapsed_time(ev1)
-
-    ms = timed_steps(0)
-    timed_steps(1)
-    t = L.PassTimers()
-    dg2d._check(L.lib.dgb_timers(h, C.byref(t)))
-    N = mesh.n_elements()
-    upd = 4 * 3 * N * 2 * args.steps
+    dg2d._check(L.lib.dgb_run_fixed_steps(ctx.handle, 2, 0.3, 1, args.warmup, C.byref(res), None))
+    ms, launches, st, _ = timed_run(ctx.handle, stream, 2, 0.3, True, args.steps, stages=2)
+    # the same run as two launches per stage (stage kernel, then limiter kernel): the stage
+    # kernel alone is the unlimited stage's cost, so the fused launch's excess over it is
+    # what limiting costs
+    L.lib.dgb_set_fused_limiter(ctx.handle, 0)
+    ms2, _, st2, lm2 = timed_run(ctx.handle, stream, 2, 0.3, True, args.steps, stages=2)
     ctx.close()
+    upd = 4 * 3 * N * 2 * args.steps
+    k, k2, l2 = float(np.median(st)), float(np.median(st2)), float(np.median(lm2))
     return {"workload": f"double Mach reflection {nx}x{ny} channel ({N} triangles), p=1, BJ limiter every "
                         f"stage, RK2 midpoint, cfl 0.3", "steps": args.steps,
             "value": upd / (ms * 1e-3), "unit": "DOF-updates/s/stage", "ms_per_step": ms / args.steps,
-            "stage_kernel_ms_per_stage": t.stage * 1e3 / (2 * args.steps),
-            "limiter_ms_per_stage": t.limiter * 1e3 / (2 * args.steps),
-            "limiter_share": t.limiter / max(t.stage + t.limiter + t.other, 1e-30),
+            "stage_kernel_ms_median": k, "stage_kernel_samples": int(st.size),
+            "launch": "stage + limiter fused in one cooperative launch (k_stage_limit)",
+            "two_kernel": {"value": upd / (ms2 * 1e-3), "stage_kernel_ms_median": k2, "limiter_ms_median": l2,
+                           "limiter_share": l2 / (k2 + l2)},
+            "limiter_overhead": k / k2 - 1.0, "limiter_share": 1.0 - k2 / k,
+            "roofline_stage": roofline(1, e, N, k, hbm_gbs, fp64_tf),
             "vs_paper_gtx580_mesh_c": upd / (ms * 1e-3) / 1.31e8}
+
+
+def leg_c5(args, local, stream, hbm_gbs, fp64_tf):
+    """BASELINE configs[4] (C5) at N=1: the synthetic 8M-triangle box (2000 x 2000, periodic,
+    isentropic vortex), p = 2..4, SSP-RK3 — the single-GPU point of the scaling curve
+    (bench.py --gpus N runs the partitioned form with N x the triangles)."""
+    from paper_1601_07944_b200 import _lib as L
+    from paper_1601_07944_b200 import dg2d
+    n = args.c5_n
+    mesh = dg2d.generate_mesh(L.MESH_PERIODIC_BOX, n, n, 10.0, 10.0)
+    N, e = mesh.n_elements(), mesh.n_edges() / mesh.n_elements()
+    out = {"workload": f"periodic {n}x{n} box ({N} triangles), isentropic vortex, SSP-RK3, cfl 0.3",
+           "steps": args.steps, "per_order": []}
+    upd_tot, ms_tot = 0.0, 0.0
+    iv = dg2d.IsentropicVortex()
+    for p in [int(x) for x in args.c5_orders.split(",")]:
+        tb = dg2d.build_tables(p)
+        ctx = dg2d.SolverContext(mesh, tb, options=dg2d.SolverOptions(scheme=L.SSP_RK3, cfl=0.3), device=local)
+        dg2d._check(L.lib.dgb_set_stream(ctx.handle, C.c_void_p(stream.cuda_stream)))
+        dg2d.project_on_device(ctx, iv)
+        res = C.c_double()
+        dg2d._check(L.lib.dgb_run_fixed_steps(ctx.handle, L.SSP_RK3, 0.3, 0, args.warmup, C.byref(res), None))
+        ms, launches, st, _ = timed_run(ctx.handle, stream, L.SSP_RK3, 0.3, False, args.steps)
+        ctx.close()
+        k = float(np.median(st))
+        upd = 4 * np_(p) * N * 3 * args.steps
+        upd_tot += upd
+        ms_tot += ms
+        out["per_order"].append({"p": p, "value": upd / (ms * 1e-3), "ms_per_step": ms / args.steps,
+                                 "stage_kernel_ms_median": k, "roofline": roofline(p, e, N, k, hbm_gbs, fp64_tf)})
+    out["value"] = upd_tot / (ms_tot * 1e-3)
+    out["unit"] = "DOF-updates/s/stage"
+    return out
+
+
+def leg_limiter_overhead(args, local, stream, hbm_gbs, fp64_tf):
+    """The reference's limiter-overhead criterion exactly as proj/tests/acceptance.cpp:368-405
+    defines it: supersonic vortex mesh C (level 2), p = 1, RK2, cfl 0.9, 200 warm-up steps,
+    then 10,000 steps timed with limiting off and on (the "on" run starts from the limited
+    projection); overhead = (t_on - t_off) / t_off (threshold 25%, PAPER.md:1060 <= 15%)."""
+    import torch
+    from paper_1601_07944_b200 import _lib as L
+    from paper_1601_07944_b200 import dg2d
+    mesh = dg2d.generate_mesh(L.MESH_VORTEX, 2, 0, 1.0, 1.384)
+    tb = dg2d.build_tables(1)
+    c0 = dg2d.project_initial(lambda xy: dg2d.vortex_exact(xy), mesh, tb)
+    times = {}
+    for lim in (False, True):
+        opts = dg2d.SolverOptions(rk_order=2, cfl=0.9, limiting=lim)
+        ctx = _leg_context(mesh, 1, dg2d.vortex_boundary(), opts, local, stream, c0)
+        if lim:
+            ctx.upload(L.SLOT_STATE, dg2d.limit(ctx, c0.copy()))
+        res = C.c_double()
+        dg2d._check(L.lib.dgb_run_fixed_steps(ctx.handle, 2, 0.9, int(lim), 200, C.byref(res), None))
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        dg2d._check(L.lib.dgb_run_fixed_steps(ctx.handle, 2, 0.9, int(lim), args.lim_steps, C.byref(res), None))
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        times["on" if lim else "off"] = ev0.elapsed_time(ev1)
+        ctx.close()
+    return {"workload": f"supersonic vortex mesh C (level 2, {mesh.n_elements()} triangles), p=1, RK2, cfl 0.9, "
+                        f"{args.lim_steps} steps after 200 warm-up (acceptance.cpp:368-405)",
+            "ms_off": times["off"], "ms_on": times["on"],
+            "overhead": (times["on"] - times["off"]) / times["off"], "threshold": 0.25}
 
 
 # ----------------------------------------------------------------------------- CPU reference
@@ -457,7 +581,12 @@ def main():
     ap.add_argument("--cpu-box", dest="cpu_n", type=int, default=708, help="box size of the CPU sample")
     ap.add_argument("--ref-steps", type=int, default=5, help="RK2 steps per reference run_fixed_steps call")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--dmr-nx", type=int, default=2000, help="DMR channel cells in x (C4 leg; 0 = skip)")
+    ap.add_argument("--dmr-nx", type=int, default=2000, help="DMR channel cells in x (C4 leg)")
+    ap.add_argument("--c3-level", type=int, default=6, help="supersonic-vortex mesh level of the C3 leg")
+    ap.add_argument("--c5-n", type=int, default=2000, help="box cells per side of the C5 leg (2 n^2 triangles)")
+    ap.add_argument("--c5-orders", default="2,3,4")
+    ap.add_argument("--lim-steps", type=int, default=10000, help="steps of the limiter-overhead leg")
+    ap.add_argument("--no-legs", action="store_true", help="headline sweep only (no C3/C4/C5/limiter legs)")
     ap.add_argument("--same-device", action="store_true",
                     help="test mode: all ranks share cuda:0 (partitioned path on one GPU)")
     args = ap.parse_args()

@@ -107,6 +107,11 @@ int dgb_set_stream(dgb_ctx* ctx, void* cuda_stream);
  * asked for by BASELINE.json's north star; oracle/dg2d_oracle.c roe()). */
 enum dgb_flux { DGB_FLUX_LLF = 0, DGB_FLUX_ROE = 1 };
 int dgb_set_flux(dgb_ctx* ctx, int flux);
+/* Limiting runs at p = 1 (whole-mesh contexts): 1 (default; env DGB_FUSED_LIMIT=0 turns it off at
+ * creation) = each RK stage and its limit (solver.cpp:517-535) in ONE persistent launch, the limiter
+ * trailing the stage tile by tile through L2; 0 = a stage kernel followed by a limiter kernel.
+ * Both give bit-identical results. */
+int dgb_set_fused_limiter(dgb_ctx* ctx, int enable);
 /* Replace the Dirichlet table (time-dependent BCs): same layout as dgb_bc_view. */
 int dgb_set_dirichlet(dgb_ctx* ctx, const double* dirichlet_state);
 
@@ -282,6 +287,10 @@ int64_t dgb_launch_count(dgb_ctx* ctx);
 /* Per-step kernel-only timing helper for the benchmark: device ms of the fused
  * stage kernels since the last reset (CUDA events on the context stream). */
 int dgb_stage_kernel_ms(dgb_ctx* ctx, double* ms, int64_t* launches);
+/* The individual device durations (ms) behind the timers since the last dgb_reset_timers, one
+ * per timed launch of `category` (dgb_pass_timers order: 0 volume, 1 surface, 2 rhs,
+ * 3 limiter, 4 other, 5 stage); *n = the count, at most `cap` are copied (benchmark medians). */
+int dgb_timer_samples(dgb_ctx* ctx, int category, double* ms, int64_t cap, int64_t* n);
 
 /* Measured FP64 FMA-pipe throughput of `device` (DFMA loop on every SM), TFLOP/s;
  * the FP64 roofline denominator (MEASURED_PEAKS.json has no FP64 entry). */

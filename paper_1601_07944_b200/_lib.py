@@ -134,6 +134,8 @@ _sig("dgb_enable_timers", C.c_int, _vp, C.c_int)
 _sig("dgb_last_abort", C.c_int, _vp, C.POINTER(AbortInfo))
 _sig("dgb_launch_count", C.c_int64, _vp)
 _sig("dgb_stage_kernel_ms", C.c_int, _vp, c_double_p, c_int64_p)
+_sig("dgb_set_fused_limiter", C.c_int, _vp, C.c_int)
+_sig("dgb_timer_samples", C.c_int, _vp, C.c_int, c_double_p, C.c_int64, c_int64_p)
 _sig("dgb_fp64_peak", C.c_int, C.c_int, c_double_p)
 _sig("dgb_part_create", C.c_int, C.POINTER(MeshView), C.POINTER(TablesView), C.POINTER(BcView),
      C.c_double, C.c_int, C.c_int, C.c_int, C.POINTER(_vp))

@@ -149,6 +149,21 @@ struct StageArgs {
   const PeerTab* peers;
 };
 
+// Fused stage + limiter launch (p = 1 with limiting, kernels_p1.cu k_stage_limit).  Work unit:
+// a tile of 32 elements (one warp).  Warp w of W (a cooperative launch: every warp resident)
+// runs tiles w, w + W, ...: the stage of tile i, published by adding 1 to the counter of its
+// chunk (kFuseChunk tiles), then the limiter of tile i - lag once every chunk holding a
+// neighbour of that tile has published this launch.  Counters only grow: a chunk of s tiles is
+// complete for launch `epoch` (1, 2, ... since the run started) at epoch * s.
+constexpr int kFuseTile = 32;   // elements per tile (one warp)
+constexpr int kFuseChunk = 32;  // tiles per chunk counter
+struct FuseArgs {
+  unsigned long long* count;  // [n_chunks] publications so far (reset at the start of each run)
+  const int2* range;          // [n_tiles] (first, last) chunk holding a neighbour of the tile (own included)
+  int n_tiles, lag;
+  unsigned long long epoch;   // launches of this run so far, this one included
+};
+
 struct LimArgs {
   double* __restrict__ c;         // limited in place
   const double* __restrict__ u;   // for the residual (final limit)

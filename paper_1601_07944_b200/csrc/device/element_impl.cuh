@@ -687,33 +687,20 @@ __device__ __forceinline__ void element_body(const Tab<P>& T, const Geo& geo, co
 // p <= 2 the per-point work (reciprocals, square roots, shuffles) dominates the
 // contractions, so spreading an element over lanes multiplies it; a thread per
 // element evaluates every pointwise quantity exactly once with no exchange.
+// The work of one element (one thread); element_body_g1 grid-strides over it, the fused
+// stage + limiter kernel (kernels_p1.cu) calls it per scheduled tile.
 template <int P, int MODE, int FLUX, int VAR>
-__device__ __forceinline__ void element_body_g1(const Tab<P>& T, const Geo& geo, const StageArgs& a) {
+__device__ __forceinline__ void g1_element(const Tab<P>& T, const Geo& geo, const StageArgs& a, int e, double dt,
+                                           double tstage, double& lam_min, double& res_max) {
   constexpr int NP = Dim<P>::NP, NQ = Dim<P>::NQ, K = Dim<P>::K;
   const long long ld = geo.ld;
-  const int stride = gridDim.x * blockDim.x;
   const double gamma = geo.gamma, g1 = gamma - 1.0;
   Scalars* sc = a.sc;
   // instance variant (kernels_tu.cuh): paths the launch knows are unused compile away
   constexpr bool RK4 = VAR & kVarRk4, LAM = VAR & kVarLambda, BND = VAR & kVarBoundary;
   const int kmode = RK4 ? a.kmode : 0;
   const bool want_lambda = LAM && a.want_lambda;
-
-  __shared__ int s_stop;
-  if (threadIdx.x == 0) s_stop = (sc->err_key != kNoError || sc->halt) ? 1 : 0;
-  __syncthreads();
-  if (s_stop) return;
-
-  double t0 = a.t_host, dt = 0.0;
-  if constexpr (MODE == kModeStage) {
-    if (!stage_prologue(a, sc, t0, dt)) return;
-  }
-  const double tstage = (MODE == kModeStage) ? fma(a.tcoef, dt, t0) : t0;
-
-  double lam_min = __longlong_as_double(0x7ff0000000000000ll);
-  double res_max = 0.0;
-
-  for (int e = a.e0 + blockIdx.x * blockDim.x + threadIdx.x; e < a.e1; e += stride) {
+  {
     double c[4][NP];
 #pragma unroll
     for (int m = 0; m < 4; ++m)
@@ -935,6 +922,31 @@ __device__ __forceinline__ void element_body_g1(const Tab<P>& T, const Geo& geo,
       }
     }
   }
+}
+
+template <int P, int MODE, int FLUX, int VAR>
+__device__ __forceinline__ void element_body_g1(const Tab<P>& T, const Geo& geo, const StageArgs& a) {
+  const int stride = gridDim.x * blockDim.x;
+  Scalars* sc = a.sc;
+  constexpr bool LAM = VAR & kVarLambda;
+  const bool want_lambda = LAM && a.want_lambda;
+
+  __shared__ int s_stop;
+  if (threadIdx.x == 0) s_stop = (sc->err_key != kNoError || sc->halt) ? 1 : 0;
+  __syncthreads();
+  if (s_stop) return;
+
+  double t0 = a.t_host, dt = 0.0;
+  if constexpr (MODE == kModeStage) {
+    if (!stage_prologue(a, sc, t0, dt)) return;
+  }
+  const double tstage = (MODE == kModeStage) ? fma(a.tcoef, dt, t0) : t0;
+
+  double lam_min = __longlong_as_double(0x7ff0000000000000ll);
+  double res_max = 0.0;
+
+  for (int e = a.e0 + blockIdx.x * blockDim.x + threadIdx.x; e < a.e1; e += stride)
+    g1_element<P, MODE, FLUX, VAR>(T, geo, a, e, dt, tstage, lam_min, res_max);
 
   if constexpr (MODE == kModeStage) {
     const int par = a.step & 1;

@@ -7,9 +7,10 @@ namespace dgbk {
 
 namespace {
 __constant__ LimTab c_lim;
+constexpr int kLimNE = 6, kLimNPT = 12;  // p = 1 tables: 2 points per edge, 3 interior
 
 __device__ __forceinline__ double ref_pressure(double rho, double mx, double my, double E, double g1) {
-  return g1 * (E - 0.5 * (mx * mx + my * my) / rho);
+  return g1 * (E - __dmul_rn(0.5, fma(my, my, __dmul_rn(mx, mx))) / rho);
 }
 }  // namespace
 
@@ -26,34 +27,46 @@ namespace {
 #endif
 // EPI: epilogues compiled into the instance (1: CFL bound, 2: residual), the launch passes
 // a.want_lambda / a.want_resid; the intermediate-stage instance carries neither.
-template <int NE, int NPT, int EPI>
-__global__ void __launch_bounds__(kBlock, DGB_LIMIT_MINB) k_limit(Geo geo, LimArgs a) {
+
+// Loads of the limiter's inputs.  The standalone kernel reads its own coefficients through L1
+// and the neighbours' means read-only; inside the fused stage + limiter kernel every read of the
+// stage output must bypass L1 (ld.global.cg): other SMs write it during the same launch, and an
+// L1 sector fetched for one neighbour may hold a not-yet-published element next to it.
+template <bool Coherent>
+__device__ __forceinline__ double lim_ld(const double* p) {
+  if constexpr (Coherent) return __ldcg(p); else return *p;
+}
+template <bool Coherent>
+__device__ __forceinline__ double lim_ldg(const double* p) {
+  if constexpr (Coherent) return __ldcg(p); else return __ldg(p);
+}
+
+// Barth-Jespersen + positivity guard of one element (solver.cpp:286-425), in place on modes
+// 1..2, with the residual and CFL epilogues of the last stage.  Every product-sum is written as
+// an explicit fma / __dmul_rn: left to the compiler, the contraction of e.g. c1 phi1 + c2 phi2
+// differed between kernel instances (measured: the EPI=2 and EPI=3 limiters gave slopes one
+// ulp apart), and the limiter must give the same bits in every instance and launch form.
+template <int NE, int NPT, int EPI, bool Coherent>
+__device__ __forceinline__ void limit_element(const Geo& geo, const LimArgs& a, int e, double& lam_min,
+                                              double& res_max) {
   const bool want_lambda = (EPI & 1) && a.want_lambda, want_resid = (EPI & 2) && a.want_resid;
   constexpr int NP = 3;
   const long long ld = geo.ld;
   const double g1 = geo.gamma - 1.0;
   const double sqrt2 = sqrt(2.0);
   Scalars* sc = a.sc;
-  __shared__ int s_stop;
-  if (threadIdx.x == 0) s_stop = (sc->err_key != kNoError || sc->halt) ? 1 : 0;
-  __syncthreads();
-  if (s_stop) return;
-
   const LimTab& L = c_lim;
   const Tab<1>& T = c_tab;
   const int n_edge = NE ? NE : L.n_edge;
   const int e_begin = NE ? NPT - NE - 3 : L.edge_begin;
   const int n_pts = NPT ? NPT : L.n_pts;
-  double lam_min = __longlong_as_double(0x7ff0000000000000ll);
-  double res_max = 0.0;
-
-  for (int e = a.e0 + blockIdx.x * blockDim.x + threadIdx.x; e < a.e1; e += gridDim.x * blockDim.x) {
+  {
     double c0[4], c1[4], c2[4];
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
-      c0[m] = a.c[(m * NP + 0) * ld + e];
-      c1[m] = a.c[(m * NP + 1) * ld + e];
-      c2[m] = a.c[(m * NP + 2) * ld + e];
+      c0[m] = lim_ld<Coherent>(a.c + (m * NP + 0) * ld + e);
+      c1[m] = lim_ld<Coherent>(a.c + (m * NP + 1) * ld + e);
+      c2[m] = lim_ld<Coherent>(a.c + (m * NP + 2) * ld + e);
     }
     int nb[3];
 #pragma unroll
@@ -74,7 +87,7 @@ __global__ void __launch_bounds__(kBlock, DGB_LIMIT_MINB) k_limit(Geo geo, LimAr
 #pragma unroll
     for (int q = 0; q < 3; ++q)
 #pragma unroll
-      for (int m = 0; m < 4; ++m) nm[q][m] = nb[q] >= 0 ? __ldg(a.c + (m * NP) * ld + nb[q]) : 0.0;
+      for (int m = 0; m < 4; ++m) nm[q][m] = nb[q] >= 0 ? lim_ldg<Coherent>(a.c + (m * NP) * ld + nb[q]) : 0.0;
 #if DGB_LIMIT_CFL_PREFETCH
     if (want_lambda) {
 #pragma unroll
@@ -107,7 +120,7 @@ __global__ void __launch_bounds__(kBlock, DGB_LIMIT_MINB) k_limit(Geo geo, LimAr
       double dpos = 0.0, dneg = 0.0;
 #pragma unroll
       for (int k = e_begin; k < e_begin + n_edge; ++k) {
-        const double d = c1[m] * L.phi1[k] + c2[m] * L.phi2[k];
+        const double d = fma(c2[m], L.phi2[k], __dmul_rn(c1[m], L.phi1[k]));
         dpos = d > dpos ? d : dpos;  // a NaN d is skipped, as by the reference's comparisons
         dneg = d < dneg ? d : dneg;
       }
@@ -126,19 +139,20 @@ __global__ void __launch_bounds__(kBlock, DGB_LIMIT_MINB) k_limit(Geo geo, LimAr
       const double eps_p = 1e-8 * p_mean;
       double dev[4];
 #pragma unroll
-      for (int m = 0; m < 4; ++m) dev[m] = fabs(c1[m]) * L.max_phi1 + fabs(c2[m]) * L.max_phi2;
+      for (int m = 0; m < 4; ++m) dev[m] = fma(fabs(c2[m]), L.max_phi2, __dmul_rn(fabs(c1[m]), L.max_phi1));
       const double rho_floor = mr - dev[0];
       bool safe = rho_floor > eps_rho;
       if (safe) {
         const double mx_peak = fabs(mmx) + dev[1];
         const double my_peak = fabs(mmy) + dev[2];
-        const double p_floor = g1 * (mE - dev[3] - 0.5 * (mx_peak * mx_peak + my_peak * my_peak) / rho_floor);
+        const double p_floor =
+            g1 * ((mE - dev[3]) - __dmul_rn(0.5, fma(my_peak, my_peak, __dmul_rn(mx_peak, mx_peak))) / rho_floor);
         safe = p_floor > eps_p;
       }
       if (!safe) {
         double rho_min = mr;
         for (int k = 0; k < n_pts; ++k)
-          rho_min = fmin(rho_min, c0[0] * sqrt2 + c1[0] * L.phi1[k] + c2[0] * L.phi2[k]);
+          rho_min = fmin(rho_min, fma(c2[0], L.phi2[k], fma(c1[0], L.phi1[k], __dmul_rn(c0[0], sqrt2))));
         if (rho_min < eps_rho) {
           const double th = fmin(fmax((mr - eps_rho) / (mr - rho_min), 0.0), 1.0);
           c1[0] *= th;
@@ -148,7 +162,7 @@ __global__ void __launch_bounds__(kBlock, DGB_LIMIT_MINB) k_limit(Geo geo, LimAr
         for (int k = 0; k < n_pts; ++k) {
           double u[4];
 #pragma unroll
-          for (int m = 0; m < 4; ++m) u[m] = c0[m] * sqrt2 + c1[m] * L.phi1[k] + c2[m] * L.phi2[k];
+          for (int m = 0; m < 4; ++m) u[m] = fma(c2[m], L.phi2[k], fma(c1[m], L.phi1[k], __dmul_rn(c0[m], sqrt2)));
           if (u[0] <= 0.0) {
             th_p = 0.0;
             break;
@@ -211,10 +225,103 @@ __global__ void __launch_bounds__(kBlock, DGB_LIMIT_MINB) k_limit(Geo geo, LimAr
 #endif
     }
   }
+}
+
+template <int NE, int NPT, int EPI>
+__global__ void __launch_bounds__(kBlock, DGB_LIMIT_MINB) k_limit(Geo geo, LimArgs a) {
+  Scalars* sc = a.sc;
+  __shared__ int s_stop;
+  if (threadIdx.x == 0) s_stop = (sc->err_key != kNoError || sc->halt) ? 1 : 0;
+  __syncthreads();
+  if (s_stop) return;
+  double lam_min = __longlong_as_double(0x7ff0000000000000ll);
+  double res_max = 0.0;
+  for (int e = a.e0 + blockIdx.x * blockDim.x + threadIdx.x; e < a.e1; e += gridDim.x * blockDim.x)
+    limit_element<NE, NPT, EPI, false>(geo, a, e, lam_min, res_max);
+  const bool want_lambda = (EPI & 1) && a.want_lambda, want_resid = (EPI & 2) && a.want_resid;
   const int par = a.step & 1;
   if (want_lambda) block_reduce_atomic<true>(lam_min, &sc->dtmin[par ^ 1]);
   if (want_resid) block_reduce_atomic<false>(res_max, &sc->resid[par]);
   if (a.push) __threadfence_system();
+}
+
+constexpr unsigned long long kFuseTimeoutKey = (7ull << 35) | 1ull;  // sorts before every solver error
+
+__device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+#ifndef DGB_FUSE_MINB
+#define DGB_FUSE_MINB 4  // blocks per SM of the fused kernel (the stage body's register budget)
+#endif
+
+// Stage + limiter in one launch.  A cooperative grid of warps, each
+// running a fixed sequence of 32-element tiles (FuseArgs): the stage of tile i (the element
+// kernel's body, no epilogues), published with a release add to its chunk counter, then the
+// limiter of tile j = i - lag once every chunk holding a neighbour of j has published (acquire,
+// one chunk per lane).  The limiter reads the fresh stage output from L2 (ld.global.cg), so the
+// unlimited state never makes an HBM round trip between two kernels, and the limiter's
+// instructions overlap other warps' stage work.  No deadlock: every warp is resident
+// (cooperative launch); a warp in its k-th tile waits only for stage parts of tiles <= i - W
+// (lag >= reach + W), i.e. of other warps' earlier iterations, and a stage part never waits.
+// No early exit once running (an error recorded by another warp of this launch must not make a
+// block skip tiles others wait for): only errors of earlier launches (sequence < a.seq) and the
+// drivers' stop rules, both grid-uniform, end the launch at its start.
+template <int FLUX, int VAR, int EPI>
+__global__ void __launch_bounds__(kBlock, DGB_FUSE_MINB) k_stage_limit(Geo geo, StageArgs a, LimArgs la,
+                                                                      FuseArgs f) {
+  __shared__ int s_stop;
+  Scalars* sc = a.sc;
+  if (threadIdx.x == 0) {
+    const unsigned long long k = sc->err_key;
+    s_stop = ((k != kNoError && (k >> 38) < a.seq) || sc->halt) ? 1 : 0;
+  }
+  __syncthreads();
+  double t0 = a.t_host, dt = 0.0;
+  const bool run = !s_stop && stage_prologue(a, sc, t0, dt);
+  const double tstage = fma(a.tcoef, dt, t0);
+  double lam_min = __longlong_as_double(0x7ff0000000000000ll), res_max = 0.0;
+  double st_lam = lam_min, st_res = 0.0;  // the stage body's epilogues are off (VAR has no kVarLambda)
+  const int lane = threadIdx.x & 31;
+  const int W = gridDim.x * (blockDim.x >> 5);
+  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  bool timed_out = false;
+  if (run) {
+    for (int i = w; i < f.n_tiles + f.lag; i += W) {
+      if (i < f.n_tiles) {
+        const int e = a.e0 + i * kFuseTile + lane;
+        if (e < a.e1) g1_element<1, kModeStage, FLUX, VAR>(c_tab, geo, a, e, dt, tstage, st_lam, st_res);
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) atomicAdd(f.count + i / kFuseChunk, 1ull);  // after the fence: a release
+      }
+      const int j = i - f.lag;
+      if (j >= 0) {
+        const int2 r = __ldg(f.range + j);
+        for (int c = r.x + lane; c <= r.y; c += 32) {
+          const unsigned long long need = f.epoch * min(kFuseChunk, f.n_tiles - c * kFuseChunk);
+          long long spins = 0;
+          while (ld_acquire_gpu(f.count + c) < need) {
+            __nanosleep(64);
+            if (++spins > (1ll << 26)) {  // seconds: a broken launch, never a hang
+              timed_out = true;
+              break;
+            }
+          }
+        }
+        __syncwarp();
+        __threadfence();
+        const int e = la.e0 + j * kFuseTile + lane;
+        if (e < la.e1) limit_element<kLimNE, kLimNPT, EPI, true>(geo, la, e, lam_min, res_max);
+      }
+    }
+  }
+  if (timed_out) record_error(sc, kFuseTimeoutKey);
+  const int par = la.step & 1;
+  if ((EPI & 1) && la.want_lambda) block_reduce_atomic<true>(lam_min, &sc->dtmin[par ^ 1]);
+  if ((EPI & 2) && la.want_resid) block_reduce_atomic<false>(res_max, &sc->resid[par]);
 }
 
 // host copy of (n_edge, n_pts) of the table uploaded to each device's bank (packed in one
@@ -228,13 +335,58 @@ cudaError_t upload_limtab(const LimTab& t, cudaStream_t s) {
   return cudaMemcpyToSymbolAsync(c_lim, &t, sizeof(t), 0, cudaMemcpyHostToDevice, s);
 }
 
-constexpr int kLimNE = 6, kLimNPT = 12;  // p = 1 tables: 2 points per edge, 3 interior
 
 int limit_resident_blocks() {
   static std::atomic<int> occ{0};
   int o = occ.load(std::memory_order_relaxed);
   if (!o) occ.store(o = occupancy(k_limit<kLimNE, kLimNPT, 3>), std::memory_order_relaxed);
   return o;
+}
+
+int stage_limit_grid() {
+  static std::atomic<int> occ{0};
+  int o = occ.load(std::memory_order_relaxed);
+  if (!o) occ.store(o = occupancy(k_stage_limit<kFluxRoe, kVarRk4 | kVarBoundary, 3>), std::memory_order_relaxed);
+  return o * sm_count();
+}
+
+cudaError_t launch_stage_limit(int grid, const Geo& g, const StageArgs& a, const LimArgs& la, const FuseArgs& f,
+                               cudaStream_t s) {
+  if (a.e1 <= a.e0) return cudaSuccess;
+  if (g_lim_pts[current_device()].load() != (kLimNE | (kLimNPT << 16))) return cudaErrorInvalidValue;
+  if (grid <= 0) grid = stage_limit_grid();
+  const int var = (g.has_bnd ? kVarBoundary : 0) | (a.kmode != 0 ? kVarRk4 : 0);
+  const bool last = la.want_lambda || la.want_resid;
+  cudaError_t err = cudaSuccess;
+  auto go = [&](auto k) {  // cooperative: every warp of the grid is resident (the tiles' waits need it)
+    void* args[] = {const_cast<Geo*>(&g), const_cast<StageArgs*>(&a), const_cast<LimArgs*>(&la),
+                    const_cast<FuseArgs*>(&f)};
+    err = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k), dim3(grid), dim3(kBlock), args, 0, s);
+  };
+  if (g.flux == kFluxRoe) {
+    switch (var | (last ? 8 : 0)) {
+      case 0: go(k_stage_limit<kFluxRoe, 0, 0>); break;
+      case 1: go(k_stage_limit<kFluxRoe, 1, 0>); break;
+      case 4: go(k_stage_limit<kFluxRoe, 4, 0>); break;
+      case 5: go(k_stage_limit<kFluxRoe, 5, 0>); break;
+      case 8: go(k_stage_limit<kFluxRoe, 0, 3>); break;
+      case 9: go(k_stage_limit<kFluxRoe, 1, 3>); break;
+      case 12: go(k_stage_limit<kFluxRoe, 4, 3>); break;
+      default: go(k_stage_limit<kFluxRoe, 5, 3>); break;
+    }
+  } else {
+    switch (var | (last ? 8 : 0)) {
+      case 0: go(k_stage_limit<kFluxLLF, 0, 0>); break;
+      case 1: go(k_stage_limit<kFluxLLF, 1, 0>); break;
+      case 4: go(k_stage_limit<kFluxLLF, 4, 0>); break;
+      case 5: go(k_stage_limit<kFluxLLF, 5, 0>); break;
+      case 8: go(k_stage_limit<kFluxLLF, 0, 3>); break;
+      case 9: go(k_stage_limit<kFluxLLF, 1, 3>); break;
+      case 12: go(k_stage_limit<kFluxLLF, 4, 3>); break;
+      default: go(k_stage_limit<kFluxLLF, 5, 3>); break;
+    }
+  }
+  return err;
 }
 
 cudaError_t launch_limit(int grid, const Geo& g, const LimArgs& a, cudaStream_t s) {

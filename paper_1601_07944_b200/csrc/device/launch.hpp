@@ -26,5 +26,10 @@ struct Launch {
 cudaError_t upload_limtab(const LimTab& t, cudaStream_t s);
 cudaError_t launch_limit(int grid, const Geo& g, const LimArgs& a, cudaStream_t s);
 int limit_resident_blocks();
+// Stage + limiter in one persistent launch (p = 1, whole-mesh contexts); grid <= 0: one
+// wave of resident blocks, stage_limit_grid() (FuseArgs::lag counts it).
+int stage_limit_grid();
+cudaError_t launch_stage_limit(int grid, const Geo& g, const StageArgs& a, const LimArgs& la, const FuseArgs& f,
+                               cudaStream_t s);
 
 }  // namespace dgbk

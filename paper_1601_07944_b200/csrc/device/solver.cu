@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -377,6 +378,16 @@ struct dgb_ctx {
   int64_t launches = 0;
   double stage_ms = 0.0;
   int64_t stage_launches = 0;
+  std::vector<double> samples[6];  // per-launch device ms of each timer category since the last reset
+
+  // fused stage + limiter (p = 1, whole mesh; kernels_p1.cu k_stage_limit)
+  bool fuse_limit = true;
+  std::vector<int2> fz_range_h;  // per 32-element tile: first and last chunk holding a neighbour
+  int fz_maxreach = 0;           // max over tiles of (last tile waited for - tile)
+  DevBuf<unsigned long long> fz_count;
+  DevBuf<int2> fz_range;
+  int fz_grid = 0, fz_lag = 0;
+  unsigned long long fz_epoch = 0;  // fused launches of the current run
 
   dgbk::Tab<1> tab1;
   dgbk::Tab<2> tab2;
@@ -447,6 +458,7 @@ void settle_timers(dgb_ctx* c) {
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, pd.a, pd.b) == cudaSuccess) {
       const double s = ms * 1e-3;
+      if (pd.cat >= 0 && pd.cat < 6) c->samples[pd.cat].push_back(ms);
       switch (pd.cat) {
         case 0: c->timers.volume += s; break;
         case 1: c->timers.surface += s; break;
@@ -647,7 +659,9 @@ std::string failure_message(dgb_ctx* c, unsigned long long key, const double* de
   const int pass = static_cast<int>((key >> 35) & 7);
   const long long id = static_cast<long long>((key >> 5) & 0x3fffffff);
   const int point = static_cast<int>(key & 31);
-  if (pass == 7) return "halo exchange timed out (a peer rank stopped signalling)";
+  if (pass == 7)
+    return (key & 31) == 1 ? "fused stage + limiter launch: a tile wait timed out"
+                            : "halo exchange timed out (a peer rank stopped signalling)";
   std::vector<double> h(static_cast<size_t>(4) * c->np * c->N);
   download_dev(c, dev_in, 4 * c->np, h.data());
   // the download holds the owned elements only (compact index = reference id - lo)
@@ -826,6 +840,25 @@ RunOut run_steps(dgb_ctx* c, const RunSpec& r) {
   }
   const bool X = exchanging(c);
   const unsigned ALL = X ? all_peers(c) : 0u;
+  // the fused stage + limiter launch (whole-mesh contexts; a partition keeps the two-kernel
+  // path, whose halo rounds it needs)
+  const bool fused = r.limiting && !c->partitioned && c->fuse_limit && c->p == 1;
+  if (fused) {
+    const int nt = static_cast<int>(c->fz_range_h.size());
+    const int nch = (nt + dgbk::kFuseChunk - 1) / dgbk::kFuseChunk;
+    if (!c->fz_range.p) {
+      c->fz_range.upload(c->fz_range_h.data(), nt, c->stream);
+      c->fz_count.alloc(nch);
+      // one warp per tile, every warp resident (cooperative launch): no more warps than tiles
+      const int warps_per_block = dgbk::kBlock / 32;
+      c->fz_grid = std::min(dgbk::stage_limit_grid(), (nt + warps_per_block - 1) / warps_per_block);
+      if (const char* g = std::getenv("DGB_FUSE_GRID")) c->fz_grid = std::max(1, std::min(c->fz_grid, std::atoi(g)));
+      c->fz_lag = c->fz_maxreach + c->fz_grid * warps_per_block;
+    }
+    // chunk counters count this run's publications: zero them, restart the epochs
+    CU(cudaMemsetAsync(c->fz_count.p, 0, nch * sizeof(unsigned long long), c->stream));
+    c->fz_epoch = 0;
+  }
   // interior elements [0, n_int) never read a halo column; boundary elements
   // [n_int, N) do, and only they feed the peers
   const int n_int = X ? c->n_int : c->N;
@@ -885,6 +918,27 @@ RunOut run_steps(dgb_ctx* c, const RunSpec& r) {
         // step start: merge the previous step's scalars (dt bound, residual, error) from every rank
         if (X && k == 0) xch_wait(c, ALL, c->pub_epoch, true, par, par ^ 1);
         const unsigned long long prev = c->epoch;
+        if (fused) {  // stage + limiter in one launch
+          LimArgs la{};
+          la.c = a.out;
+          la.u = u;
+          la.step = static_cast<int>(s);
+          la.want_lambda = last && r.dt_mode == 1;
+          la.want_resid = last;
+          la.seq = static_cast<unsigned long long>(s + 1) * 8;
+          la.sc = c->d_sc;
+          la.e0 = 0;
+          la.e1 = c->N;
+          a.e0 = 0;
+          a.e1 = c->N;
+          dgbk::FuseArgs f{c->fz_count.p, c->fz_range.p, static_cast<int>(c->fz_range_h.size()), c->fz_lag,
+                           ++c->fz_epoch};
+          Timed tm(c, 5);
+          CU(dgbk::launch_stage_limit(c->fz_grid, c->geo, a, la, f, c->stream));
+          ++c->launches;
+          ++c->stage_launches;
+          continue;
+        }
         {
           Timed tm(c, 5);
           a.e0 = 0;
@@ -1175,6 +1229,27 @@ int dgb_part_create(const dgb_mesh_view* m, const dgb_tables_view* t, const dgb_
       cmp[N + h] = N + h;
     }
     c->sends.assign(world, {});
+    {  // neighbour chunk ranges for the fused stage + limiter launch (whole-mesh contexts)
+      constexpr int TL = dgbk::kFuseTile, CH = dgbk::kFuseChunk;
+      const int nt = (N + TL - 1) / TL;
+      c->fz_range_h.assign(nt, make_int2(0, 0));
+      c->fz_maxreach = 0;
+      for (int t = 0; t < nt; ++t) {
+        int lo_c = t / CH, hi_c = t / CH;
+        for (int d = t * TL; d < std::min(N, (t + 1) * TL); ++d)
+          for (int q = 0; q < 3; ++q) {
+            const int nbd = nbr[static_cast<size_t>(q) * ld + d];
+            if (nbd < 0 || nbd >= N) continue;
+            lo_c = std::min(lo_c, nbd / TL / CH);
+            hi_c = std::max(hi_c, nbd / TL / CH);
+          }
+        c->fz_range_h[t] = make_int2(lo_c, hi_c);
+        // the last tile the limiter of t waits for
+        c->fz_maxreach = std::max(c->fz_maxreach, std::min(nt - 1, (hi_c + 1) * CH - 1) - t);
+      }
+      const char* env = std::getenv("DGB_FUSED_LIMIT");
+      c->fuse_limit = !(env && env[0] == '0');
+    }
     c->d_tau.upload(tau.data(), tau.size(), c->stream);
     c->d_inv_det.upload(inv_det.data(), ld, c->stream);
     c->d_inradius.upload(inr.data(), ld, c->stream);
@@ -1387,6 +1462,12 @@ int dgb_set_flux(dgb_ctx* c, int flux) {
     return DGB_ERR_ARG;
   }
   c->geo.flux = flux;
+  return DGB_OK;
+}
+
+int dgb_set_fused_limiter(dgb_ctx* c, int enable) {
+  if (!c) return DGB_ERR_ARG;
+  c->fuse_limit = enable != 0;
   return DGB_OK;
 }
 
@@ -1872,6 +1953,7 @@ int dgb_reset_timers(dgb_ctx* c) {
     c->timers = dgb_pass_timers{};
     c->stage_ms = 0.0;
     c->stage_launches = 0;
+    for (auto& v : c->samples) v.clear();
     return DGB_OK;
   });
 }
@@ -2104,6 +2186,18 @@ int dgb_part_set_timeout(dgb_ctx* c, double seconds) {
   if (!c || !(seconds > 0)) return DGB_ERR_ARG;
   c->timeout_s = seconds;
   return DGB_OK;
+}
+
+int dgb_timer_samples(dgb_ctx* c, int category, double* ms, int64_t cap, int64_t* n) {
+  return guarded([&] {
+    if (category < 0 || category > 5) throw Fail{DGB_ERR_ARG, "timer category must be in [0,5]"};
+    set_device(c);
+    sync(c);
+    const std::vector<double>& v = c->samples[category];
+    if (n) *n = static_cast<int64_t>(v.size());
+    if (ms) std::copy(v.begin(), v.begin() + std::min<int64_t>(cap, static_cast<int64_t>(v.size())), ms);
+    return DGB_OK;
+  });
 }
 
 int dgb_stage_kernel_ms(dgb_ctx* c, double* ms, int64_t* launches) {

@@ -523,3 +523,27 @@ def test_async_copies_pipeline_bitwise_equal_to_synchronous():
     for out, w in zip(outs, want):
         assert np.array_equal(out.numpy().reshape(w.shape), w)
     ctx.close()
+
+
+@pytest.mark.parametrize("scheme,flux,nx", [(2, "llf", 200), (4, "llf", 120), (103, "llf", 200), (102, "roe", 120),
+                                            (2, "llf", 2000)])
+def test_fused_stage_limiter_bitwise_equal_to_two_kernels(scheme, flux, nx):
+    """The fused stage + limiter launch (k_stage_limit: tiles taken from a counter, the limiter
+    trailing through L2 behind published tiles) is bit-identical to the stage kernel followed by
+    the limiter kernel, for every scheme, both fluxes, and at the C4 size (2000 x 500)."""
+    mesh = dg2d.generate_mesh(L.MESH_DOUBLE_MACH, nx, nx // 4, 1.0 / 6.0)
+    tb = dg2d.build_tables(1)
+    setup = dg2d.DoubleMachSetup()
+    bc = dg2d.double_mach_boundary(setup)
+    opts = dg2d.SolverOptions(scheme=scheme, cfl=0.3, limiting=True, flux=flux)
+    out = []
+    for fused in (1, 0):
+        ctx = dg2d.SolverContext(mesh, tb, bc=bc, options=opts)
+        assert L.lib.dgb_set_fused_limiter(ctx.handle, fused) == 0
+        c0 = dg2d.limit(ctx, dg2d.project_initial(lambda xy: dg2d.double_mach_initial(xy, setup), mesh, tb))
+        st = dg2d.SolverState(c0)
+        res = dg2d.run_fixed_steps(ctx, st, 30 if nx < 1000 else 10)
+        out.append((st.coeffs, st.t, res))
+        ctx.close()
+    assert np.array_equal(out[0][0], out[1][0])
+    assert out[0][1] == out[1][1] and out[0][2] == out[1][2]
