@@ -107,11 +107,17 @@ int dgb_set_stream(dgb_ctx* ctx, void* cuda_stream);
  * asked for by BASELINE.json's north star; oracle/dg2d_oracle.c roe()). */
 enum dgb_flux { DGB_FLUX_LLF = 0, DGB_FLUX_ROE = 1 };
 int dgb_set_flux(dgb_ctx* ctx, int flux);
-/* Limiting runs at p = 1 (whole-mesh contexts): 1 (default; env DGB_FUSED_LIMIT=0 turns it off at
- * creation) = each RK stage and its limit (solver.cpp:517-535) in ONE persistent launch, the limiter
- * trailing the stage tile by tile through L2; 0 = a stage kernel followed by a limiter kernel.
- * Both give bit-identical results. */
+/* Limiting runs at p = 1 (whole-mesh contexts): 1 = each RK stage and its limit (solver.cpp:517-535)
+ * in ONE persistent launch, the limiter trailing the stage tile by tile through L2; 0 = a stage
+ * kernel followed by a limiter kernel; -1 (default; env DGB_FUSED_LIMIT=0/1 fixes it at creation) =
+ * the fused launch on meshes up to 400K triangles, where it saves a launch per stage, the two
+ * kernels above (measured).  All give bit-identical results. */
 int dgb_set_fused_limiter(dgb_ctx* ctx, int enable);
+/* Launch forms for small meshes (no reference counterpart: the CPU has no launch shape).  A p <= 2
+ * stage launch of at most stage_max_n elements, and a limiter launch of at most limit_max_n, take
+ * the four-lanes-per-element latency form instead of one thread per element; -1 = the built-in
+ * size (env DGB_G4_MAXN / DGB_LIM4_MAXN), 0 = never.  Both forms give bit-identical results. */
+int dgb_set_latency_forms(dgb_ctx* ctx, int stage_max_n, int limit_max_n);
 /* Replace the Dirichlet table (time-dependent BCs): same layout as dgb_bc_view. */
 int dgb_set_dirichlet(dgb_ctx* ctx, const double* dirichlet_state);
 

@@ -86,6 +86,8 @@ _vp = C.c_void_p
 
 
 def _sig(name, res, *args):
+    if os.environ.get("DGB_LIB") and not hasattr(lib, name):
+        return None  # an older tuning build (A/B timing) may lack the newest entry points
     f = getattr(lib, name)
     f.restype = res
     f.argtypes = list(args)
@@ -135,6 +137,7 @@ _sig("dgb_last_abort", C.c_int, _vp, C.POINTER(AbortInfo))
 _sig("dgb_launch_count", C.c_int64, _vp)
 _sig("dgb_stage_kernel_ms", C.c_int, _vp, c_double_p, c_int64_p)
 _sig("dgb_set_fused_limiter", C.c_int, _vp, C.c_int)
+_sig("dgb_set_latency_forms", C.c_int, _vp, C.c_int, C.c_int)
 _sig("dgb_timer_samples", C.c_int, _vp, C.c_int, c_double_p, C.c_int64, c_int64_p)
 _sig("dgb_fp64_peak", C.c_int, C.c_int, c_double_p)
 _sig("dgb_part_create", C.c_int, C.POINTER(MeshView), C.POINTER(TablesView), C.POINTER(BcView),

@@ -109,6 +109,9 @@ struct Geo {
   // basis tables in DMMA fragment order (element_mma.cuh), p >= 3
   const double* __restrict__ mma_tab;
   int flux;  // numerical flux: 0 local Lax-Friedrichs (euler.hpp:59-71), 1 Roe
+  // launch forms (kernels_tu.cuh, kernels_p1.cu): launches of at most this many elements take
+  // the four-lane latency form of the p <= 2 stage kernel / the limiter; -1 = the built-in size
+  int lat_stage_n, lat_limit_n;
 };
 
 // Modes of the fused element kernel.

@@ -66,11 +66,13 @@ __device__ __forceinline__ double rcp_nr(double x) {
   return fma(r, e, r);
 }
 
+// One Newton step on the 2^-20 MUFU seed (2^-40), then the square-root correction s + (a - s^2)
+// y / 2 (2^-80 before rounding): equal to IEEE sqrt on all 1.2e9 log-uniform samples in
+// [1e-6, 1e6] (tools/micro/mufu_prec.cu, profiles/r02_mufu_prec.txt), as was the two-step form.
 __device__ __forceinline__ double sqrt_nr(double a) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
   const double h = 0.5 * a;
-  y = y * fma(-h * y, y, 1.5);
   y = y * fma(-h * y, y, 1.5);
   const double s = a * y;
   return fma(0.5 * y, fma(-s, s, a), s);
@@ -195,6 +197,32 @@ __device__ __forceinline__ void num_flux(const double (&UL)[4], const Prim& wl, 
     llf_flux(UL, wl, UR, wr, nx, ny, gamma, fn);
 }
 
+// The numerical flux times a signed quadrature weight w (-h w_k on the edge's left element, +h w_k
+// on its right one).  LLF folds w into its two coefficients, cf = (w/2)(F(U_L).n + F(U_R).n) -
+// (w hs)(U_R - U_L): 18 FP64 operations instead of 20 and no sign selects.  Exactly antisymmetric
+// in the sign of w (IEEE negation commutes with products and fma), so the two elements of an edge
+// still receive bitwise-opposite contributions.  Roe: w f.
+template <int FLUX>
+__device__ __forceinline__ void num_flux_w(const double (&UL)[4], const Prim& wl, const double (&UR)[4],
+                                           const Prim& wr, double nx, double ny, double gamma, double w,
+                                           double (&cf)[4]) {
+  if constexpr (FLUX == kFluxRoe) {
+    double f[4];
+    roe_flux(UL, wl, UR, wr, nx, ny, gamma, f);
+#pragma unroll
+    for (int m = 0; m < 4; ++m) cf[m] = w * f[m];
+  } else {
+    double fl[4], fr[4], vnl, vnr;
+    normal_flux(UL, wl, nx, ny, vnl, fl);
+    normal_flux(UR, wr, nx, ny, vnr, fr);
+    const double sl = fabs(vnl) + sqrt_nr(gamma * wl.p * wl.inv);
+    const double sr = fabs(vnr) + sqrt_nr(gamma * wr.p * wr.inv);
+    const double a = 0.5 * w, b = (0.5 * std_max(sl, sr)) * w;  // std::max as euler.hpp:64
+#pragma unroll
+    for (int m = 0; m < 4; ++m) cf[m] = fma(-b, UR[m] - UL[m], a * (fl[m] + fr[m]));
+  }
+}
+
 __device__ __forceinline__ void reflect(const double (&u)[4], double nx, double ny, double (&g)[4]) {
   const double mn = 2.0 * (u[1] * nx + u[2] * ny);
   g[0] = u[0];
@@ -275,6 +303,58 @@ __device__ __forceinline__ void block_reduce_atomic(double v, unsigned long long
   __syncthreads();
 }
 
+// cp.async of one double into shared memory (zero-filled when !pred); lane-private
+// destinations, so the issuing lane's wait_group is the only synchronisation needed.
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool pred) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sa), "l"(src), "r"(pred ? 8 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Cross-element software pipeline of the one-thread kernel (g1_element with PF): each thread
+// owns shared-memory rows, row r at base[r * stride] (stride = blockDim.x: consecutive threads
+// hit consecutive words, no bank conflicts).  Rows [0, 4NP) hold the element's own coefficient
+// column, rows [4NP (1 + q), 4NP (2 + q)) the neighbour column of side q.  While element e is
+// evaluated, the column of the thread's next element and, side by side as the slots free up,
+// its neighbours' columns are in flight (cp.async, one commit group per slot, so every wait is
+// wait_group 3: the slot needed now is the fourth-newest group).
+struct G1Pipe {
+  double* base;
+  int stride;
+  int e_next;     // next element of this thread (>= a.e1: none)
+  int nb_next[3]; // its neighbours (BC code < 0: none)
+};
+template <int NP>
+__device__ __forceinline__ void g1_fetch_col(const G1Pipe& pp, int slot, const double* __restrict__ in, long long ld,
+                                             int col, bool ok) {
+#pragma unroll
+  for (int r = 0; r < 4 * NP; ++r)
+    cp_async8(pp.base + (slot * 4 * NP + r) * pp.stride, ok ? in + static_cast<long long>(r) * ld + col : in, ok);
+  cp_async_commit();
+}
+
+// neighbour_trace from the pipeline's shared-memory column (same FMA chain: bit-identical)
+template <int P, int S>
+__device__ __forceinline__ void neighbour_trace_s(const Tab<P>& T, const double* __restrict__ col, int stride,
+                                                  double (&un)[Dim<P>::K][4]) {
+  constexpr int NP = Dim<P>::NP, K = Dim<P>::K;
+#pragma unroll
+  for (int j = 0; j < NP; ++j) {
+#pragma unroll
+    for (int mm = 0; mm < 4; ++mm) {
+      const double cn = col[(mm * NP + j) * stride];
+      const double p0 = T.phe[S][0][0] * cn;  // the mode-0 basis value is the same at every point
+#pragma unroll
+      for (int ko = 0; ko < K; ++ko) {
+        const double ph = T.phe[S][K - 1 - ko][j];
+        un[ko][mm] = (j == 0) ? p0 : fma(ph, cn, un[ko][mm]);
+      }
+    }
+  }
+}
+
 // Trace of the neighbour's coefficients on its side S at the reversed points,
 // streamed from global memory (the neighbour's column is an L1/L2 hit).  The
 // FMA chain is the same as the one the neighbour uses for its own trace, so
@@ -288,10 +368,13 @@ __device__ __forceinline__ void neighbour_trace(const Tab<P>& T, const double* _
 #pragma unroll
     for (int mm = 0; mm < MG; ++mm) {
       const double cn = __ldg(in + (static_cast<long long>(m0 + mm) * NP + j) * ld + nb);
+      // the mode-0 basis value is the same double at every point (a constant function): one
+      // product serves all K points, bit-identical to the per-point product
+      const double p0 = T.phe[S][0][0] * cn;
 #pragma unroll
       for (int ko = 0; ko < K; ++ko) {
         const double ph = T.phe[S][K - 1 - ko][j];
-        un[ko][mm] = (j == 0) ? ph * cn : fma(ph, cn, un[ko][mm]);
+        un[ko][mm] = (j == 0) ? p0 : fma(ph, cn, un[ko][mm]);
       }
     }
   }
@@ -369,6 +452,24 @@ __device__ __forceinline__ double ld_nc(const double* p) {
   double r;
   asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(r) : "l"(p));
   return r;
+}
+#ifndef DGB_G1_HOIST_MAXP
+#define DGB_G1_HOIST_MAXP 2  // one-thread kernel: mode-0 products formed once per variable (not per point)
+#endif
+#ifndef DGB_G1_PF_MAXP
+#define DGB_G1_PF_MAXP 0  // one-thread kernel degrees with the cross-element pipeline (G1Pipe); measured at p=1:
+                          // 0.161 vs 0.127 ms per stage (spills, L1 reduced to 64 KB): off
+#endif
+// Whether element_body_g1 runs the cross-element shared-memory pipeline (every mode that
+// reads neighbour columns: the volume mode has no side loop to keep the group count).
+template <int P, int MODE>
+struct G1Prefetch {
+  static constexpr bool value = P <= DGB_G1_PF_MAXP && MODE != kModeVolume;
+};
+// shared memory of the pipeline per thread (bytes): own column + three neighbour columns
+template <int P>
+constexpr int g1_pipe_bytes() {
+  return G1Prefetch<P, kModeStage>::value ? 4 * 4 * Dim<P>::NP * 8 : 0;
 }
 // Degrees up to DGB_G1_MAXP use one thread per element, higher ones four lanes.
 template <int P>
@@ -575,17 +676,15 @@ __device__ __forceinline__ void element_body(const Tab<P>& T, const Geo& geo, co
           const int kc = left ? ko : K - 1 - ko;  // canonical (left-element) point index
           if (BND && bnd) ghost_state<K>(UL, nb, ed, kc, nx, ny, tstage, geo, UR);
           const Prim wl = primitives(UL, g1), wr = primitives(UR, g1);
+          const double wl_ = h * pick_weight<K>(T.we, kc);
           double fn[4];
           if (admissible(UL, wl) && admissible(UR, wr)) {
-            num_flux<FLUX>(UL, wl, UR, wr, nx, ny, gamma, fn);
+            num_flux_w<FLUX>(UL, wl, UR, wr, nx, ny, gamma, left ? -wl_ : wl_, fn);
           } else {
             if (valid && g < nk) record_error(sc, err_key(a.seq, kPassSurface, ed, kc));
 #pragma unroll
             for (int m = 0; m < 4; ++m) fn[m] = 0.0;
           }
-          const double wl_ = h * pick_weight<K>(T.we, kc);
-#pragma unroll
-          for (int m = 0; m < 4; ++m) fn[m] = left ? -(wl_ * fn[m]) : (wl_ * fn[m]);
           transpose4(fn, g);  // lane g: weighted flux of variable g at points k0..k0+3
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
@@ -689,9 +788,10 @@ __device__ __forceinline__ void element_body(const Tab<P>& T, const Geo& geo, co
 // element evaluates every pointwise quantity exactly once with no exchange.
 // The work of one element (one thread); element_body_g1 grid-strides over it, the fused
 // stage + limiter kernel (kernels_p1.cu) calls it per scheduled tile.
-template <int P, int MODE, int FLUX, int VAR>
+template <int P, int MODE, int FLUX, int VAR, bool PF = false>
 __device__ __forceinline__ void g1_element(const Tab<P>& T, const Geo& geo, const StageArgs& a, int e, double dt,
-                                           double tstage, double& lam_min, double& res_max) {
+                                           double tstage, double& lam_min, double& res_max,
+                                           const G1Pipe* pipe = nullptr) {
   constexpr int NP = Dim<P>::NP, NQ = Dim<P>::NQ, K = Dim<P>::K;
   const long long ld = geo.ld;
   const double gamma = geo.gamma, g1 = gamma - 1.0;
@@ -700,12 +800,22 @@ __device__ __forceinline__ void g1_element(const Tab<P>& T, const Geo& geo, cons
   constexpr bool RK4 = VAR & kVarRk4, LAM = VAR & kVarLambda, BND = VAR & kVarBoundary;
   const int kmode = RK4 ? a.kmode : 0;
   const bool want_lambda = LAM && a.want_lambda;
+  constexpr bool kHoist0 = P <= DGB_G1_HOIST_MAXP;
   {
     double c[4][NP];
+    if constexpr (PF) {
+      cp_async_wait<3>();  // this element's column (issued during the previous element)
 #pragma unroll
-    for (int m = 0; m < 4; ++m)
+      for (int m = 0; m < 4; ++m)
 #pragma unroll
-      for (int j = 0; j < NP; ++j) c[m][j] = __ldg(a.in + (static_cast<long long>(m) * NP + j) * ld + e);
+        for (int j = 0; j < NP; ++j) c[m][j] = pipe->base[(m * NP + j) * pipe->stride];
+      g1_fetch_col<NP>(*pipe, 0, a.in, ld, pipe->e_next, pipe->e_next < a.e1);
+    } else {
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int j = 0; j < NP; ++j) c[m][j] = __ldg(a.in + (static_cast<long long>(m) * NP + j) * ld + e);
+    }
     double acc[4][NP];
 #pragma unroll
     for (int m = 0; m < 4; ++m)
@@ -725,6 +835,11 @@ __device__ __forceinline__ void g1_element(const Tab<P>& T, const Geo& geo, cons
     }
 #endif
 
+    // mode-0 products of the interpolations and own traces (the mode-0 basis function is a
+    // constant: every table holds the same double in column 0), formed once per variable
+    double c0p[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) c0p[m] = kHoist0 ? T.phi[0][0] * c[m][0] : 0.0;
     // ------------------------------------------------------------ volume
     if constexpr (MODE != kModeSurface) {
       const double ta = __ldg(geo.tau + e), tb = __ldg(geo.tau + ld + e);
@@ -734,7 +849,7 @@ __device__ __forceinline__ void g1_element(const Tab<P>& T, const Geo& geo, cons
         double U[4];
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
-          double s = T.phi[k][0] * c[m][0];
+          double s = kHoist0 ? c0p[m] : T.phi[k][0] * c[m][0];  // the same product at every point
 #pragma unroll
           for (int j = 1; j < NP; ++j) s = fma(T.phi[k][j], c[m][j], s);
           U[m] = s;
@@ -775,13 +890,26 @@ __device__ __forceinline__ void g1_element(const Tab<P>& T, const Geo& geo, cons
         const double nx = __ldg(geo.enx + ed), ny = __ldg(geo.eny + ed), h = __ldg(geo.eh + ed);
         const bool bnd = nb < 0;
         double un[K][4];
-        if (!bnd) {
+        if constexpr (PF) {
+          cp_async_wait<3>();  // side q's neighbour column
+          const double* col = pipe->base + (q + 1) * 4 * NP * pipe->stride;
+          if (!bnd) {
+            switch (snb) {
+              case 1: neighbour_trace_s<P, 0>(T, col, pipe->stride, un); break;
+              case 2: neighbour_trace_s<P, 1>(T, col, pipe->stride, un); break;
+              default: neighbour_trace_s<P, 2>(T, col, pipe->stride, un); break;
+            }
+          }
+          const int nbn = q == 0 ? pipe->nb_next[0] : (q == 1 ? pipe->nb_next[1] : pipe->nb_next[2]);
+          g1_fetch_col<NP>(*pipe, q + 1, a.in, ld, nbn, pipe->e_next < a.e1 && nbn >= 0);
+        } else if (!bnd) {
           switch (snb) {
             case 1: neighbour_trace<P, 0, 4>(T, a.in, ld, 0, nb, un); break;
             case 2: neighbour_trace<P, 1, 4>(T, a.in, ld, 0, nb, un); break;
             default: neighbour_trace<P, 2, 4>(T, a.in, ld, 0, nb, un); break;
           }
-        } else {
+        }
+        if (bnd) {
 #pragma unroll
           for (int ko = 0; ko < K; ++ko)
 #pragma unroll
@@ -805,9 +933,14 @@ __device__ __forceinline__ void g1_element(const Tab<P>& T, const Geo& geo, cons
           for (int j = 0; j < NP; ++j) {
             const double cj = ld_nc(a.in + (static_cast<long long>(m) * NP + j) * ld + e);
 #pragma unroll
-            for (int ko = 0; ko < K; ++ko) uoa[ko][m] = j == 0 ? phq[ko * NP] * cj : fma(phq[ko * NP + j], cj, uoa[ko][m]);
+            const double cj0 = phq[0] * cj;  // the mode-0 product, the same at every point
+#pragma unroll
+            for (int ko = 0; ko < K; ++ko) uoa[ko][m] = j == 0 ? cj0 : fma(phq[ko * NP + j], cj, uoa[ko][m]);
           }
         }
+        double c0q[4];  // mode-0 products of the own trace, once per side (not kept across the loop)
+#pragma unroll
+        for (int m = 0; m < 4; ++m) c0q[m] = (kReload || !kHoist0) ? 0.0 : phq[0] * c[m][0];
 #pragma unroll
         for (int ko = 0; ko < K; ++ko) {
           double uo[4];
@@ -816,7 +949,7 @@ __device__ __forceinline__ void g1_element(const Tab<P>& T, const Geo& geo, cons
             if constexpr (kReload) {
               uo[m] = uoa[ko][m];
             } else {
-              double s = phq[ko * NP] * c[m][0];
+              double s = kHoist0 ? c0q[m] : phq[ko * NP] * c[m][0];
 #pragma unroll
               for (int j = 1; j < NP; ++j) s = fma(phq[ko * NP + j], c[m][j], s);
               uo[m] = s;
@@ -831,20 +964,19 @@ __device__ __forceinline__ void g1_element(const Tab<P>& T, const Geo& geo, cons
           const int kc = left ? ko : K - 1 - ko;
           if (BND && bnd) ghost_state<K>(UL, nb, ed, kc, nx, ny, tstage, geo, UR);
           const Prim wl = primitives(UL, g1), wr = primitives(UR, g1);
-          double fn[4];
+          const double wl_ = h * pick_weight<K>(T.we, kc);
+          double cf[4];
           if (admissible(UL, wl) && admissible(UR, wr)) {
-            num_flux<FLUX>(UL, wl, UR, wr, nx, ny, gamma, fn);
+            num_flux_w<FLUX>(UL, wl, UR, wr, nx, ny, gamma, left ? -wl_ : wl_, cf);
           } else {
             record_error(sc, err_key(a.seq, kPassSurface, ed, kc));
 #pragma unroll
-            for (int m = 0; m < 4; ++m) fn[m] = 0.0;
+            for (int m = 0; m < 4; ++m) cf[m] = 0.0;
           }
-          const double wl_ = h * pick_weight<K>(T.we, kc);
 #pragma unroll
           for (int m = 0; m < 4; ++m) {
-            const double cf = left ? -(wl_ * fn[m]) : (wl_ * fn[m]);
 #pragma unroll
-            for (int j = 0; j < NP; ++j) acc[m][j] = fma(cf, phq[ko * NP + j], acc[m][j]);
+            for (int j = 0; j < NP; ++j) acc[m][j] = fma(cf[m], phq[ko * NP + j], acc[m][j]);
           }
         }
         if constexpr (MODE == kModeSurface) {
@@ -899,12 +1031,15 @@ __device__ __forceinline__ void g1_element(const Tab<P>& T, const Geo& geo, cons
       if (a.push && e >= geo.send_begin) push_element<NP, 4>(geo, a.peers, a.out_buf, e, 0, acc);
       if (want_lambda) {
         double lam = 0.0;
+        double a0[4];  // mode-0 products of the midpoint states (the same at the three midpoints)
+#pragma unroll
+        for (int m = 0; m < 4; ++m) a0[m] = T.phm[0][0] * acc[m][0];
 #pragma unroll 1
         for (int q = 0; q < 3; ++q) {
           double U[4];
 #pragma unroll
           for (int m = 0; m < 4; ++m) {
-            double s = T.phm[q][0] * acc[m][0];
+            double s = a0[m];
 #pragma unroll
             for (int j = 1; j < NP; ++j) s = fma(T.phm[q][j], acc[m][j], s);
             U[m] = s;
@@ -945,8 +1080,33 @@ __device__ __forceinline__ void element_body_g1(const Tab<P>& T, const Geo& geo,
   double lam_min = __longlong_as_double(0x7ff0000000000000ll);
   double res_max = 0.0;
 
-  for (int e = a.e0 + blockIdx.x * blockDim.x + threadIdx.x; e < a.e1; e += stride)
-    g1_element<P, MODE, FLUX, VAR>(T, geo, a, e, dt, tstage, lam_min, res_max);
+  if constexpr (G1Prefetch<P, MODE>::value) {
+    // cross-element pipeline (G1Pipe): the first element's columns, then one element ahead
+    extern __shared__ double pfbuf[];
+    G1Pipe pp;
+    pp.base = pfbuf + threadIdx.x;
+    pp.stride = blockDim.x;
+    const long long ld = geo.ld;
+    constexpr int NP = Dim<P>::NP;
+    int e = a.e0 + blockIdx.x * blockDim.x + threadIdx.x;
+    const bool ok = e < a.e1;
+    int nb[3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) nb[q] = ok ? __ldg(geo.nbr + q * ld + e) : -1;
+    g1_fetch_col<NP>(pp, 0, a.in, ld, e, ok);
+#pragma unroll
+    for (int q = 0; q < 3; ++q) g1_fetch_col<NP>(pp, q + 1, a.in, ld, nb[q], ok && nb[q] >= 0);
+    for (; e < a.e1; e += stride) {
+      pp.e_next = e + stride;
+#pragma unroll
+      for (int q = 0; q < 3; ++q) pp.nb_next[q] = pp.e_next < a.e1 ? __ldg(geo.nbr + q * ld + pp.e_next) : -1;
+      g1_element<P, MODE, FLUX, VAR, true>(T, geo, a, e, dt, tstage, lam_min, res_max, &pp);
+    }
+    cp_async_wait<0>();
+  } else {
+    for (int e = a.e0 + blockIdx.x * blockDim.x + threadIdx.x; e < a.e1; e += stride)
+      g1_element<P, MODE, FLUX, VAR>(T, geo, a, e, dt, tstage, lam_min, res_max);
+  }
 
   if constexpr (MODE == kModeStage) {
     const int par = a.step & 1;

@@ -100,15 +100,6 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
       : "d"(a), "d"(b));
 }
 
-// cp.async of one double into shared memory (zero-filled when !pred); lane-private
-// destinations, so the issuing lane's wait_group is the only synchronisation needed.
-__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool pred) {
-  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(dst));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sa), "l"(src), "r"(pred ? 8 : 0) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 // A-fragment copy of one element column (4 variables x Np modes) into a lane-private
 // slot array [4 * KS][32] of shared memory.
@@ -434,17 +425,17 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
           const int kc = left ? ko : K - 1 - ko;  // canonical (left-element) point index
           if (BND && bnd && live) ghost_state<K>(UL, nb, ed, kc, nx, ny, tstage, geo, UR);
           const Prim wl = primitives(UL, g1), wr = primitives(UR, g1);
+          const double wh = live ? h * smem[D::kWe + kc] : 0.0;
           double f[4];
           if (admissible(UL, wl) && admissible(UR, wr)) {
-            num_flux<FLUX>(UL, wl, UR, wr, nx, ny, gamma, f);
+            num_flux_w<FLUX>(UL, wl, UR, wr, nx, ny, gamma, left ? -wh : wh, f);
           } else {
             if (valid && live) record_error(sc, err_key(a.seq, kPassSurface, ed, kc));
 #pragma unroll
             for (int m = 0; m < 4; ++m) f[m] = 0.0;
           }
-          const double wh = live ? h * smem[D::kWe + kc] : 0.0;
 #pragma unroll
-          for (int m = 0; m < 4; ++m) fn[m][i] = left ? -(wh * f[m]) : (wh * f[m]);
+          for (int m = 0; m < 4; ++m) fn[m][i] = f[m];
         }
         __syncwarp();
         if (kHalfS && sp == D::NSP - 1) {  // half-live last packed tile (p = 3): one k-step
@@ -545,17 +536,17 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
           const bool live = ko < K;
           if (BND && bnd && live) ghost_state<K>(UL, nb, ed, kc, nx, ny, tstage, geo, UR);
           const Prim wl = primitives(UL, g1), wr = primitives(UR, g1);
+          const double wh = live ? h * smem[D::kWe + (kc < 8 ? kc : 0)] : 0.0;
           double f[4];
           if (admissible(UL, wl) && admissible(UR, wr)) {
-            num_flux<FLUX>(UL, wl, UR, wr, nx, ny, gamma, f);
+            num_flux_w<FLUX>(UL, wl, UR, wr, nx, ny, gamma, left ? -wh : wh, f);
           } else {
             if (valid && live) record_error(sc, err_key(a.seq, kPassSurface, ed, kc));
 #pragma unroll
             for (int m = 0; m < 4; ++m) f[m] = 0.0;
           }
-          const double wh = live ? h * smem[D::kWe + (kc < 8 ? kc : 0)] : 0.0;
 #pragma unroll
-          for (int m = 0; m < 4; ++m) fn[m][i] = left ? -(wh * f[m]) : (wh * f[m]);
+          for (int m = 0; m < 4; ++m) fn[m][i] = f[m];
         }
         __syncwarp();
 #pragma unroll

@@ -1,6 +1,8 @@
 // Kernels for polynomial degree 1 (see kernels_tu.cuh) plus the p = 1
 // Barth-Jespersen limiter with the positivity guard (solver.cpp:286-425).
 #define DGB_P 1
+#include <cstdlib>
+
 #include "kernels_tu.cuh"
 
 namespace dgbk {
@@ -8,6 +10,7 @@ namespace dgbk {
 namespace {
 __constant__ LimTab c_lim;
 constexpr int kLimNE = 6, kLimNPT = 12;  // p = 1 tables: 2 points per edge, 3 interior
+constexpr int kLim4PerSm = 128;          // latency-form limiter up to this many elements per SM
 
 __device__ __forceinline__ double ref_pressure(double rho, double mx, double my, double E, double g1) {
   return g1 * (E - __dmul_rn(0.5, fma(my, my, __dmul_rn(mx, mx))) / rho);
@@ -101,12 +104,12 @@ __device__ __forceinline__ void limit_element(const Geo& geo, const LimArgs& a, 
     // Barth-Jespersen per conserved variable against the neighbours' centroid range
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
-      const double uc = c0[m] * sqrt2;
+      const double uc = __dmul_rn(c0[m], sqrt2);
       double umax = uc, umin = uc;
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
         if (nb[q] < 0) continue;
-        const double un = nm[q][m] * sqrt2;
+        const double un = __dmul_rn(nm[q][m], sqrt2);
         umax = std_max(umax, un);
         umin = std_min(umin, un);
       }
@@ -132,7 +135,8 @@ __device__ __forceinline__ void limit_element(const Geo& geo, const LimArgs& a, 
     }
 
     // positivity guard toward the cell mean (solver.cpp:363-417)
-    const double mr = c0[0] * sqrt2, mmx = c0[1] * sqrt2, mmy = c0[2] * sqrt2, mE = c0[3] * sqrt2;
+    const double mr = __dmul_rn(c0[0], sqrt2), mmx = __dmul_rn(c0[1], sqrt2), mmy = __dmul_rn(c0[2], sqrt2),
+                 mE = __dmul_rn(c0[3], sqrt2);
     const double p_mean = ref_pressure(mr, mmx, mmy, mE, g1);
     if (mr > 0.0 && p_mean > 0.0) {
       const double eps_rho = 1e-8 * mr;
@@ -225,6 +229,197 @@ __device__ __forceinline__ void limit_element(const Geo& geo, const LimArgs& a, 
 #endif
     }
   }
+}
+
+// The latency form of limit_element: four lanes per element, lane v owning conserved variable
+// v, for launches that leave the GPU mostly idle (small meshes: a stage then costs one element's
+// dependency chain, not bandwidth).  Barth-Jespersen of variable v runs on lane v with exactly
+// the operations of limit_element's loop body for m = v; the positivity guard gathers the four
+// means and deviations by shuffles and every lane of the quad evaluates it redundantly (the same
+// operations on the same operands, so the same decision and factors); the CFL epilogue evaluates
+// midpoint q on lane q.  Bit-identical to limit_element (tests/test_gpu_parity.py).
+template <int NE, int NPT, int EPI>
+__device__ __forceinline__ void limit_element4(const Geo& geo, const LimArgs& a, int e, bool valid, int v,
+                                               double& lam_min, double& res_max) {
+  const bool want_lambda = (EPI & 1) && a.want_lambda, want_resid = (EPI & 2) && a.want_resid;
+  constexpr int NP = 3;
+  const long long ld = geo.ld;
+  const double g1 = geo.gamma - 1.0;
+  const double sqrt2 = sqrt(2.0);
+  Scalars* sc = a.sc;
+  const LimTab& L = c_lim;
+  const Tab<1>& T = c_tab;
+  const int n_edge = NE ? NE : L.n_edge;
+  const int e_begin = NE ? NPT - NE - 3 : L.edge_begin;
+  const int n_pts = NPT ? NPT : L.n_pts;
+  const double* __restrict__ cv = a.c + static_cast<long long>(v) * NP * ld;
+  const double c0 = cv[e];
+  double c1 = cv[ld + e], c2 = cv[2 * ld + e];
+  int nb[3];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) nb[q] = __ldg(geo.nbr + q * ld + e);
+  // CFL epilogue operands of midpoint q = v, requested with the neighbour means
+  double enx = 0.0, eny = 0.0, rin = 0.0;
+  if (want_lambda) {
+    const int ed = __ldg(geo.eid + (v < 3 ? v : 2) * ld + e);
+    rin = __ldg(geo.inradius + e);
+    enx = __ldg(geo.enx + ed);
+    eny = __ldg(geo.eny + ed);
+  }
+  double nm[3];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) nm[q] = nb[q] >= 0 ? __ldg(cv + nb[q]) : 0.0;
+
+  // Barth-Jespersen of variable v (limit_element, loop body for m = v)
+  {
+    const double uc = __dmul_rn(c0, sqrt2);
+    double umax = uc, umin = uc;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      if (nb[q] < 0) continue;
+      const double un = __dmul_rn(nm[q], sqrt2);
+      umax = std_max(umax, un);
+      umin = std_min(umin, un);
+    }
+    const double tol = 1e-13 * (fabs(uc) + (umax - umin));
+    double dpos = 0.0, dneg = 0.0;
+#pragma unroll
+    for (int k = e_begin; k < e_begin + n_edge; ++k) {
+      const double d = fma(c2, L.phi2[k], __dmul_rn(c1, L.phi1[k]));
+      dpos = d > dpos ? d : dpos;
+      dneg = d < dneg ? d : dneg;
+    }
+    double alpha = 1.0;
+    if (dpos > tol) alpha = std_min(alpha, std_clamp01((umax - uc) / dpos));
+    if (dneg < -tol) alpha = std_min(alpha, std_clamp01((umin - uc) / dneg));
+    c1 *= alpha;
+    c2 *= alpha;
+  }
+
+  // positivity guard toward the cell mean (solver.cpp:363-417) on the gathered quad
+  const double dv = fma(fabs(c2), L.max_phi2, __dmul_rn(fabs(c1), L.max_phi1));
+  double C0[4], dev[4];
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    C0[m] = __shfl_sync(kFull, c0, m, 4);
+    dev[m] = __shfl_sync(kFull, dv, m, 4);
+  }
+  const double mr = __dmul_rn(C0[0], sqrt2), mmx = __dmul_rn(C0[1], sqrt2), mmy = __dmul_rn(C0[2], sqrt2),
+               mE = __dmul_rn(C0[3], sqrt2);
+  const double p_mean = ref_pressure(mr, mmx, mmy, mE, g1);
+  const bool guard = mr > 0.0 && p_mean > 0.0;
+  const double eps_rho = 1e-8 * mr;
+  const double eps_p = 1e-8 * p_mean;
+  bool safe = true;
+  if (guard) {
+    const double rho_floor = mr - dev[0];
+    safe = rho_floor > eps_rho;
+    if (safe) {
+      const double mx_peak = fabs(mmx) + dev[1];
+      const double my_peak = fabs(mmy) + dev[2];
+      const double p_floor =
+          g1 * ((mE - dev[3]) - __dmul_rn(0.5, fma(my_peak, my_peak, __dmul_rn(mx_peak, mx_peak))) / rho_floor);
+      safe = p_floor > eps_p;
+    }
+  }
+  const bool slow = guard && !safe;
+  if (__any_sync(kFull, slow)) {  // shuffles by the whole warp, the sweep only where needed
+    double C1[4], C2[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      C1[m] = __shfl_sync(kFull, c1, m, 4);
+      C2[m] = __shfl_sync(kFull, c2, m, 4);
+    }
+    if (slow) {
+      double rho_min = mr;
+      for (int k = 0; k < n_pts; ++k)
+        rho_min = fmin(rho_min, fma(C2[0], L.phi2[k], fma(C1[0], L.phi1[k], __dmul_rn(C0[0], sqrt2))));
+      if (rho_min < eps_rho) {
+        const double th = fmin(fmax((mr - eps_rho) / (mr - rho_min), 0.0), 1.0);
+        C1[0] *= th;
+        C2[0] *= th;
+        if (v == 0) {
+          c1 = C1[0];
+          c2 = C2[0];
+        }
+      }
+      double th_p = 1.0;
+      for (int k = 0; k < n_pts; ++k) {
+        double u[4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) u[m] = fma(C2[m], L.phi2[k], fma(C1[m], L.phi1[k], __dmul_rn(C0[m], sqrt2)));
+        if (u[0] <= 0.0) {
+          th_p = 0.0;
+          break;
+        }
+        const double pk = ref_pressure(u[0], u[1], u[2], u[3], g1);
+        if (pk < eps_p) th_p = fmin(th_p, (p_mean - eps_p) / (p_mean - pk));
+      }
+      if (th_p < 1.0) {
+        th_p = fmax(th_p, 0.0);
+        c1 *= th_p;
+        c2 *= th_p;
+      }
+    }
+  }
+  if (valid) {
+    double* __restrict__ cw = a.c + static_cast<long long>(v) * NP * ld;
+    cw[ld + e] = c1;
+    cw[2 * ld + e] = c2;
+    if (a.push && e >= geo.send_begin) {
+      const double w[1][NP] = {{c0, c1, c2}};
+      push_element<NP, 1>(geo, a.peers, a.out_buf, e, v, w);
+    }
+    if (want_resid) {
+      const double* __restrict__ uv = a.u + static_cast<long long>(v) * NP * ld;
+      res_max = std_max(res_max, fabs(__ldg(uv + e) - c0));
+      res_max = std_max(res_max, fabs(__ldg(uv + ld + e) - c1));
+      res_max = std_max(res_max, fabs(__ldg(uv + 2 * ld + e) - c2));
+    }
+  }
+  if (want_lambda) {  // CFL bound of the limited state (solver.cpp:439-457), midpoint q on lane q
+    double U[4];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) U[q] = fma(T.phm[q][2], c2, fma(T.phm[q][1], c1, T.phm[q][0] * c0));
+    U[3] = U[0];
+    transpose4(U, v);  // lane q: the four variables at midpoint q
+    bool ok;
+    const double ws = wave_speed_ieee(U, enx, eny, geo.gamma, ok);
+    double lam = 0.0;
+    if (v < 3) {
+      if (ok) {
+        lam = ws;
+      } else if (valid) {
+        record_error(sc, err_key(a.seq, kPassDt, __ldg(geo.ref_id + e), v + 1));
+      }
+    }
+    lam = std_max(lam, __shfl_xor_sync(kFull, lam, 1));
+    lam = std_max(lam, __shfl_xor_sync(kFull, lam, 2));
+    if (valid && v == 0) lam_min = std_min(lam_min, 2.0 * rin / (3.0 * lam));
+  }
+}
+
+template <int NE, int NPT, int EPI>
+__global__ void __launch_bounds__(kBlock) k_limit4(Geo geo, LimArgs a) {
+  Scalars* sc = a.sc;
+  __shared__ int s_stop;
+  if (threadIdx.x == 0) s_stop = (sc->err_key != kNoError || sc->halt) ? 1 : 0;
+  __syncthreads();
+  if (s_stop) return;
+  double lam_min = __longlong_as_double(0x7ff0000000000000ll);
+  double res_max = 0.0;
+  const int n4 = ((a.e1 - a.e0) * 4 + 31) & ~31;  // whole warps: the quads shuffle warp-wide
+  for (int tid = blockIdx.x * blockDim.x + threadIdx.x; tid < n4; tid += gridDim.x * blockDim.x) {
+    int e = a.e0 + (tid >> 2);
+    const bool valid = e < a.e1;
+    if (!valid) e = a.e1 - 1;
+    limit_element4<NE, NPT, EPI>(geo, a, e, valid, tid & 3, lam_min, res_max);
+  }
+  const bool want_lambda = (EPI & 1) && a.want_lambda, want_resid = (EPI & 2) && a.want_resid;
+  const int par = a.step & 1;
+  if (want_lambda) block_reduce_atomic<true>(lam_min, &sc->dtmin[par ^ 1]);
+  if (want_resid) block_reduce_atomic<false>(res_max, &sc->resid[par]);
+  if (a.push) __threadfence_system();
 }
 
 template <int NE, int NPT, int EPI>
@@ -336,6 +531,25 @@ cudaError_t upload_limtab(const LimTab& t, cudaStream_t s) {
 }
 
 
+cudaError_t preload_limit() {
+  cudaError_t err = cudaSuccess;
+  auto touch = [&](auto k) {
+    cudaFuncAttributes fa;
+    const cudaError_t e = cudaFuncGetAttributes(&fa, k);
+    if (e != cudaSuccess) err = e;
+  };
+  touch(k_limit<0, 0, 3>);
+  touch(k_limit<kLimNE, kLimNPT, 0>);
+  touch(k_limit<kLimNE, kLimNPT, 1>);
+  touch(k_limit<kLimNE, kLimNPT, 2>);
+  touch(k_limit<kLimNE, kLimNPT, 3>);
+  touch(k_limit4<kLimNE, kLimNPT, 0>);
+  touch(k_limit4<kLimNE, kLimNPT, 1>);
+  touch(k_limit4<kLimNE, kLimNPT, 2>);
+  touch(k_limit4<kLimNE, kLimNPT, 3>);
+  return err;
+}
+
 int limit_resident_blocks() {
   static std::atomic<int> occ{0};
   int o = occ.load(std::memory_order_relaxed);
@@ -389,10 +603,34 @@ cudaError_t launch_stage_limit(int grid, const Geo& g, const StageArgs& a, const
   return err;
 }
 
+// Elements up to which a limiter launch takes the four-lane latency form (k_limit4): below
+// this the one-thread form leaves most of the GPU idle and the launch costs one element's
+// dependency chain.  DGB_LIM4_MAXN overrides (0: never).
+int limit_latency_max_n() {
+  static std::atomic<int> v{-1};
+  int n = v.load(std::memory_order_relaxed);
+  if (n < 0) {
+    const char* env = std::getenv("DGB_LIM4_MAXN");
+    n = env ? std::atoi(env) : kLim4PerSm * sm_count();
+    v.store(n, std::memory_order_relaxed);
+  }
+  return n;
+}
+
 cudaError_t launch_limit(int grid, const Geo& g, const LimArgs& a, cudaStream_t s) {
   if (a.e1 <= a.e0) return cudaSuccess;
-  if (grid <= 0) grid = grid_for(a.e1 - a.e0, limit_resident_blocks());
   const int epi = (a.want_lambda ? 1 : 0) | (a.want_resid ? 2 : 0);
+  if (a.e1 - a.e0 <= (g.lat_limit_n >= 0 ? g.lat_limit_n : limit_latency_max_n()) && g_lim_pts[current_device()].load() == (kLimNE | (kLimNPT << 16))) {
+    if (grid <= 0) grid = grid_for(static_cast<long long>(a.e1 - a.e0) * 4, 16);
+    switch (epi) {
+      case 0: k_limit4<kLimNE, kLimNPT, 0><<<grid, kBlock, 0, s>>>(g, a); break;
+      case 1: k_limit4<kLimNE, kLimNPT, 1><<<grid, kBlock, 0, s>>>(g, a); break;
+      case 2: k_limit4<kLimNE, kLimNPT, 2><<<grid, kBlock, 0, s>>>(g, a); break;
+      default: k_limit4<kLimNE, kLimNPT, 3><<<grid, kBlock, 0, s>>>(g, a); break;
+    }
+    return cudaGetLastError();
+  }
+  if (grid <= 0) grid = grid_for(a.e1 - a.e0, limit_resident_blocks());
   if (g_lim_pts[current_device()].load() == (kLimNE | (kLimNPT << 16))) {
     switch (epi) {
       case 0: k_limit<kLimNE, kLimNPT, 0><<<grid, kBlock, 0, s>>>(g, a); break;

@@ -2,6 +2,7 @@
 // element-kernel modes and the CFL kernel.  Included by kernels_pN.cu with
 // DGB_P defined.
 #include <atomic>
+#include <cstdlib>
 
 #include "element_mma.cuh"
 #include "launch.hpp"
@@ -25,12 +26,17 @@ namespace dgbk {
 namespace {
 __constant__ Tab<DGB_P> c_tab;
 constexpr int kG = Lanes<DGB_P>::value;  // lanes per element
+#ifndef DGB_G4_PER_SM
+#define DGB_G4_PER_SM 32  // measured on the 2,880-triangle vortex mesh: 11.6 vs 12.5 us per stage; 11,520: 13.6 vs 12.7 (worse)
+#endif
+constexpr int kG4PerSm = DGB_G4_PER_SM;  // latency-form stage kernel up to this many elements per SM
 
 constexpr bool kMma = DGB_P >= DGB_MMA_MINP;
 constexpr int kMinB = kMma ? DGB_MMA_MINB(DGB_P) : MinBlocks<DGB_P>::value;
 constexpr int kThreads = kMma ? DGB_MMA_THREADS(DGB_P) : kBlock;  // threads per block of k_element
 // dynamic shared memory (bytes): tables + per-warp staging buffers
-constexpr int kSmem = kMma ? (MmaDim<DGB_P>::kSize + (kThreads / 32) * MmaDim<DGB_P>::kWarpBuf) * 8 : 0;
+constexpr int kSmem = kMma ? (MmaDim<DGB_P>::kSize + (kThreads / 32) * MmaDim<DGB_P>::kWarpBuf) * 8
+                            : (kG == 1 ? g1_pipe_bytes<DGB_P>() * kThreads : 0);
 
 // One instance per mode, numerical flux (geo.flux) and variant (kVar* bits, dg_kernels.cuh):
 // the stage mode with or without the RK4 accumulator (a.kmode != 0) and the CFL epilogue
@@ -47,6 +53,28 @@ __global__ void __launch_bounds__(kThreads, kMinB) k_element(Geo geo, StageArgs 
     element_body_g1<DGB_P, MODE, FLUX, VAR>(c_tab, geo, a);
   } else {
     element_body<DGB_P, MODE, FLUX, VAR>(c_tab, geo, a);
+  }
+}
+
+// Latency form of the low-degree stage kernel: four lanes per element (element_body, lane =
+// conserved variable, each pointwise evaluation on its own lane), for launches too small to
+// fill the GPU, where a stage costs one element's dependency chain rather than bandwidth.
+// The same operations in the same order as the one-thread body: bit-identical.
+template <int FLUX, int VAR>
+__global__ void __launch_bounds__(kBlock) k_element4(Geo geo, StageArgs a) {
+  if constexpr (!kMma && kG == 1) element_body<DGB_P, kModeStage, FLUX, VAR>(c_tab, geo, a);
+}
+template <int FLUX, class F>
+void with_instance4(int var, F&& f) {
+  switch (var & 7) {
+    case 0: f(k_element4<FLUX, 0>); break;
+    case 1: f(k_element4<FLUX, 1>); break;
+    case 2: f(k_element4<FLUX, 2>); break;
+    case 3: f(k_element4<FLUX, 3>); break;
+    case 4: f(k_element4<FLUX, 4>); break;
+    case 5: f(k_element4<FLUX, 5>); break;
+    case 6: f(k_element4<FLUX, 6>); break;
+    default: f(k_element4<FLUX, 7>); break;
   }
 }
 
@@ -134,7 +162,7 @@ int grid_for(long long threads, int blocks_per_sm, int block = kBlock) {
 
 template <>
 cudaError_t Launch<DGB_P>::upload(const Tab<DGB_P>& t, cudaStream_t s) {
-  if constexpr (kMma) {  // opt in to > 48 KB of dynamic shared memory: a per-device function attribute
+  if constexpr (kSmem > 32 * 1024) {  // opt in to large dynamic shared memory (with the static part > 48 KB): a per-device function attribute
     static std::atomic<unsigned long long> done{0};
     const unsigned long long bit = 1ull << current_device();
     if (!(done.load() & bit)) {
@@ -166,6 +194,25 @@ int Launch<DGB_P>::resident_blocks(int mode) {
 }
 
 template <>
+cudaError_t Launch<DGB_P>::preload() {
+  cudaError_t err = cudaSuccess;
+  auto touch = [&](auto k) {
+    cudaFuncAttributes fa;
+    const cudaError_t e = cudaFuncGetAttributes(&fa, k);
+    if (e != cudaSuccess) err = e;
+  };
+  for (int flux = 0; flux < 2; ++flux)
+    for (int mode = 0; mode < 4; ++mode)
+      for (int var = 0; var < 8; ++var) with_instance(flux, mode, var, touch);
+  for (int var = 0; var < 8; ++var) {
+    with_instance4<kFluxLLF>(var, touch);
+    with_instance4<kFluxRoe>(var, touch);
+  }
+  touch(k_dt);
+  return err;
+}
+
+template <>
 int Launch<DGB_P>::lanes() {
   return kMma ? 0 : kG;
 }
@@ -180,9 +227,37 @@ int Launch<DGB_P>::mma_table(const Tab<DGB_P>& t, double* out) {
   }
 }
 
+// Elements up to which a low-degree stage launch takes the four-lane latency form
+// (k_element4); DGB_G4_MAXN overrides (0: never).
+namespace {
+int stage_latency_max_n() {
+  static std::atomic<int> v{-1};
+  int n = v.load(std::memory_order_relaxed);
+  if (n < 0) {
+    const char* env = std::getenv("DGB_G4_MAXN");
+    n = env ? std::atoi(env) : kG4PerSm * sm_count();
+    v.store(n, std::memory_order_relaxed);
+  }
+  return n;
+}
+}  // namespace
+
 template <>
 cudaError_t Launch<DGB_P>::element(int mode, int grid, const Geo& g, const StageArgs& a, cudaStream_t s) {
   if (a.e1 <= a.e0) return cudaSuccess;
+  if constexpr (!kMma && kG == 1) {
+    if (mode == kModeStage && a.e1 - a.e0 <= (g.lat_stage_n >= 0 ? g.lat_stage_n : stage_latency_max_n())) {
+      if (grid <= 0) grid = grid_for(static_cast<long long>((a.e1 - a.e0 + 31) & ~31) * 4, 16);
+      cudaError_t err = cudaSuccess;
+      auto go = [&](auto k) {
+        k<<<grid, kBlock, 0, s>>>(g, a);
+        err = cudaGetLastError();
+      };
+      const int var = variant_of(mode, g, a);
+      if (g.flux == kFluxRoe) with_instance4<kFluxRoe>(var, go); else with_instance4<kFluxLLF>(var, go);
+      return err;
+    }
+  }
   if (grid <= 0) {
     // DMMA variant: one 8-element tile per warp; others: kG lanes per element
     const long long threads = kMma ? static_cast<long long>((a.e1 - a.e0 + 7) / 8) * 32

@@ -21,9 +21,14 @@ struct Launch {
   // DMMA fragment-ordered tables: size in doubles (0 when the degree does not use
   // the DMMA kernel); fills `out` when non-null
   static int mma_table(const Tab<P>& t, double* out);
+  // Load every kernel instance of this degree now.  Under CUDA's lazy loading the first launch
+  // of a function loads its module, which waits for the device; a partition whose peers are
+  // spinning in a flag wait on other streams would then stall until their timeout.
+  static cudaError_t preload();
 };
 
 cudaError_t upload_limtab(const LimTab& t, cudaStream_t s);
+cudaError_t preload_limit();  // every limiter instance (see Launch::preload)
 cudaError_t launch_limit(int grid, const Geo& g, const LimArgs& a, cudaStream_t s);
 int limit_resident_blocks();
 // Stage + limiter in one persistent launch (p = 1, whole-mesh contexts); grid <= 0: one

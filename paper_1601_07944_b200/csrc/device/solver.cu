@@ -32,6 +32,7 @@ namespace {
 
 constexpr int kWindow = 256;  // renumbering window (elements), multiple of 32
 constexpr int kBatch = 64;    // steps per host synchronisation in open-ended drivers
+constexpr int kFuseMaxN = 400000;  // fused stage + limiter launch by default up to this many elements (crossover measured between 184K and 737K)
 
 struct Fail {
   int code;
@@ -352,7 +353,11 @@ struct dgb_ctx {
   // device geometry
   DevBuf<double> d_tau, d_inv_det, d_inradius, d_enx, d_eny, d_eh, d_bstate, d_bwn, d_bx, d_mma;
   DevBuf<int> d_nbr, d_eid, d_info, d_ref_id;  // d_ref_id: reference id of each device column
-  Geo geo{};
+  Geo geo = [] {
+    Geo g{};
+    g.lat_stage_n = g.lat_limit_n = -1;  // built-in latency-form sizes
+    return g;
+  }();
 
   // coefficient buffers (device order [4][np][ld])
   DevBuf<double> state[2], input, volume, deriv, stage[2], kacc, slots, staging, hist, staging_in, staging_out;
@@ -381,7 +386,7 @@ struct dgb_ctx {
   std::vector<double> samples[6];  // per-launch device ms of each timer category since the last reset
 
   // fused stage + limiter (p = 1, whole mesh; kernels_p1.cu k_stage_limit)
-  bool fuse_limit = true;
+  int fuse_limit = -1;  // 1 fused stage + limiter launch, 0 two kernels, -1 by mesh size (kFuseMaxN)
   std::vector<int2> fz_range_h;  // per 32-element tile: first and last chunk holding a neighbour
   int fz_maxreach = 0;           // max over tiles of (last tile waited for - tile)
   DevBuf<unsigned long long> fz_count;
@@ -842,7 +847,8 @@ RunOut run_steps(dgb_ctx* c, const RunSpec& r) {
   const unsigned ALL = X ? all_peers(c) : 0u;
   // the fused stage + limiter launch (whole-mesh contexts; a partition keeps the two-kernel
   // path, whose halo rounds it needs)
-  const bool fused = r.limiting && !c->partitioned && c->fuse_limit && c->p == 1;
+  const bool fused = r.limiting && !c->partitioned && c->p == 1 &&
+                     (c->fuse_limit < 0 ? c->N <= kFuseMaxN : c->fuse_limit != 0);
   if (fused) {
     const int nt = static_cast<int>(c->fz_range_h.size());
     const int nch = (nt + dgbk::kFuseChunk - 1) / dgbk::kFuseChunk;
@@ -882,6 +888,10 @@ RunOut run_steps(dgb_ctx* c, const RunSpec& r) {
     for (int64_t b = 0; b < batch; ++b) {
       const int64_t s = launched + b;
       const int par = static_cast<int>(s & 1);
+      // max|u_new - u| (max_abs_diff, solver.cpp:536) is observable only through the stop rules, the
+      // on_step history and the residual of the last step: a fixed-step run without a history
+      // evaluates it on its last step alone (the limiter then skips reading u^n on every other step)
+      const bool resid = r.stop_t || r.stop_steady || d_hist || s + 1 == r.max_steps;
       double* u = c->state[(cur0 + s) & 1].p;
       double* unext = c->state[(cur0 + s + 1) & 1].p;
       for (int k = 0; k < S; ++k) {
@@ -908,7 +918,7 @@ RunOut run_steps(dgb_ctx* c, const RunSpec& r) {
         a.first = k == 0;
         a.last = last;
         a.want_lambda = last && !r.limiting && r.dt_mode == 1;
-        a.want_resid = last && !r.limiting;
+        a.want_resid = last && !r.limiting && resid;
         a.seq = static_cast<unsigned long long>(s) * 8 + k + 1;
         a.seq_next = static_cast<unsigned long long>(s + 1) * 8;
         a.sc = c->d_sc;
@@ -924,7 +934,7 @@ RunOut run_steps(dgb_ctx* c, const RunSpec& r) {
           la.u = u;
           la.step = static_cast<int>(s);
           la.want_lambda = last && r.dt_mode == 1;
-          la.want_resid = last;
+          la.want_resid = last && resid;
           la.seq = static_cast<unsigned long long>(s + 1) * 8;
           la.sc = c->d_sc;
           la.e0 = 0;
@@ -967,7 +977,7 @@ RunOut run_steps(dgb_ctx* c, const RunSpec& r) {
           la.u = u;
           la.step = static_cast<int>(s);
           la.want_lambda = last && r.dt_mode == 1;
-          la.want_resid = last;
+          la.want_resid = last && resid;
           la.seq = static_cast<unsigned long long>(s + 1) * 8;
           la.sc = c->d_sc;
           la.peers = c->d_peers;
@@ -1248,7 +1258,7 @@ int dgb_part_create(const dgb_mesh_view* m, const dgb_tables_view* t, const dgb_
         c->fz_maxreach = std::max(c->fz_maxreach, std::min(nt - 1, (hi_c + 1) * CH - 1) - t);
       }
       const char* env = std::getenv("DGB_FUSED_LIMIT");
-      c->fuse_limit = !(env && env[0] == '0');
+      c->fuse_limit = env ? (env[0] == '0' ? 0 : (env[0] == '1' ? 1 : -1)) : -1;
     }
     c->d_tau.upload(tau.data(), tau.size(), c->stream);
     c->d_inv_det.upload(inv_det.data(), ld, c->stream);
@@ -1466,8 +1476,15 @@ int dgb_set_flux(dgb_ctx* c, int flux) {
 }
 
 int dgb_set_fused_limiter(dgb_ctx* c, int enable) {
-  if (!c) return DGB_ERR_ARG;
-  c->fuse_limit = enable != 0;
+  if (!c || enable < -1 || enable > 1) return DGB_ERR_ARG;
+  c->fuse_limit = enable;
+  return DGB_OK;
+}
+
+int dgb_set_latency_forms(dgb_ctx* c, int stage_max_n, int limit_max_n) {
+  if (!c || stage_max_n < -1 || limit_max_n < -1) return DGB_ERR_ARG;
+  c->geo.lat_stage_n = stage_max_n;
+  c->geo.lat_limit_n = limit_max_n;
   return DGB_OK;
 }
 
@@ -2176,6 +2193,19 @@ int dgb_part_finalize(dgb_ctx* c) {
     c->geo.send_ent = c->d_send_ent.p;
     c->geo.send_begin = c->n_int;
     CU(cudaMemcpyAsync(c->d_peers, &c->h_peers, sizeof(dgbk::PeerTab), cudaMemcpyHostToDevice, c->stream));
+    // every kernel a step may launch is loaded now, not lazily while the peers spin in k_wait
+    {
+      cudaFuncAttributes fa;
+      CU(cudaFuncGetAttributes(&fa, k_signal));
+      CU(cudaFuncGetAttributes(&fa, k_wait));
+    }
+    switch (c->p) {
+      case 1: CU(dgbk::Launch<1>::preload()); CU(dgbk::preload_limit()); break;
+      case 2: CU(dgbk::Launch<2>::preload()); break;
+      case 3: CU(dgbk::Launch<3>::preload()); break;
+      case 4: CU(dgbk::Launch<4>::preload()); break;
+      default: CU(dgbk::Launch<5>::preload()); break;
+    }
     sync(c);
     c->finalized = true;
     return DGB_OK;

@@ -547,3 +547,46 @@ def test_fused_stage_limiter_bitwise_equal_to_two_kernels(scheme, flux, nx):
         ctx.close()
     assert np.array_equal(out[0][0], out[1][0])
     assert out[0][1] == out[1][1] and out[0][2] == out[1][2]
+
+
+@pytest.mark.parametrize("p,scheme,flux,limiting,mesh_kind", [
+    (1, 2, "llf", True, "dmr"), (1, 4, "roe", True, "dmr"), (1, 102, "llf", True, "dmr"),
+    (1, 103, "llf", False, "vortex"), (2, 103, "llf", False, "vortex"), (2, 4, "roe", False, "vortex"),
+    (1, 2, "llf", False, "box")])
+def test_latency_forms_bitwise_equal_to_one_thread_forms(p, scheme, flux, limiting, mesh_kind):
+    """The four-lanes-per-element latency forms (stage kernel at p <= 2, limiter) chosen for small
+    launches give the same bits as the one-thread forms: every scheme family, both fluxes, the
+    boundary-code instance (double Mach, supersonic vortex) and a periodic box."""
+    if mesh_kind == "dmr":
+        mesh = dg2d.generate_mesh(L.MESH_DOUBLE_MACH, 120, 30, 1.0 / 6.0)
+        setup = dg2d.DoubleMachSetup()
+        bc = dg2d.double_mach_boundary(setup)
+        u0 = lambda xy: dg2d.double_mach_initial(xy, setup)  # noqa: E731
+        cfl = 0.3
+    elif mesh_kind == "vortex":
+        mesh = dg2d.generate_mesh(L.MESH_VORTEX, 2, 0, 1.0, 1.384)
+        bc = dg2d.vortex_boundary()
+        u0 = dg2d.vortex_exact
+        cfl = 0.3
+    else:
+        mesh = dg2d.generate_mesh(L.MESH_PERIODIC_BOX, 40, 40, 10.0, 10.0)
+        bc = None
+        u0 = dg2d.IsentropicVortex()
+        cfl = 0.3
+    tb = dg2d.build_tables(p)
+    opts = dg2d.SolverOptions(scheme=scheme, cfl=cfl, limiting=limiting, flux=flux)
+    out = []
+    for forms in ((0, 0), (1 << 30, 1 << 30)):
+        ctx = dg2d.SolverContext(mesh, tb, bc=bc, options=opts)
+        assert L.lib.dgb_set_latency_forms(ctx.handle, *forms) == 0
+        assert L.lib.dgb_set_fused_limiter(ctx.handle, 0) == 0
+        c0 = dg2d.project_initial(u0, mesh, tb)
+        if limiting:
+            c0 = dg2d.limit(ctx, c0)
+        st = dg2d.SolverState(c0)
+        res = dg2d.run_fixed_steps(ctx, st, 25)
+        out.append((st.coeffs, st.t, res))
+        ctx.close()
+    assert np.array_equal(out[0][0], out[1][0])
+    assert out[0][1] == out[1][1] and out[0][2] == out[1][2]
+    assert L.lib.dgb_set_latency_forms(None, 0, 0) == L.ERR_ARG
