@@ -125,6 +125,10 @@ enum : int { kVarRk4 = 1, kVarLambda = 2, kVarBoundary = 4 };
 
 struct StageArgs {
   const double* __restrict__ in;  // stage input coefficients
+  // TMA tensor map (CUtensorMap in global memory) of `in` viewed as [4][n_p][ld] doubles, box
+  // 8 elements x n_p modes x 4 variables: the DMMA kernel (p >= 3) loads each tile's own
+  // coefficients with one cp.async.bulk.tensor; null = per-lane cp.async
+  const void* tm_in;
   const double* __restrict__ u;   // u^n (for alpha, residual, rk4 combine)
   double* __restrict__ out;       // output (volume / slots / deriv / next stage)
   double* __restrict__ kacc;      // RK4 derivative accumulator

@@ -932,7 +932,6 @@ __device__ __forceinline__ void g1_element(const Tab<P>& T, const Geo& geo, cons
 #pragma unroll
           for (int j = 0; j < NP; ++j) {
             const double cj = ld_nc(a.in + (static_cast<long long>(m) * NP + j) * ld + e);
-#pragma unroll
             const double cj0 = phq[0] * cj;  // the mode-0 product, the same at every point
 #pragma unroll
             for (int ko = 0; ko < K; ++ko) uoa[ko][m] = j == 0 ? cj0 : fma(phq[ko * NP + j], cj, uoa[ko][m]);

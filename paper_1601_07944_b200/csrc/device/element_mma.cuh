@@ -52,6 +52,9 @@ constexpr int kMmaPackUnroll = DGB_MMA_PACK_UNROLL;
 #ifndef DGB_MMA_U_AHEAD
 #define DGB_MMA_U_AHEAD 1
 #endif
+#ifndef DGB_MMA_TMA
+#define DGB_MMA_TMA 1  // own coefficients of a tile by one TMA box (0: per-lane cp.async)
+#endif
 #ifndef DGB_MMA_PACK_MAXK
 #define DGB_MMA_PACK_MAXK 5  // largest edge-point count K that uses the packed surface
 #endif
@@ -86,6 +89,8 @@ struct MmaDim {
   static constexpr int kPkNb = kPkOwn + (kPacked ? NSP * KS * 32 : 0);      // [NSP][3 sides][3 classes][KS][32]
   static constexpr int kPkProj = kPkNb + (kPacked ? NSP * 9 * KS * 32 : 0);  // [NSP][2][JT][32]
   static constexpr int kSize = kPkProj + (kPacked ? NSP * 2 * JT * 32 : 0);
+  // the per-warp buffers start 128-byte aligned (TMA destination)
+  static constexpr int kBufOff = (kSize + 15) / 16 * 16;
   // per-warp staging after the tables: own [4 KS][32] + neighbour [4 KS][32] (two
   // neighbour buffers when the surface is packed: a tile spans two sides)
   static constexpr int kWarpBuf = (kPacked ? 3 : 2) * 4 * KS * 32;
@@ -132,6 +137,38 @@ __device__ __forceinline__ int half_operands(const double (&v)[4][2], double (&a
   return hi ? 1 : 0;
 }
 
+// ---- TMA load of a tile's own coefficients (one cp.async.bulk.tensor per tile, lane 0)
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+}
+// Box {8 elements, NP modes, 4 variables} of the [4][NP][ld] tensor at element column `col`, into
+// dst[(m NP + j) 8 + g]; completes on `bar`, its transaction count armed with the box bytes.  (A
+// box of 4 KS mode rows, the padding rows zero-filled outside the tensor, measured slower: p=3
+// 0.725 vs 0.718 ms, p=4 0.996 vs 0.979.)  The fence orders the warp's earlier generic-proxy
+// reads of dst before the async-proxy write.
+template <int NP>
+__device__ __forceinline__ void tma_own_tile(double* dst, const void* tm, int col, unsigned long long* bar) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(NP * 4 * 8 * 8)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(smem_u32(dst)),
+      "l"(tm), "r"(col), "r"(0), "r"(0), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  unsigned done;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  } while (!done);
+}
+
 template <int P, int MODE, int FLUX, int VAR>
 __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo, const StageArgs& a,
                                                  double* __restrict__ smem) {
@@ -166,7 +203,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
   const int nwarps = gridDim.x * (blockDim.x >> 5);
   const int ntiles = (a.e1 - a.e0 + 7) >> 3;
   // per-warp staging: own coefficients of the tile, neighbour coefficients of one side
-  double* __restrict__ w_own = smem + D::kSize + wib * D::kWarpBuf;
+  double* __restrict__ w_own = smem + D::kBufOff + wib * D::kWarpBuf;
   double* __restrict__ w_nbr = w_own + FR;
   // packed surface (p = 3, 4): a second neighbour buffer, side q lives in buffer q & 1
   constexpr bool kPk = D::kPacked && (MODE == kModeRhs || MODE == kModeStage);
@@ -179,6 +216,37 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
   constexpr bool kCSmem = P >= DGB_MMA_C_SMEM_MINP && MODE == kModeStage;
   constexpr bool kUAhead = DGB_MMA_U_AHEAD != 0;
   double* __restrict__ w_nbr2 = w_own + 2 * FR;
+  // Own coefficients of a tile.  kTma builds: one cp.async.bulk.tensor box per tile (a.tm_in, the
+  // launcher guarantees an even first column: 16-byte aligned boxes), issued by lane 0 into
+  // w_own[(m NP + j) 8 + g] and completing on the warp's mbarrier.  Otherwise per-lane cp.async
+  // into the fragment order w_own[(m KS + ks) 32 + lane].
+  constexpr bool kTma = DGB_MMA_TMA != 0;
+  __shared__ unsigned long long s_own_bar[32];
+  unsigned long long* own_bar = &s_own_bar[wib];
+  unsigned own_phase = 0;
+  if (kTma) {
+    if (lane == 0) {
+      mbar_init(own_bar);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+  }
+  auto own_fetch = [&](int tl, int col, bool ok) {  // tile tl (element column col of lane group g)
+    if constexpr (kTma) {
+      if (lane == 0 && tl < ntiles) tma_own_tile<NP>(w_own, a.tm_in, a.e0 + tl * 8, own_bar);
+    } else {
+      fetch_frag<NP, KS>(w_own, a.in, ld, col, ok, lane, t);
+    }
+  };
+  // A fragment (element g, mode 4 ks + t) of variable m from the own buffer
+  auto own_a = [&](int m, int ks) -> double {
+    if constexpr (kTma) {
+      const int j = 4 * ks + t;
+      return j < NP ? w_own[(m * NP + j) * 8 + g] : 0.0;
+    } else {
+      return w_own[(m * KS + ks) * 32 + lane];
+    }
+  };
 
   double lam_min = __longlong_as_double(0x7ff0000000000000ll);
   double res_max = 0.0;
@@ -195,7 +263,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
   {
     bool ok;
     const int e = elem_of(warp, ok);
-    fetch_frag<NP, KS>(w_own, a.in, ld, e, ok, lane, t);
+    own_fetch(warp, e, ok);
     cp_async_commit();
     if constexpr (MODE != kModeVolume) {
 #pragma unroll
@@ -223,6 +291,10 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
       inf = __ldg(geo.info + e);
     }
     cp_async_wait<0>();  // own coefficients and side-0 neighbours of this tile
+    if constexpr (kTma) {
+      mbar_wait(own_bar, own_phase);
+      own_phase ^= 1u;
+    }
     __syncwarp();
 
     double R[4][JT][2];
@@ -243,7 +315,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
         for (int ks = 0; ks < KS; ++ks) {
           const double b = smem[D::kPhi + (ks * NT + nt) * 32 + lane];
 #pragma unroll
-          for (int m = 0; m < 4; ++m) dmma(u[m], w_own[(m * KS + ks) * 32 + lane], b);
+          for (int m = 0; m < 4; ++m) dmma(u[m], own_a(m, ks), b);
         }
       };
       constexpr int NTD = D::NTD;
@@ -321,7 +393,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
         for (int m = 0; m < 4; ++m) {
           double sum = 0.0;
 #pragma unroll
-          for (int ks = 0; ks < KS; ++ks) sum = fma(w_own[(m * KS + ks) * 32 + lane], smem[D::kTail + ks * 4 + t], sum);
+          for (int ks = 0; ks < KS; ++ks) sum = fma(own_a(m, ks), smem[D::kTail + ks * 4 + t], sum);
           sum += __shfl_xor_sync(0xffffffffu, sum, 1);
           sum += __shfl_xor_sync(0xffffffffu, sum, 2);
           v[m] = sum;
@@ -368,7 +440,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
         for (int ks = 0; ks < KS; ++ks) {
           const double b = smem[D::kPkOwn + (sp * KS + ks) * 32 + lane];
 #pragma unroll
-          for (int m = 0; m < 4; ++m) dmma(Tw[m], w_own[(m * KS + ks) * 32 + lane], b);
+          for (int m = 0; m < 4; ++m) dmma(Tw[m], own_a(m, ks), b);
         }
         // neighbour traces of the sides present in this tile (their columns only)
 #pragma unroll
@@ -400,7 +472,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
         } else {
           fetch_frag<NP, KS>(w_nbr, a.in, ld, nbn[0], nvalid && nbn[0] >= 0, lane, t);
           fetch_frag<NP, KS>(w_nbr2, a.in, ld, nbn[1], nvalid && nbn[1] >= 0, lane, t);
-          if (!kCSmem) fetch_frag<NP, KS>(w_own, a.in, ld, e_next, nvalid, lane, t);
+          if (!kCSmem) own_fetch(tile + nwarps, e_next, nvalid);
         }
         cp_async_commit();
         // numerical flux at this lane's two packed points, canonical orientation
@@ -489,7 +561,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
         for (int ks = 0; ks < KS; ++ks) {
           const double b = smem[D::kPhe + (q * KS + ks) * 32 + lane];
 #pragma unroll
-          for (int m = 0; m < 4; ++m) dmma(Tw[m], w_own[(m * KS + ks) * 32 + lane], b);
+          for (int m = 0; m < 4; ++m) dmma(Tw[m], own_a(m, ks), b);
         }
         // neighbour trace (reversed points) — one pass per neighbour side label
         // present in the warp (class renumbering makes that one pass almost always)
@@ -518,7 +590,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
           fetch_frag<NP, KS>(w_nbr, a.in, ld, nbq[q + 1], valid && nbq[q + 1] >= 0, lane, t);
         } else {
           fetch_frag<NP, KS>(w_nbr, a.in, ld, nbn[0], nvalid && nbn[0] >= 0, lane, t);
-          if (!kCSmem) fetch_frag<NP, KS>(w_own, a.in, ld, e_next, nvalid, lane, t);
+          if (!kCSmem) own_fetch(tile + nwarps, e_next, nvalid);
         }
         cp_async_commit();
         // numerical flux at points ko = 2t + i, canonical orientation
@@ -574,7 +646,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
     } else {
       // volume-only: own prefetch for the next tile
       __syncwarp();
-      fetch_frag<NP, KS>(w_own, a.in, ld, e_next, nvalid, lane, t);
+      own_fetch(tile + nwarps, e_next, nvalid);
       cp_async_commit();
     }
 
@@ -629,7 +701,9 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
             const long long idx = (static_cast<long long>(m) * NP + j) * ld + e;
             if (!kUAhead) uv[jt][ii] = (need_u && j < NP) ? __ldg(a.u + idx) : 0.0;
             if constexpr (kCSmem) {  // element g's mode j from the tile's own fragment buffer
-              cv[jt][ii] = (need_c && j < NP) ? w_own[(m * KS + (j >> 2)) * 32 + (g << 2) + (j & 3)] : 0.0;
+              cv[jt][ii] = (need_c && j < NP) ? (kTma ? w_own[(m * NP + j) * 8 + g]
+                                                      : w_own[(m * KS + (j >> 2)) * 32 + (g << 2) + (j & 3)])
+                                              : 0.0;
             } else {
               cv[jt][ii] = (need_c && j < NP) ? __ldg(a.in + idx) : 0.0;
             }
@@ -720,7 +794,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
     }
     if constexpr (kCSmem) {  // the own buffer is free only now
       __syncwarp();
-      fetch_frag<NP, KS>(w_own, a.in, ld, e_next, nvalid, lane, t);
+      own_fetch(tile + nwarps, e_next, nvalid);
       cp_async_commit();
     }
 #pragma unroll

@@ -35,7 +35,7 @@ constexpr bool kMma = DGB_P >= DGB_MMA_MINP;
 constexpr int kMinB = kMma ? DGB_MMA_MINB(DGB_P) : MinBlocks<DGB_P>::value;
 constexpr int kThreads = kMma ? DGB_MMA_THREADS(DGB_P) : kBlock;  // threads per block of k_element
 // dynamic shared memory (bytes): tables + per-warp staging buffers
-constexpr int kSmem = kMma ? (MmaDim<DGB_P>::kSize + (kThreads / 32) * MmaDim<DGB_P>::kWarpBuf) * 8
+constexpr int kSmem = kMma ? (MmaDim<DGB_P>::kBufOff + (kThreads / 32) * MmaDim<DGB_P>::kWarpBuf) * 8
                             : (kG == 1 ? g1_pipe_bytes<DGB_P>() * kThreads : 0);
 
 // One instance per mode, numerical flux (geo.flux) and variant (kVar* bits, dg_kernels.cuh):
@@ -47,7 +47,7 @@ constexpr int kSmem = kMma ? (MmaDim<DGB_P>::kSize + (kThreads / 32) * MmaDim<DG
 template <int MODE, int FLUX, int VAR>
 __global__ void __launch_bounds__(kThreads, kMinB) k_element(Geo geo, StageArgs a) {
   if constexpr (kMma) {
-    extern __shared__ double smem[];
+    extern __shared__ __align__(128) double smem[];
     element_body_mma<DGB_P, MODE, FLUX, VAR>(c_tab, geo, a, smem);
   } else if constexpr (kG == 1) {
     element_body_g1<DGB_P, MODE, FLUX, VAR>(c_tab, geo, a);

@@ -5,6 +5,8 @@
 // reference's rk_step_ws / run_* loops (proj/src/solver.cpp:506-613) with a
 // device step loop: dt, stop rules and residuals stay on the GPU and the host
 // synchronises once per batch of steps.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -385,6 +387,11 @@ struct dgb_ctx {
   int64_t stage_launches = 0;
   std::vector<double> samples[6];  // per-launch device ms of each timer category since the last reset
 
+  // TMA tensor maps of the coefficient buffers the DMMA kernel reads (p >= 3): host cache
+  // keyed by the buffer address, the maps themselves in device memory (kMaxMaps slots)
+  std::vector<const double*> tm_keys;
+  DevBuf<CUtensorMap> tm_dev;
+
   // fused stage + limiter (p = 1, whole mesh; kernels_p1.cu k_stage_limit)
   int fuse_limit = -1;  // 1 fused stage + limiter launch, 0 two kernels, -1 by mesh size (kFuseMaxN)
   std::vector<int2> fz_range_h;  // per 32-element tile: first and last chunk holding a neighbour
@@ -541,7 +548,56 @@ void fill_tab(dgbk::Tab<P>& T, const dgb_tables_view* t) {
     for (int j = 0; j < NP; ++j) T.phm[q][j] = t->phi_edge_mid[q * NP + j];
 }
 
-cudaError_t launch_element(dgb_ctx* c, int mode, const StageArgs& a) {
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda link).
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
+constexpr int kMaxMaps = 16;
+
+// The device address of the tensor map of coefficient buffer `buf` ([4][np][ld] doubles, box
+// {8 elements, np modes, 4 variables}), encoded and uploaded on first use.  Columns past ld (a
+// tail tile) are zero-filled by the TMA unit.
+const void* tensor_map_of(dgb_ctx* c, const double* buf) {
+  if (!buf) return nullptr;
+  for (size_t i = 0; i < c->tm_keys.size(); ++i)
+    if (c->tm_keys[i] == buf) return c->tm_dev.p + i;
+  PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+  if (!enc) throw Fail{DGB_ERR_CUDA, "cuTensorMapEncodeTiled is unavailable"};
+  if (!c->tm_dev.p) c->tm_dev.alloc(kMaxMaps);
+  if (c->tm_keys.size() == static_cast<size_t>(kMaxMaps)) {  // buffers were reallocated: start over
+    CU(cudaStreamSynchronize(c->stream));
+    c->tm_keys.clear();
+  }
+  CUtensorMap m;
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(c->ld), static_cast<cuuint64_t>(c->np), 4};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(c->ld) * 8, static_cast<cuuint64_t>(c->np) * c->ld * 8};
+  const cuuint32_t box[3] = {8, static_cast<cuuint32_t>(c->np), 4};
+  const cuuint32_t es[3] = {1, 1, 1};
+  const CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(buf), dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Fail{DGB_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")"};
+  const size_t i = c->tm_keys.size();
+  c->tm_keys.push_back(buf);
+  CU(cudaMemcpyAsync(c->tm_dev.p + i, &m, sizeof(m), cudaMemcpyHostToDevice, c->stream));
+  return c->tm_dev.p + i;
+}
+
+cudaError_t launch_element(dgb_ctx* c, int mode, const StageArgs& a_in) {
+  StageArgs a = a_in;
+  // the DMMA kernel's own-tile TMA boxes start at column e0 + 8 k: 16-byte aligned for an even e0
+  // (run_steps splits partitions at an even column; every other launch starts at 0)
+  if (c->p >= 3 && (a.e0 & 1)) throw Fail{DGB_ERR_ARG, "DMMA stage launch at an odd first column"};
+  a.tm_in = c->p >= 3 ? tensor_map_of(c, a.in) : nullptr;
   switch (c->p) {
     case 1: return dgbk::Launch<1>::element(mode, 0, c->geo, a, c->stream);
     case 2: return dgbk::Launch<2>::element(mode, 0, c->geo, a, c->stream);
@@ -866,8 +922,10 @@ RunOut run_steps(dgb_ctx* c, const RunSpec& r) {
     c->fz_epoch = 0;
   }
   // interior elements [0, n_int) never read a halo column; boundary elements
-  // [n_int, N) do, and only they feed the peers
-  const int n_int = X ? c->n_int : c->N;
+  // [n_int, N) do, and only they feed the peers.  The split point is rounded down to an even
+  // column (an interior element computed after the halo wait is harmless): the DMMA kernel's
+  // TMA boxes start at e0 + 8 k and must be 16-byte aligned.
+  const int n_int = X ? (c->n_int & ~1) : c->N;
 
   const int cur0 = c->cur;
   reset_scalars(c, c->t);
