@@ -321,6 +321,11 @@ def run_b200(args, rank, world, local, pg):
                     legs[name] = fn(args, local, stream, hbm_gbs, fp64_tf)
                 except Exception as e:  # an informational leg must never break the headline
                     legs[name] = {"failed": repr(e)}
+        elif world > 1 and not args.no_legs:
+            try:
+                legs["c5"] = leg_c5_partitioned(args, rank, world, local, stream, pg, hbm_gbs, fp64_tf)
+            except Exception as e:  # an informational leg must never break the headline
+                legs["c5"] = {"failed": repr(e)}
 
     dom = max(per_order, key=lambda r: r["stage_kernel_ms_median"] * stages)
     line = {
@@ -462,6 +467,50 @@ def leg_c5(args, local, stream, hbm_gbs, fp64_tf):
                                  "stage_kernel_ms_median": k, "roofline": roofline(p, e, N, k, hbm_gbs, fp64_tf)})
     out["value"] = upd_tot / (ms_tot * 1e-3)
     out["unit"] = "DOF-updates/s/stage"
+    return out
+
+
+def leg_c5_partitioned(args, rank, world, local, stream, pg, hbm_gbs, fp64_tf):
+    """BASELINE configs[4] (C5) at N > 1: the 8M-triangle box (2000 x 2000, periodic, isentropic
+    vortex), p = 2..4, SSP-RK3, partitioned across the N ranks (contiguous strips, peer-memory
+    halo exchange fused into the stage kernel, CUDA IPC between the processes): strong scaling of a
+    fixed mesh, device-timed as the max over ranks.  The halo bytes per stage are the send lists'
+    element columns x 4 Np doubles, pushed by the stage kernel over NVLink P2P."""
+    from paper_1601_07944_b200 import _lib as L
+    from paper_1601_07944_b200 import dg2d
+    from paper_1601_07944_b200 import dist as D
+    n = args.c5_n
+    mesh = dg2d.generate_mesh(L.MESH_PERIODIC_BOX, n, n, 10.0, 10.0)
+    N, e = mesh.n_elements(), mesh.n_edges() / mesh.n_elements()
+    out = {"workload": f"periodic {n}x{n} box ({N} triangles) partitioned over {world} ranks, isentropic vortex, "
+                       "SSP-RK3, cfl 0.3", "scaling": "strong", "steps": args.steps, "per_order": []}
+    upd_tot, ms_tot = 0.0, 0.0
+    iv = dg2d.IsentropicVortex()
+    for p in [int(x) for x in args.c5_orders.split(",")]:
+        tb = dg2d.build_tables(p)
+        ctx = D.PartContext(mesh, tb, rank, world, options=dg2d.SolverOptions(scheme=L.SSP_RK3, cfl=0.3),
+                            device=local)
+        D.connect_process_group(ctx)
+        dg2d._check(L.lib.dgb_set_stream(ctx.handle, C.c_void_p(stream.cuda_stream)))
+        ctx.upload(L.SLOT_STATE, D.project_local(ctx, lambda xy: iv(xy)))
+        res = C.c_double()
+        dg2d._check(L.lib.dgb_run_fixed_steps(ctx.handle, L.SSP_RK3, 0.3, 0, args.warmup, C.byref(res), None))
+        ms, launches, st, _ = timed_run(ctx.handle, stream, L.SSP_RK3, 0.3, False, args.steps, pg, local)
+        info = ctx.info
+        ctx.close()
+        k = float(np.median(st))
+        upd = 4 * np_(p) * N * 3 * args.steps
+        upd_tot += upd
+        ms_tot += ms
+        out["per_order"].append({"p": p, "value": upd / (ms * 1e-3), "ms_per_step": ms / args.steps,
+                                 "stage_kernel_ms_median_rank0": k, "owned_rank0": int(info.n_owned),
+                                 "halo_rank0": int(info.n_halo),
+                                 "halo_bytes_per_stage_rank0": int(info.n_halo) * 4 * np_(p) * 8,
+                                 "launches_per_step": launches / args.steps,
+                                 "roofline_rank0": roofline(p, e, int(info.n_owned), k, hbm_gbs, fp64_tf)})
+    out["value"] = upd_tot / (ms_tot * 1e-3)
+    out["unit"] = "DOF-updates/s/stage"
+    out["exchange"] = "CUDA IPC peer mappings (dgb_part_attach_peer_ipc); halo columns written by the stage kernel"
     return out
 
 
