@@ -569,7 +569,7 @@ def cpu_sample(orders, n, steps=2):
             "sample": f"one run_fixed_steps call of {steps} RK2 (midpoint) steps per order "
                       f"p={','.join(map(str, orders))} on the periodic {n}^2 box ({r['N']} triangles), the "
                       f"reference's own build (-O3 -march=native -fno-math-errno, OpenMP over {r['threads']} "
-                      "threads, OMP_PROC_BIND=close), no warm-up"}
+                      "threads, unbound: the reference runs its own worker pool), no warm-up"}
 
 
 def cpu_baseline(orders, args):
@@ -601,7 +601,7 @@ def run_reference(args, rank, world):
               f"p={args.orders} round robin, on the periodic {args.cpu_n}^2 box ({N} triangles); per order the best "
               f"of its {min(len(v) for v in r['all_s'].values())}+ timed calls; the reference's own build "
               f"({r['so']}: -O3 -march=native -fno-math-errno) with OpenMP over {r['threads']} threads, "
-              "OMP_PROC_BIND=close")
+              "unbound (the reference runs its own worker pool))")
     return {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "DOF-updates/s/stage",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -629,7 +629,7 @@ def main():
     ap.add_argument("--cfl", type=float, default=0.3)
     ap.add_argument("--e2e-steps", type=int, default=16)
     ap.add_argument("--cpu-box", dest="cpu_n", type=int, default=708, help="box size of the CPU sample")
-    ap.add_argument("--ref-steps", type=int, default=5, help="RK2 steps per reference run_fixed_steps call")
+    ap.add_argument("--ref-steps", type=int, default=3, help="RK2 steps per reference run_fixed_steps call")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--dmr-nx", type=int, default=2000, help="DMR channel cells in x (C4 leg)")
     ap.add_argument("--c3-level", type=int, default=6, help="supersonic-vortex mesh level of the C3 leg")
