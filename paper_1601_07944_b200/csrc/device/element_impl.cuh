@@ -539,17 +539,227 @@ __device__ __forceinline__ bool stage_prologue(const StageArgs& a, Scalars* sc, 
 //   kModeSurface -> per-side surface integrals into the slot buffer (eval_surface_pass)
 //   kModeRhs     -> (volume + surface) / det (compute_rhs)
 //   kModeStage   -> RK stage update with the fused epilogues
+// The work of one element in the four-lane form (lane g = conserved variable g): element_body
+// grid-strides over it, the fused latency-form stage + limiter kernel (kernels_p1.cu) calls it
+// per scheduled 8-element subtile.
 template <int P, int MODE, int FLUX, int VAR>
-__device__ __forceinline__ void element_body(const Tab<P>& T, const Geo& geo, const StageArgs& a) {
+__device__ __forceinline__ void g4_element(const Tab<P>& T, const Geo& geo, const StageArgs& a, int e, bool valid,
+                                           int g, double dt, double tstage, double& lam_min, double& res_max) {
   constexpr int NP = Dim<P>::NP, NQ = Dim<P>::NQ, K = Dim<P>::K;
   const long long ld = geo.ld;
-  const int gsize = ((a.e1 - a.e0 + 31) & ~31) * 4;  // whole warps (8 elements each), whole blocks
-  const int stride = gridDim.x * blockDim.x;
   const double gamma = geo.gamma, g1 = gamma - 1.0;
   Scalars* sc = a.sc;
-  // instance variant (kernels_tu.cuh): paths the launch knows are unused compile away
   constexpr bool RK4 = VAR & kVarRk4, LAM = VAR & kVarLambda, BND = VAR & kVarBoundary;
   const int kmode = RK4 ? a.kmode : 0;
+  const bool want_lambda = LAM && a.want_lambda;
+  {
+  const long long row = static_cast<long long>(g) * NP * ld + e;  // (g, j=0, e)
+
+  double c[NP];
+#pragma unroll
+  for (int j = 0; j < NP; ++j) c[j] = __ldg(a.in + row + j * ld);
+  double acc[NP];
+#pragma unroll
+  for (int j = 0; j < NP; ++j) acc[j] = 0.0;
+
+  // ------------------------------------------------------------ volume
+  if constexpr (MODE != kModeSurface) {
+    const double ta = __ldg(geo.tau + e), tb = __ldg(geo.tau + ld + e);
+    const double tc = __ldg(geo.tau + 2 * ld + e), td = __ldg(geo.tau + 3 * ld + e);
+#pragma unroll kVolUnroll
+    for (int k0 = 0; k0 < NQ; k0 += 4) {
+      const int nk = (NQ - k0) < 4 ? (NQ - k0) : 4;
+      double v[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (i < nk) {
+          double s = T.phi[k0 + i][0] * c[0];
+#pragma unroll
+          for (int j = 1; j < NP; ++j) s = fma(T.phi[k0 + i][j], c[j], s);
+          v[i] = s;
+        } else {
+          v[i] = v[0];  // padding lane: duplicate of a real point
+        }
+      }
+      transpose4(v, g);  // lane g: full state at point k0 + g
+      Prim w = primitives(v, g1);
+      if (!admissible(v, w)) {
+        if (valid && g < nk) record_error(sc, err_key(a.seq, kPassVolume, __ldg(geo.ref_id + e), k0 + g));
+        v[0] = 1.0; v[1] = 0.0; v[2] = 0.0; v[3] = 2.5;  // placeholder (solver.cpp:129-132)
+        w.inv = 1.0; w.vx = 0.0; w.vy = 0.0; w.p = 1.0;
+      }
+      double fr[4], fs[4];  // contravariant fluxes along r and s
+      contravariant_flux(v, w, ta, tb, tc, td, fr, fs);
+      transpose4(fr, g);  // lane g: variable g at points k0..k0+3
+      transpose4(fs, g);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (i < nk) {
+#pragma unroll
+          for (int j = 0; j < NP; ++j) acc[j] = fma(T.drw[k0 + i][j], fr[i], fma(T.dsw[k0 + i][j], fs[i], acc[j]));
+        }
+      }
+    }
+  }
+
+  // ------------------------------------------------------------ surface
+  double snx[3], sny[3];
+  if constexpr (MODE != kModeVolume) {
+    const int inf = __ldg(geo.info + e);
+#pragma unroll kSideUnroll
+    for (int q = 0; q < 3; ++q) {
+      const int nb = __ldg(geo.nbr + q * ld + e);
+      const int ed = __ldg(geo.eid + q * ld + e);
+      const int snb = (inf >> (2 * q)) & 3;
+      const bool left = (inf >> (6 + q)) & 1;
+      const double nx = __ldg(geo.enx + ed), ny = __ldg(geo.eny + ed), h = __ldg(geo.eh + ed);
+      snx[q] = nx;
+      sny[q] = ny;
+      const bool bnd = nb < 0;
+
+      double un[K][1];
+      if (!bnd) {
+        switch (snb) {
+          case 1: neighbour_trace<P, 0, 1>(T, a.in, ld, g, nb, un); break;
+          case 2: neighbour_trace<P, 1, 1>(T, a.in, ld, g, nb, un); break;
+          default: neighbour_trace<P, 2, 1>(T, a.in, ld, g, nb, un); break;
+        }
+      } else {
+#pragma unroll
+        for (int ko = 0; ko < K; ++ko) un[ko][0] = 0.0;
+      }
+      double uo[K];
+#pragma unroll
+      for (int ko = 0; ko < K; ++ko) {
+        double s = T.phe[q][ko][0] * c[0];
+#pragma unroll
+        for (int j = 1; j < NP; ++j) s = fma(T.phe[q][ko][j], c[j], s);
+        uo[ko] = s;
+      }
+      if constexpr (MODE == kModeSurface) {
+#pragma unroll
+        for (int j = 0; j < NP; ++j) acc[j] = 0.0;
+      }
+#pragma unroll
+      for (int k0 = 0; k0 < K; k0 += 4) {
+        const int nk = (K - k0) < 4 ? (K - k0) : 4;
+        double UL[4], UR[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int ko = (i < nk) ? k0 + i : k0;
+          UL[i] = left ? uo[ko] : un[ko][0];
+          UR[i] = left ? un[ko][0] : uo[ko];
+        }
+        transpose4(UL, g);  // lane g: full traces at own point k0 + g
+        transpose4(UR, g);
+        const int ko = (g < nk) ? k0 + g : k0;
+        const int kc = left ? ko : K - 1 - ko;  // canonical (left-element) point index
+        if (BND && bnd) ghost_state<K>(UL, nb, ed, kc, nx, ny, tstage, geo, UR);
+        const Prim wl = primitives(UL, g1), wr = primitives(UR, g1);
+        const double wl_ = h * pick_weight<K>(T.we, kc);
+        double fn[4];
+        if (admissible(UL, wl) && admissible(UR, wr)) {
+          num_flux_w<FLUX>(UL, wl, UR, wr, nx, ny, gamma, left ? -wl_ : wl_, fn);
+        } else {
+          if (valid && g < nk) record_error(sc, err_key(a.seq, kPassSurface, ed, kc));
+#pragma unroll
+          for (int m = 0; m < 4; ++m) fn[m] = 0.0;
+        }
+        transpose4(fn, g);  // lane g: weighted flux of variable g at points k0..k0+3
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (i < nk) {
+#pragma unroll
+            for (int j = 0; j < NP; ++j) acc[j] = fma(fn[i], T.phe[q][k0 + i][j], acc[j]);
+          }
+        }
+      }
+      if constexpr (MODE == kModeSurface) {
+        if (valid) {
+#pragma unroll
+          for (int j = 0; j < NP; ++j) a.out[(static_cast<long long>(q) * 4 * NP + g * NP + j) * ld + e] = acc[j];
+        }
+      }
+    }
+  }
+
+  // ------------------------------------------------------------ outputs
+  if constexpr (MODE == kModeVolume) {
+    if (valid) {
+#pragma unroll
+      for (int j = 0; j < NP; ++j) a.out[row + j * ld] = acc[j];
+    }
+  } else if constexpr (MODE == kModeRhs) {
+    const double idet = __ldg(geo.inv_det + e);
+    if (valid) {
+#pragma unroll
+      for (int j = 0; j < NP; ++j) a.out[row + j * ld] = acc[j] * idet;
+    }
+  } else if constexpr (MODE == kModeStage) {
+    const double idet = __ldg(geo.inv_det + e);
+    const double gdt = a.gcoef * dt;
+    const double dt6 = dt / 6.0;
+    const bool need_u = a.alpha != 0.0 || a.want_resid || kmode == 3;
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
+      const long long idx = row + j * ld;
+      const double d = acc[j] * idet;
+      const double uu = need_u ? __ldg(a.u + idx) : 0.0;
+      double o;
+      if (kmode == 3) {
+        o = fma(dt6, __ldg(a.kacc + idx) + d, uu);
+      } else {
+        const double base = (a.alpha != 0.0) ? fma(a.alpha, uu, a.beta * c[j]) : a.beta * c[j];
+        o = fma(gdt, d, base);
+        if (kmode == 1 && valid) a.kacc[idx] = d;
+        if (kmode == 2 && valid) a.kacc[idx] = fma(2.0, d, a.kacc[idx]);
+      }
+      if (valid) {
+        a.out[idx] = o;
+        if (a.want_resid) res_max = std_max(res_max, fabs(uu - o));
+      }
+      acc[j] = o;  // keep the new stage for the CFL epilogue
+    }
+    if (a.push && valid && e >= geo.send_begin) {
+      const double(&v)[1][NP] = reinterpret_cast<const double(&)[1][NP]>(acc);
+      push_element<NP, 1>(geo, a.peers, a.out_buf, e, g, v);
+    }
+    if (want_lambda) {
+      double v[4];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        double s = T.phm[q][0] * acc[0];
+#pragma unroll
+        for (int j = 1; j < NP; ++j) s = fma(T.phm[q][j], acc[j], s);
+        v[q] = s;
+      }
+      v[3] = v[0];
+      transpose4(v, g);  // lane q < 3: state at the midpoint of side q
+      const double nxq = g == 0 ? snx[0] : (g == 1 ? snx[1] : snx[2]);
+      const double nyq = g == 0 ? sny[0] : (g == 1 ? sny[1] : sny[2]);
+      double lam = 0.0;
+      bool ok;
+      const double ws = wave_speed_ieee(v, nxq, nyq, gamma, ok);
+      if (ok) {
+        lam = ws;
+      } else if (valid && g < 3) {
+        record_error(sc, err_key(a.seq_next, kPassDt, __ldg(geo.ref_id + e), g + 1));
+      }
+      if (g == 3) lam = 0.0;
+      lam = std_max(lam, __shfl_xor_sync(kFull, lam, 1));
+      lam = std_max(lam, __shfl_xor_sync(kFull, lam, 2));
+      if (valid && g == 0) lam_min = std_min(lam_min, 2.0 * __ldg(geo.inradius + e) / ((2.0 * P + 1.0) * lam));
+    }
+  }
+  }
+}
+
+template <int P, int MODE, int FLUX, int VAR>
+__device__ __forceinline__ void element_body(const Tab<P>& T, const Geo& geo, const StageArgs& a) {
+  const int gsize = ((a.e1 - a.e0 + 31) & ~31) * 4;  // whole warps (8 elements each), whole blocks
+  const int stride = gridDim.x * blockDim.x;
+  Scalars* sc = a.sc;
+  constexpr bool LAM = VAR & kVarLambda;
   const bool want_lambda = LAM && a.want_lambda;
 
   // block-uniform early exit: an error or a stop rule fired in an earlier launch
@@ -573,204 +783,7 @@ __device__ __forceinline__ void element_body(const Tab<P>& T, const Geo& geo, co
     int e = a.e0 + (tid >> 2);
     const bool valid = e < a.e1;
     if (!valid) e = a.e1 - 1;
-    const long long row = static_cast<long long>(g) * NP * ld + e;  // (g, j=0, e)
-
-    double c[NP];
-#pragma unroll
-    for (int j = 0; j < NP; ++j) c[j] = __ldg(a.in + row + j * ld);
-    double acc[NP];
-#pragma unroll
-    for (int j = 0; j < NP; ++j) acc[j] = 0.0;
-
-    // ------------------------------------------------------------ volume
-    if constexpr (MODE != kModeSurface) {
-      const double ta = __ldg(geo.tau + e), tb = __ldg(geo.tau + ld + e);
-      const double tc = __ldg(geo.tau + 2 * ld + e), td = __ldg(geo.tau + 3 * ld + e);
-#pragma unroll kVolUnroll
-      for (int k0 = 0; k0 < NQ; k0 += 4) {
-        const int nk = (NQ - k0) < 4 ? (NQ - k0) : 4;
-        double v[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          if (i < nk) {
-            double s = T.phi[k0 + i][0] * c[0];
-#pragma unroll
-            for (int j = 1; j < NP; ++j) s = fma(T.phi[k0 + i][j], c[j], s);
-            v[i] = s;
-          } else {
-            v[i] = v[0];  // padding lane: duplicate of a real point
-          }
-        }
-        transpose4(v, g);  // lane g: full state at point k0 + g
-        Prim w = primitives(v, g1);
-        if (!admissible(v, w)) {
-          if (valid && g < nk) record_error(sc, err_key(a.seq, kPassVolume, __ldg(geo.ref_id + e), k0 + g));
-          v[0] = 1.0; v[1] = 0.0; v[2] = 0.0; v[3] = 2.5;  // placeholder (solver.cpp:129-132)
-          w.inv = 1.0; w.vx = 0.0; w.vy = 0.0; w.p = 1.0;
-        }
-        double fr[4], fs[4];  // contravariant fluxes along r and s
-        contravariant_flux(v, w, ta, tb, tc, td, fr, fs);
-        transpose4(fr, g);  // lane g: variable g at points k0..k0+3
-        transpose4(fs, g);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          if (i < nk) {
-#pragma unroll
-            for (int j = 0; j < NP; ++j) acc[j] = fma(T.drw[k0 + i][j], fr[i], fma(T.dsw[k0 + i][j], fs[i], acc[j]));
-          }
-        }
-      }
-    }
-
-    // ------------------------------------------------------------ surface
-    double snx[3], sny[3];
-    if constexpr (MODE != kModeVolume) {
-      const int inf = __ldg(geo.info + e);
-#pragma unroll kSideUnroll
-      for (int q = 0; q < 3; ++q) {
-        const int nb = __ldg(geo.nbr + q * ld + e);
-        const int ed = __ldg(geo.eid + q * ld + e);
-        const int snb = (inf >> (2 * q)) & 3;
-        const bool left = (inf >> (6 + q)) & 1;
-        const double nx = __ldg(geo.enx + ed), ny = __ldg(geo.eny + ed), h = __ldg(geo.eh + ed);
-        snx[q] = nx;
-        sny[q] = ny;
-        const bool bnd = nb < 0;
-
-        double un[K][1];
-        if (!bnd) {
-          switch (snb) {
-            case 1: neighbour_trace<P, 0, 1>(T, a.in, ld, g, nb, un); break;
-            case 2: neighbour_trace<P, 1, 1>(T, a.in, ld, g, nb, un); break;
-            default: neighbour_trace<P, 2, 1>(T, a.in, ld, g, nb, un); break;
-          }
-        } else {
-#pragma unroll
-          for (int ko = 0; ko < K; ++ko) un[ko][0] = 0.0;
-        }
-        double uo[K];
-#pragma unroll
-        for (int ko = 0; ko < K; ++ko) {
-          double s = T.phe[q][ko][0] * c[0];
-#pragma unroll
-          for (int j = 1; j < NP; ++j) s = fma(T.phe[q][ko][j], c[j], s);
-          uo[ko] = s;
-        }
-        if constexpr (MODE == kModeSurface) {
-#pragma unroll
-          for (int j = 0; j < NP; ++j) acc[j] = 0.0;
-        }
-#pragma unroll
-        for (int k0 = 0; k0 < K; k0 += 4) {
-          const int nk = (K - k0) < 4 ? (K - k0) : 4;
-          double UL[4], UR[4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int ko = (i < nk) ? k0 + i : k0;
-            UL[i] = left ? uo[ko] : un[ko][0];
-            UR[i] = left ? un[ko][0] : uo[ko];
-          }
-          transpose4(UL, g);  // lane g: full traces at own point k0 + g
-          transpose4(UR, g);
-          const int ko = (g < nk) ? k0 + g : k0;
-          const int kc = left ? ko : K - 1 - ko;  // canonical (left-element) point index
-          if (BND && bnd) ghost_state<K>(UL, nb, ed, kc, nx, ny, tstage, geo, UR);
-          const Prim wl = primitives(UL, g1), wr = primitives(UR, g1);
-          const double wl_ = h * pick_weight<K>(T.we, kc);
-          double fn[4];
-          if (admissible(UL, wl) && admissible(UR, wr)) {
-            num_flux_w<FLUX>(UL, wl, UR, wr, nx, ny, gamma, left ? -wl_ : wl_, fn);
-          } else {
-            if (valid && g < nk) record_error(sc, err_key(a.seq, kPassSurface, ed, kc));
-#pragma unroll
-            for (int m = 0; m < 4; ++m) fn[m] = 0.0;
-          }
-          transpose4(fn, g);  // lane g: weighted flux of variable g at points k0..k0+3
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            if (i < nk) {
-#pragma unroll
-              for (int j = 0; j < NP; ++j) acc[j] = fma(fn[i], T.phe[q][k0 + i][j], acc[j]);
-            }
-          }
-        }
-        if constexpr (MODE == kModeSurface) {
-          if (valid) {
-#pragma unroll
-            for (int j = 0; j < NP; ++j) a.out[(static_cast<long long>(q) * 4 * NP + g * NP + j) * ld + e] = acc[j];
-          }
-        }
-      }
-    }
-
-    // ------------------------------------------------------------ outputs
-    if constexpr (MODE == kModeVolume) {
-      if (valid) {
-#pragma unroll
-        for (int j = 0; j < NP; ++j) a.out[row + j * ld] = acc[j];
-      }
-    } else if constexpr (MODE == kModeRhs) {
-      const double idet = __ldg(geo.inv_det + e);
-      if (valid) {
-#pragma unroll
-        for (int j = 0; j < NP; ++j) a.out[row + j * ld] = acc[j] * idet;
-      }
-    } else if constexpr (MODE == kModeStage) {
-      const double idet = __ldg(geo.inv_det + e);
-      const double gdt = a.gcoef * dt;
-      const double dt6 = dt / 6.0;
-      const bool need_u = a.alpha != 0.0 || a.want_resid || kmode == 3;
-#pragma unroll
-      for (int j = 0; j < NP; ++j) {
-        const long long idx = row + j * ld;
-        const double d = acc[j] * idet;
-        const double uu = need_u ? __ldg(a.u + idx) : 0.0;
-        double o;
-        if (kmode == 3) {
-          o = fma(dt6, __ldg(a.kacc + idx) + d, uu);
-        } else {
-          const double base = (a.alpha != 0.0) ? fma(a.alpha, uu, a.beta * c[j]) : a.beta * c[j];
-          o = fma(gdt, d, base);
-          if (kmode == 1 && valid) a.kacc[idx] = d;
-          if (kmode == 2 && valid) a.kacc[idx] = fma(2.0, d, a.kacc[idx]);
-        }
-        if (valid) {
-          a.out[idx] = o;
-          if (a.want_resid) res_max = std_max(res_max, fabs(uu - o));
-        }
-        acc[j] = o;  // keep the new stage for the CFL epilogue
-      }
-      if (a.push && valid && e >= geo.send_begin) {
-        const double(&v)[1][NP] = reinterpret_cast<const double(&)[1][NP]>(acc);
-        push_element<NP, 1>(geo, a.peers, a.out_buf, e, g, v);
-      }
-      if (want_lambda) {
-        double v[4];
-#pragma unroll
-        for (int q = 0; q < 3; ++q) {
-          double s = T.phm[q][0] * acc[0];
-#pragma unroll
-          for (int j = 1; j < NP; ++j) s = fma(T.phm[q][j], acc[j], s);
-          v[q] = s;
-        }
-        v[3] = v[0];
-        transpose4(v, g);  // lane q < 3: state at the midpoint of side q
-        const double nxq = g == 0 ? snx[0] : (g == 1 ? snx[1] : snx[2]);
-        const double nyq = g == 0 ? sny[0] : (g == 1 ? sny[1] : sny[2]);
-        double lam = 0.0;
-        bool ok;
-        const double ws = wave_speed_ieee(v, nxq, nyq, gamma, ok);
-        if (ok) {
-          lam = ws;
-        } else if (valid && g < 3) {
-          record_error(sc, err_key(a.seq_next, kPassDt, __ldg(geo.ref_id + e), g + 1));
-        }
-        if (g == 3) lam = 0.0;
-        lam = std_max(lam, __shfl_xor_sync(kFull, lam, 1));
-        lam = std_max(lam, __shfl_xor_sync(kFull, lam, 2));
-        if (valid && g == 0) lam_min = std_min(lam_min, 2.0 * __ldg(geo.inradius + e) / ((2.0 * P + 1.0) * lam));
-      }
-    }
+    g4_element<P, MODE, FLUX, VAR>(T, geo, a, e, valid, g, dt, tstage, lam_min, res_max);
   }
 
   if constexpr (MODE == kModeStage) {

@@ -238,9 +238,31 @@ __device__ __forceinline__ void limit_element(const Geo& geo, const LimArgs& a, 
 // means and deviations by shuffles and every lane of the quad evaluates it redundantly (the same
 // operations on the same operands, so the same decision and factors); the CFL epilogue evaluates
 // midpoint q on lane q.  Bit-identical to limit_element (tests/test_gpu_parity.py).
-template <int NE, int NPT, int EPI>
+// The geometry limit_element4 reads (it does not depend on the state, so the fused kernel
+// requests it before waiting for the neighbours' stage output).
+struct LimGeo4 {
+  int nb[3];
+  double enx, eny, rin;
+};
+template <int EPI>
+__device__ __forceinline__ LimGeo4 lim_geo4(const Geo& geo, const LimArgs& a, int e, int v) {
+  LimGeo4 r;
+  const long long ld = geo.ld;
+#pragma unroll
+  for (int q = 0; q < 3; ++q) r.nb[q] = __ldg(geo.nbr + q * ld + e);
+  r.enx = r.eny = r.rin = 0.0;
+  if ((EPI & 1) && a.want_lambda) {  // CFL epilogue operands of midpoint q = v
+    const int ed = __ldg(geo.eid + (v < 3 ? v : 2) * ld + e);
+    r.rin = __ldg(geo.inradius + e);
+    r.enx = __ldg(geo.enx + ed);
+    r.eny = __ldg(geo.eny + ed);
+  }
+  return r;
+}
+
+template <int NE, int NPT, int EPI, bool Coherent = false>
 __device__ __forceinline__ void limit_element4(const Geo& geo, const LimArgs& a, int e, bool valid, int v,
-                                               double& lam_min, double& res_max) {
+                                               double& lam_min, double& res_max, const LimGeo4* pre = nullptr) {
   const bool want_lambda = (EPI & 1) && a.want_lambda, want_resid = (EPI & 2) && a.want_resid;
   constexpr int NP = 3;
   const long long ld = geo.ld;
@@ -253,22 +275,14 @@ __device__ __forceinline__ void limit_element4(const Geo& geo, const LimArgs& a,
   const int e_begin = NE ? NPT - NE - 3 : L.edge_begin;
   const int n_pts = NPT ? NPT : L.n_pts;
   const double* __restrict__ cv = a.c + static_cast<long long>(v) * NP * ld;
-  const double c0 = cv[e];
-  double c1 = cv[ld + e], c2 = cv[2 * ld + e];
-  int nb[3];
-#pragma unroll
-  for (int q = 0; q < 3; ++q) nb[q] = __ldg(geo.nbr + q * ld + e);
-  // CFL epilogue operands of midpoint q = v, requested with the neighbour means
-  double enx = 0.0, eny = 0.0, rin = 0.0;
-  if (want_lambda) {
-    const int ed = __ldg(geo.eid + (v < 3 ? v : 2) * ld + e);
-    rin = __ldg(geo.inradius + e);
-    enx = __ldg(geo.enx + ed);
-    eny = __ldg(geo.eny + ed);
-  }
+  const double c0 = lim_ld<Coherent>(cv + e);
+  double c1 = lim_ld<Coherent>(cv + ld + e), c2 = lim_ld<Coherent>(cv + 2 * ld + e);
+  const LimGeo4 gg = pre ? *pre : lim_geo4<EPI>(geo, a, e, v);
+  const int nb[3] = {gg.nb[0], gg.nb[1], gg.nb[2]};
+  const double enx = gg.enx, eny = gg.eny, rin = gg.rin;
   double nm[3];
 #pragma unroll
-  for (int q = 0; q < 3; ++q) nm[q] = nb[q] >= 0 ? __ldg(cv + nb[q]) : 0.0;
+  for (int q = 0; q < 3; ++q) nm[q] = nb[q] >= 0 ? lim_ldg<Coherent>(cv + nb[q]) : 0.0;
 
   // Barth-Jespersen of variable v (limit_element, loop body for m = v)
   {
@@ -519,6 +533,69 @@ __global__ void __launch_bounds__(kBlock, DGB_FUSE_MINB) k_stage_limit(Geo geo, 
   if ((EPI & 2) && la.want_resid) block_reduce_atomic<false>(res_max, &sc->resid[par]);
 }
 
+// Latency form of k_stage_limit for small meshes (a grid with one warp per 8-element subtile):
+// warp w runs the stage of subtile w first (four lanes per element, g4_element), then limiter
+// subtiles w, w + W, ... (four lanes per element, limit_element4), each once the chunks holding
+// its neighbours have published (4 subtiles per 32-element tile).  Stage parts never wait and
+// every warp is resident, so no warp waits on work that cannot start.  Bit-identical to the
+// other forms.
+template <int FLUX, int VAR, int EPI>
+__global__ void __launch_bounds__(kBlock, DGB_FUSE_MINB) k_stage_limit4(Geo geo, StageArgs a, LimArgs la,
+                                                                       FuseArgs f) {
+  __shared__ int s_stop;
+  Scalars* sc = a.sc;
+  if (threadIdx.x == 0) {
+    const unsigned long long k = sc->err_key;
+    s_stop = ((k != kNoError && (k >> 38) < a.seq) || sc->halt) ? 1 : 0;
+  }
+  __syncthreads();
+  double t0 = a.t_host, dt = 0.0;
+  const bool run = !s_stop && stage_prologue(a, sc, t0, dt);
+  const double tstage = fma(a.tcoef, dt, t0);
+  double lam_min = __longlong_as_double(0x7ff0000000000000ll), res_max = 0.0;
+  double st_lam = lam_min, st_res = 0.0;
+  const int lane = threadIdx.x & 31;
+  const int W = gridDim.x * (blockDim.x >> 5);
+  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  bool timed_out = false;
+  if (run) {
+    if (w < 4 * f.n_tiles) {
+      int e = a.e0 + w * 8 + (lane >> 2);
+      const bool valid = e < a.e1;
+      if (!valid) e = a.e1 - 1;
+      g4_element<1, kModeStage, FLUX, VAR>(c_tab, geo, a, e, valid, lane & 3, dt, tstage, st_lam, st_res);
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) atomicAdd(f.count + (w >> 2) / kFuseChunk, 1ull);
+    }
+    for (int j4 = w; j4 < 4 * f.n_tiles; j4 += W) {
+      int e = la.e0 + j4 * 8 + (lane >> 2);
+      const bool valid = e < la.e1;
+      if (!valid) e = la.e1 - 1;
+      const LimGeo4 gg = lim_geo4<EPI>(geo, la, e, lane & 3);  // in flight during the wait
+      const int2 r = __ldg(f.range + (j4 >> 2));
+      for (int c = r.x + lane; c <= r.y; c += 32) {
+        const unsigned long long need = 4 * f.epoch * min(kFuseChunk, f.n_tiles - c * kFuseChunk);
+        long long spins = 0;
+        while (ld_acquire_gpu(f.count + c) < need) {
+          __nanosleep(32);
+          if (++spins > (1ll << 26)) {
+            timed_out = true;
+            break;
+          }
+        }
+      }
+      __syncwarp();
+      __threadfence();
+      limit_element4<kLimNE, kLimNPT, EPI, true>(geo, la, e, valid, lane & 3, lam_min, res_max, &gg);
+    }
+  }
+  if (timed_out) record_error(sc, kFuseTimeoutKey);
+  const int par = la.step & 1;
+  if ((EPI & 1) && la.want_lambda) block_reduce_atomic<true>(lam_min, &sc->dtmin[par ^ 1]);
+  if ((EPI & 2) && la.want_resid) block_reduce_atomic<false>(res_max, &sc->resid[par]);
+}
+
 // host copy of (n_edge, n_pts) of the table uploaded to each device's bank (packed in one
 // atomic word: the limiter may be launched from several host threads)
 std::atomic<int> g_lim_pts[kMaxDevices];
@@ -572,11 +649,38 @@ cudaError_t launch_stage_limit(int grid, const Geo& g, const StageArgs& a, const
   const int var = (g.has_bnd ? kVarBoundary : 0) | (a.kmode != 0 ? kVarRk4 : 0);
   const bool last = la.want_lambda || la.want_resid;
   cudaError_t err = cudaSuccess;
+  // latency form: one warp per stage tile and per 8-element limiter subtile fit in one wave
+  const int wpb = kBlock / 32;
+  const bool lat = f.n_tiles > 0 && 4 * f.n_tiles <= stage_limit_grid() * wpb &&
+                   (g.lat_limit_n >= 0 ? a.e1 - a.e0 <= g.lat_limit_n : true);
+  if (lat) grid = (4 * f.n_tiles + wpb - 1) / wpb;
   auto go = [&](auto k) {  // cooperative: every warp of the grid is resident (the tiles' waits need it)
     void* args[] = {const_cast<Geo*>(&g), const_cast<StageArgs*>(&a), const_cast<LimArgs*>(&la),
                     const_cast<FuseArgs*>(&f)};
     err = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k), dim3(grid), dim3(kBlock), args, 0, s);
   };
+  if (lat) {
+    const bool roe = g.flux == kFluxRoe;
+    switch (var | (last ? 8 : 0) | (roe ? 16 : 0)) {
+      case 0: go(k_stage_limit4<kFluxLLF, 0, 0>); break;
+      case 1: go(k_stage_limit4<kFluxLLF, 1, 0>); break;
+      case 4: go(k_stage_limit4<kFluxLLF, 4, 0>); break;
+      case 5: go(k_stage_limit4<kFluxLLF, 5, 0>); break;
+      case 8: go(k_stage_limit4<kFluxLLF, 0, 3>); break;
+      case 9: go(k_stage_limit4<kFluxLLF, 1, 3>); break;
+      case 12: go(k_stage_limit4<kFluxLLF, 4, 3>); break;
+      case 13: go(k_stage_limit4<kFluxLLF, 5, 3>); break;
+      case 16: go(k_stage_limit4<kFluxRoe, 0, 0>); break;
+      case 17: go(k_stage_limit4<kFluxRoe, 1, 0>); break;
+      case 20: go(k_stage_limit4<kFluxRoe, 4, 0>); break;
+      case 21: go(k_stage_limit4<kFluxRoe, 5, 0>); break;
+      case 24: go(k_stage_limit4<kFluxRoe, 0, 3>); break;
+      case 25: go(k_stage_limit4<kFluxRoe, 1, 3>); break;
+      case 28: go(k_stage_limit4<kFluxRoe, 4, 3>); break;
+      default: go(k_stage_limit4<kFluxRoe, 5, 3>); break;
+    }
+    return err;
+  }
   if (g.flux == kFluxRoe) {
     switch (var | (last ? 8 : 0)) {
       case 0: go(k_stage_limit<kFluxRoe, 0, 0>); break;
