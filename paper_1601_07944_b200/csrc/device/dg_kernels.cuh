@@ -132,6 +132,7 @@ struct StageArgs {
   const double* __restrict__ u;   // u^n (for alpha, residual, rk4 combine)
   double* __restrict__ out;       // output (volume / slots / deriv / next stage)
   double* __restrict__ kacc;      // RK4 derivative accumulator
+  double* __restrict__ means;     // p <= 2 with a limiter kernel next: the new cell means, [ld][4] (null: none)
   double alpha, beta, gcoef;      // out = alpha u + beta in + (gcoef dt) L(in)
   double tcoef;                   // stage time = t + tcoef dt
   int kmode;                      // 0 none, 1 kacc = L, 2 kacc += 2L, 3 out = u + dt/6 (kacc + L)
@@ -173,6 +174,7 @@ struct FuseArgs {
 
 struct LimArgs {
   double* __restrict__ c;         // limited in place
+  const double* __restrict__ means;  // the stage kernel's compact copy of c's mode 0, [ld][4] (null: read c)
   const double* __restrict__ u;   // for the residual (final limit)
   int step, want_lambda, want_resid;
   unsigned long long seq;         // error key for the CFL epilogue (next step)

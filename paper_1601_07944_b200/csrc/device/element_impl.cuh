@@ -720,6 +720,7 @@ __device__ __forceinline__ void g4_element(const Tab<P>& T, const Geo& geo, cons
       }
       acc[j] = o;  // keep the new stage for the CFL epilogue
     }
+    if (a.means && valid) a.means[4 * static_cast<long long>(e) + g] = acc[0];
     if (a.push && valid && e >= geo.send_begin) {
       const double(&v)[1][NP] = reinterpret_cast<const double(&)[1][NP]>(acc);
       push_element<NP, 1>(geo, a.peers, a.out_buf, e, g, v);
@@ -1039,6 +1040,11 @@ __device__ __forceinline__ void g1_element(const Tab<P>& T, const Geo& geo, cons
           if (a.want_resid) res_max = std_max(res_max, fabs(uu - o));
           acc[m][j] = o;
         }
+      }
+      if (a.means) {  // the limiter's neighbour means as one 32-byte sector per element
+        double2* mp = reinterpret_cast<double2*>(a.means + 4 * static_cast<long long>(e));
+        mp[0] = make_double2(acc[0][0], acc[1][0]);
+        mp[1] = make_double2(acc[2][0], acc[3][0]);
       }
       if (a.push && e >= geo.send_begin) push_element<NP, 4>(geo, a.peers, a.out_buf, e, 0, acc);
       if (want_lambda) {

@@ -87,10 +87,22 @@ __device__ __forceinline__ void limit_element(const Geo& geo, const LimArgs& a, 
     // the neighbours' means, all requested at once (mode 0 is never written here,
     // so the read-only path is safe)
     double nm[3][4];
+    if (!Coherent && a.means) {  // the same values from the stage kernel's compact means: 2 loads per neighbour
 #pragma unroll
-    for (int q = 0; q < 3; ++q)
+      for (int q = 0; q < 3; ++q) {
+        const double2* mp = reinterpret_cast<const double2*>(a.means + 4 * static_cast<long long>(nb[q] >= 0 ? nb[q] : e));
+        const double2 lo = __ldg(mp), hi = __ldg(mp + 1);
+        nm[q][0] = nb[q] >= 0 ? lo.x : 0.0;
+        nm[q][1] = nb[q] >= 0 ? lo.y : 0.0;
+        nm[q][2] = nb[q] >= 0 ? hi.x : 0.0;
+        nm[q][3] = nb[q] >= 0 ? hi.y : 0.0;
+      }
+    } else {
 #pragma unroll
-      for (int m = 0; m < 4; ++m) nm[q][m] = nb[q] >= 0 ? lim_ldg<Coherent>(a.c + (m * NP) * ld + nb[q]) : 0.0;
+      for (int q = 0; q < 3; ++q)
+#pragma unroll
+        for (int m = 0; m < 4; ++m) nm[q][m] = nb[q] >= 0 ? lim_ldg<Coherent>(a.c + (m * NP) * ld + nb[q]) : 0.0;
+    }
 #if DGB_LIMIT_CFL_PREFETCH
     if (want_lambda) {
 #pragma unroll

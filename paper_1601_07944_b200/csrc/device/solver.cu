@@ -363,6 +363,7 @@ struct dgb_ctx {
 
   // coefficient buffers (device order [4][np][ld])
   DevBuf<double> state[2], input, volume, deriv, stage[2], kacc, slots, staging, hist, staging_in, staging_out;
+  DevBuf<double> means;  // [ld][4] cell means of the last stage output (two-kernel limiter path)
   int cur = 0;
   Scalars* d_sc = nullptr;
   Scalars* h_sc = nullptr;  // pinned mirror
@@ -921,6 +922,15 @@ RunOut run_steps(dgb_ctx* c, const RunSpec& r) {
     CU(cudaMemsetAsync(c->fz_count.p, 0, nch * sizeof(unsigned long long), c->stream));
     c->fz_epoch = 0;
   }
+  // two-kernel limiting on a whole mesh: the stage kernel also writes the new cell means as one
+  // 32-byte record per element, the limiter gathers its neighbours' means from it (one sector
+  // per neighbour instead of four); a partition keeps reading the coefficient columns (its halo
+  // columns arrive through the coefficient push)
+  double* means_buf = nullptr;
+  if (r.limiting && !fused && !c->partitioned) {
+    if (c->means.n < static_cast<size_t>(4) * c->ld) c->means.alloc(static_cast<size_t>(4) * c->ld);
+    means_buf = c->means.p;
+  }
   // interior elements [0, n_int) never read a halo column; boundary elements
   // [n_int, N) do, and only they feed the peers.  The split point is rounded down to an even
   // column (an interior element computed after the halo wait is harmless): the DMMA kernel's
@@ -959,6 +969,7 @@ RunOut run_steps(dgb_ctx* c, const RunSpec& r) {
         a.u = u;
         a.out = last ? unext : c->stage[k & 1].p;
         a.kacc = c->kacc.p;
+        a.means = means_buf;
         a.alpha = st[k].alpha;
         a.beta = st[k].beta;
         a.gcoef = st[k].gcoef;
@@ -1036,6 +1047,7 @@ RunOut run_steps(dgb_ctx* c, const RunSpec& r) {
           la.step = static_cast<int>(s);
           la.want_lambda = last && r.dt_mode == 1;
           la.want_resid = last && resid;
+          la.means = means_buf;
           la.seq = static_cast<unsigned long long>(s + 1) * 8;
           la.sc = c->d_sc;
           la.peers = c->d_peers;
