@@ -223,6 +223,39 @@ __device__ __forceinline__ void num_flux_w(const double (&UL)[4], const Prim& wl
   }
 }
 
+// num_flux_w from the element's own view: UO = its own trace, UN = the neighbour's (or the
+// ghost state), wmag = h w_k > 0, `left` = the element is the edge's left (canonical) element.
+// LLF needs no orientation selects: with the canonical operands UL, UR = (UO, UN) or (UN, UO),
+// F(UL).n + F(UR).n and max(s_L, s_R) are symmetric, U_R - U_L = +-(UN - UO) exactly, and
+// fma(-p, q, c) = fma(p, -q, c) exactly, so cf = fma(hs wmag, UN - UO, +-(wmag/2)(F(UO).n + F(UN).n))
+// is bitwise the value num_flux_w gives on the canonical operands.  Roe is not symmetric in its
+// operand order and keeps the canonical selects.
+template <int FLUX>
+__device__ __forceinline__ void num_flux_own(const double (&UO)[4], const Prim& wo, const double (&UN)[4],
+                                             const Prim& wn, double nx, double ny, double gamma, double wmag,
+                                             bool left, double (&cf)[4]) {
+  if constexpr (FLUX == kFluxRoe) {
+    double UL[4], UR[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      UL[m] = left ? UO[m] : UN[m];
+      UR[m] = left ? UN[m] : UO[m];
+    }
+    const Prim wl = left ? wo : wn, wr = left ? wn : wo;
+    num_flux_w<FLUX>(UL, wl, UR, wr, nx, ny, gamma, left ? -wmag : wmag, cf);
+  } else {
+    double fo[4], fn[4], vno, vnn;
+    normal_flux(UO, wo, nx, ny, vno, fo);
+    normal_flux(UN, wn, nx, ny, vnn, fn);
+    const double so = fabs(vno) + sqrt_nr(gamma * wo.p * wo.inv);
+    const double sn = fabs(vnn) + sqrt_nr(gamma * wn.p * wn.inv);
+    const double b = (0.5 * std_max(so, sn)) * wmag;  // std::max as euler.hpp:64
+    const double a = left ? -(0.5 * wmag) : 0.5 * wmag;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) cf[m] = fma(b, UN[m] - UO[m], a * (fo[m] + fn[m]));
+  }
+}
+
 __device__ __forceinline__ void reflect(const double (&u)[4], double nx, double ny, double (&g)[4]) {
   const double mn = 2.0 * (u[1] * nx + u[2] * ny);
   g[0] = u[0];
@@ -643,23 +676,23 @@ __device__ __forceinline__ void g4_element(const Tab<P>& T, const Geo& geo, cons
 #pragma unroll
       for (int k0 = 0; k0 < K; k0 += 4) {
         const int nk = (K - k0) < 4 ? (K - k0) : 4;
-        double UL[4], UR[4];
+        double UO[4], UN[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int ko = (i < nk) ? k0 + i : k0;
-          UL[i] = left ? uo[ko] : un[ko][0];
-          UR[i] = left ? un[ko][0] : uo[ko];
+          UO[i] = uo[ko];
+          UN[i] = un[ko][0];
         }
-        transpose4(UL, g);  // lane g: full traces at own point k0 + g
-        transpose4(UR, g);
+        transpose4(UO, g);  // lane g: full traces at own point k0 + g
+        transpose4(UN, g);
         const int ko = (g < nk) ? k0 + g : k0;
         const int kc = left ? ko : K - 1 - ko;  // canonical (left-element) point index
-        if (BND && bnd) ghost_state<K>(UL, nb, ed, kc, nx, ny, tstage, geo, UR);
-        const Prim wl = primitives(UL, g1), wr = primitives(UR, g1);
+        if (BND && bnd) ghost_state<K>(UO, nb, ed, kc, nx, ny, tstage, geo, UN);  // boundary: the element is left
+        const Prim wo = primitives(UO, g1), wn = primitives(UN, g1);
         const double wl_ = h * pick_weight<K>(T.we, kc);
         double fn[4];
-        if (admissible(UL, wl) && admissible(UR, wr)) {
-          num_flux_w<FLUX>(UL, wl, UR, wr, nx, ny, gamma, left ? -wl_ : wl_, fn);
+        if (admissible(UO, wo) && admissible(UN, wn)) {
+          num_flux_own<FLUX>(UO, wo, UN, wn, nx, ny, gamma, wl_, left, fn);
         } else {
           if (valid && g < nk) record_error(sc, err_key(a.seq, kPassSurface, ed, kc));
 #pragma unroll
@@ -968,19 +1001,16 @@ __device__ __forceinline__ void g1_element(const Tab<P>& T, const Geo& geo, cons
               uo[m] = s;
             }
           }
-          double UL[4], UR[4];
+          double UN[4];
 #pragma unroll
-          for (int m = 0; m < 4; ++m) {
-            UL[m] = left ? uo[m] : un[ko][m];
-            UR[m] = left ? un[ko][m] : uo[m];
-          }
+          for (int m = 0; m < 4; ++m) UN[m] = un[ko][m];
           const int kc = left ? ko : K - 1 - ko;
-          if (BND && bnd) ghost_state<K>(UL, nb, ed, kc, nx, ny, tstage, geo, UR);
-          const Prim wl = primitives(UL, g1), wr = primitives(UR, g1);
+          if (BND && bnd) ghost_state<K>(uo, nb, ed, kc, nx, ny, tstage, geo, UN);  // boundary: the element is left
+          const Prim wo = primitives(uo, g1), wn = primitives(UN, g1);
           const double wl_ = h * pick_weight<K>(T.we, kc);
           double cf[4];
-          if (admissible(UL, wl) && admissible(UR, wr)) {
-            num_flux_w<FLUX>(UL, wl, UR, wr, nx, ny, gamma, left ? -wl_ : wl_, cf);
+          if (admissible(uo, wo) && admissible(UN, wn)) {
+            num_flux_own<FLUX>(uo, wo, UN, wn, nx, ny, gamma, wl_, left, cf);
           } else {
             record_error(sc, err_key(a.seq, kPassSurface, ed, kc));
 #pragma unroll

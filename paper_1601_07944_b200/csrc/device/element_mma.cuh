@@ -53,7 +53,7 @@ constexpr int kMmaPackUnroll = DGB_MMA_PACK_UNROLL;
 #define DGB_MMA_U_AHEAD 1
 #endif
 #ifndef DGB_MMA_TMA
-#define DGB_MMA_TMA 1  // own coefficients of a tile by one TMA box (0: per-lane cp.async)
+#define DGB_MMA_TMA(P) 1  // own coefficients of a tile by one TMA box (0: per-lane cp.async)
 #endif
 #ifndef DGB_MMA_PACK_MAXK
 #define DGB_MMA_PACK_MAXK 5  // largest edge-point count K that uses the packed surface
@@ -245,7 +245,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
   // launcher guarantees an even first column: 16-byte aligned boxes), issued by lane 0 into
   // w_own[(m NP + j) 8 + g] and completing on the warp's mbarrier.  Otherwise per-lane cp.async
   // into the fragment order w_own[(m KS + ks) 32 + lane].
-  constexpr bool kTma = DGB_MMA_TMA != 0;
+  constexpr bool kTma = DGB_MMA_TMA(P) != 0;
   __shared__ unsigned long long s_own_bar[32];
   unsigned long long* own_bar = &s_own_bar[wib];
   unsigned own_phase = 0;
@@ -513,19 +513,19 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
           const double h = sel3(q, eh[0], eh[1], eh[2]);
           const bool left = (inf >> (6 + q)) & 1;
           const bool bnd = nb < 0;
-          double UL[4], UR[4];
+          double UO[4], UN[4];
 #pragma unroll
           for (int m = 0; m < 4; ++m) {
-            UL[m] = left ? Tw[m][i] : Tn[m][i];
-            UR[m] = left ? Tn[m][i] : Tw[m][i];
+            UO[m] = Tw[m][i];
+            UN[m] = Tn[m][i];
           }
           const int kc = left ? ko : K - 1 - ko;  // canonical (left-element) point index
-          if (BND && bnd && live) ghost_state<K>(UL, nb, ed, kc, nx, ny, tstage, geo, UR);
-          const Prim wl = primitives(UL, g1), wr = primitives(UR, g1);
+          if (BND && bnd && live) ghost_state<K>(UO, nb, ed, kc, nx, ny, tstage, geo, UN);  // boundary: left
+          const Prim wo = primitives(UO, g1), wn = primitives(UN, g1);
           const double wh = live ? h * smem[D::kWe + kc] : 0.0;
           double f[4];
-          if (admissible(UL, wl) && admissible(UR, wr)) {
-            num_flux_w<FLUX>(UL, wl, UR, wr, nx, ny, gamma, left ? -wh : wh, f);
+          if (admissible(UO, wo) && admissible(UN, wn)) {
+            num_flux_own<FLUX>(UO, wo, UN, wn, nx, ny, gamma, wh, left, f);
           } else {
             if (valid && live) record_error(sc, err_key(a.seq, kPassSurface, ed, kc));
 #pragma unroll
@@ -623,20 +623,20 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
           const int ko = 2 * t + i;
-          double UL[4], UR[4];
+          double UO[4], UN[4];
 #pragma unroll
           for (int m = 0; m < 4; ++m) {
-            UL[m] = left ? Tw[m][i] : Tn[m][i];
-            UR[m] = left ? Tn[m][i] : Tw[m][i];
+            UO[m] = Tw[m][i];
+            UN[m] = Tn[m][i];
           }
           const int kc = left ? ko : K - 1 - ko;  // canonical (left-element) point index
           const bool live = ko < K;
-          if (BND && bnd && live) ghost_state<K>(UL, nb, ed, kc, nx, ny, tstage, geo, UR);
-          const Prim wl = primitives(UL, g1), wr = primitives(UR, g1);
+          if (BND && bnd && live) ghost_state<K>(UO, nb, ed, kc, nx, ny, tstage, geo, UN);  // boundary: left
+          const Prim wo = primitives(UO, g1), wn = primitives(UN, g1);
           const double wh = live ? h * smem[D::kWe + (kc < 8 ? kc : 0)] : 0.0;
           double f[4];
-          if (admissible(UL, wl) && admissible(UR, wr)) {
-            num_flux_w<FLUX>(UL, wl, UR, wr, nx, ny, gamma, left ? -wh : wh, f);
+          if (admissible(UO, wo) && admissible(UN, wn)) {
+            num_flux_own<FLUX>(UO, wo, UN, wn, nx, ny, gamma, wh, left, f);
           } else {
             if (valid && live) record_error(sc, err_key(a.seq, kPassSurface, ed, kc));
 #pragma unroll
