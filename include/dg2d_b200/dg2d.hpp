@@ -22,6 +22,7 @@
 #include <cstring>
 #include <fstream>
 #include <functional>
+#include <utility>
 #include <memory>
 #include <optional>
 #include <stdexcept>
@@ -407,11 +408,25 @@ struct SolverContext {  // solver.hpp:80-87
     return dev_->ctx;
   }
   void refresh_bc(double t) const {
-    if (bc && bc->time_dependent && bc->dirichlet) {
+    if (time_dependent()) {
       std::vector<double> dir, wn;
       detail::bc_tables(*mesh, *tables, *bc, t, dir, wn);
       detail::check(dgb_set_dirichlet(handle(), dir.data()));
     }
+  }
+  bool time_dependent() const { return bc && bc->time_dependent && bc->dirichlet; }
+  // The Dirichlet closure at every stage time t + c_k dt of the next step (the reference
+  // evaluates it inside each surface pass, solver.cpp:198-211).
+  void stage_bc(double t, double dt) const {
+    double c[8];
+    int n = 0;
+    detail::check(dgb_scheme_stage_times(options.scheme_id(), c, &n));
+    std::vector<double> all, dir, wn;
+    for (int k = 0; k < n; ++k) {
+      detail::bc_tables(*mesh, *tables, *bc, t + c[k] * dt, dir, wn);
+      all.insert(all.end(), dir.begin(), dir.end());
+    }
+    detail::check(dgb_set_dirichlet_stages(handle(), n, all.data()));
   }
   void read_timers() const {
     dgb_pass_timers t{};
@@ -525,7 +540,7 @@ inline double stable_dt(const SolverContext& ctx, const CoefficientArray& coeffs
 
 // solver.cpp:545-557 — the whole step on the device
 inline double rk_step(const SolverContext& ctx, SolverState& state, double dt) {
-  ctx.refresh_bc(state.t);
+  if (ctx.time_dependent()) ctx.stage_bc(state.t, dt);
   detail::push_state(ctx, state);
   double res = 0.0;
   const int rc = dgb_rk_step(ctx.handle(), ctx.options.scheme_id(), dt, ctx.options.limiting ? 1 : 0, &res);
@@ -601,6 +616,34 @@ inline double rk_step(const SolverContext& ctx, SolverState& state, double dt, c
 }
 
 namespace detail {
+// The drivers for time-dependent Dirichlet data: the reference's own step loop (solver.cpp:559-613)
+// on the host — stable_dt, the stage-time tables, one device step — the state on the device.
+inline std::pair<std::int64_t, double> host_stepped(const SolverContext& ctx, SolverState& state,
+                                                    std::int64_t max_steps, const double* t_end, const double* tol,
+                                                    const std::function<void(std::int64_t, double)>& on_step) {
+  push_state(ctx, state);
+  std::int64_t steps = 0;
+  double residual = 0.0, t = state.t;
+  std::int64_t sc = state.step_count;
+  int rc = DGB_OK;
+  while (rc == DGB_OK && steps < max_steps && (!t_end || t < *t_end)) {
+    double dt = 0.0;
+    rc = dgb_stable_dt(ctx.handle(), DGB_SLOT_STATE, ctx.options.cfl, &dt);
+    if (rc != DGB_OK) break;
+    if (t_end && t + dt > *t_end) dt = *t_end - t;
+    ctx.stage_bc(t, dt);
+    rc = dgb_rk_step(ctx.handle(), ctx.options.scheme_id(), dt, ctx.options.limiting ? 1 : 0, &residual);
+    if (rc != DGB_OK) break;
+    ++steps;
+    dgb_get_time(ctx.handle(), &t, &sc);
+    if (on_step) on_step(steps, residual);
+    if (tol && residual <= *tol) break;
+  }
+  pull_state(ctx, state);
+  check(rc);
+  return {steps, residual};
+}
+
 inline void replay(const std::function<void(std::int64_t, double)>& on_step, const std::vector<double>& hist,
                    std::int64_t steps) {
   if (!on_step) return;
@@ -611,6 +654,10 @@ inline void replay(const std::function<void(std::int64_t, double)>& on_step, con
 // solver.cpp:559-579
 inline SteadyResult run_to_steady(const SolverContext& ctx, SolverState& state, double tol, std::int64_t max_steps,
                                   const std::function<void(std::int64_t, double)>& on_step = {}) {
+  if (ctx.time_dependent()) {
+    const auto o = detail::host_stepped(ctx, state, max_steps, nullptr, &tol, on_step);
+    return SteadyResult{o.first, o.second, o.first > 0 && o.second <= tol};
+  }
   detail::push_state(ctx, state);
   SteadyResult r;
   int conv = 0;
@@ -628,6 +675,11 @@ inline SteadyResult run_to_steady(const SolverContext& ctx, SolverState& state, 
 // solver.cpp:581-598
 inline double run_to_time(const SolverContext& ctx, SolverState& state, double t_end, std::int64_t max_steps,
                           const std::function<void(std::int64_t, double)>& on_step = {}) {
+  if (ctx.time_dependent()) {
+    const auto o = detail::host_stepped(ctx, state, max_steps, &t_end, nullptr, on_step);
+    if (state.t < t_end) throw SolverAbort("t_end not reached within " + std::to_string(max_steps) + " steps");
+    return o.second;
+  }
   detail::push_state(ctx, state);
   double res = 0.0;
   std::int64_t steps = 0;
@@ -644,6 +696,7 @@ inline double run_to_time(const SolverContext& ctx, SolverState& state, double t
 // solver.cpp:600-613
 inline double run_fixed_steps(const SolverContext& ctx, SolverState& state, std::int64_t n_steps,
                               const std::function<void(std::int64_t, double)>& on_step = {}) {
+  if (ctx.time_dependent()) return detail::host_stepped(ctx, state, n_steps, nullptr, nullptr, on_step).second;
   detail::push_state(ctx, state);
   double res = 0.0;
   std::vector<double> hist(static_cast<size_t>(std::max<std::int64_t>(n_steps, 1)));

@@ -120,6 +120,14 @@ int dgb_set_fused_limiter(dgb_ctx* ctx, int enable);
 int dgb_set_latency_forms(dgb_ctx* ctx, int stage_max_n, int limit_max_n);
 /* Replace the Dirichlet table (time-dependent BCs): same layout as dgb_bc_view. */
 int dgb_set_dirichlet(dgb_ctx* ctx, const double* dirichlet_state);
+/* Time-dependent boundary data inside the step (the reference evaluates its Dirichlet closure at
+ * every stage time, solver.cpp:198-211): n_tables (1..8) tables laid out as dgb_bc_view's, table k
+ * holding the closure at the time of stage k of the next step (t + c_k dt, dgb_scheme_stage_times);
+ * a stage beyond the last table reads the last one.  Kept until replaced; dgb_set_dirichlet
+ * returns to one table for every stage. */
+int dgb_set_dirichlet_stages(dgb_ctx* ctx, int n_tables, const double* tables);
+/* Stage-time coefficients c_k of a scheme (stage k runs at t + c_k dt) and the stage count. */
+int dgb_scheme_stage_times(int scheme, double* tcoef, int* n_stages);
 
 /* Coefficient slots living on the device, reference layout at the boundary. */
 enum dgb_slot {

@@ -354,6 +354,10 @@ struct dgb_ctx {
 
   // device geometry
   DevBuf<double> d_tau, d_inv_det, d_inradius, d_enx, d_eny, d_eh, d_bstate, d_bwn, d_bx, d_mma;
+  // Dirichlet tables at the stage times of the next step (time-dependent boundary data,
+  // dgb_set_dirichlet_stages): stage k of a step reads table min(k, n_dir_stages - 1)
+  DevBuf<double> d_bstage;
+  int n_dir_stages = 0;
   DevBuf<int> d_nbr, d_eid, d_info, d_ref_id;  // d_ref_id: reference id of each device column
   Geo geo = [] {
     Geo g{};
@@ -964,6 +968,8 @@ RunOut run_steps(dgb_ctx* c, const RunSpec& r) {
       double* unext = c->state[(cur0 + s + 1) & 1].p;
       for (int k = 0; k < S; ++k) {
         const bool last = k == S - 1;
+        if (c->n_dir_stages > 0)  // the boundary data at this stage's time (solver.cpp:198-211)
+          c->geo.bstate = c->d_bstage.p + static_cast<size_t>(std::min(k, c->n_dir_stages - 1)) * 4 * c->n_bnd * c->K;
         StageArgs a{};
         a.in = k == 0 ? u : c->stage[(k - 1) & 1].p;
         a.u = u;
@@ -1566,9 +1572,37 @@ int dgb_set_dirichlet(dgb_ctx* c, const double* states) {
     c->d_bstate.upload(c->bc_dir.data(), c->bc_dir.size(), c->stream);
     c->geo.bstate = c->d_bstate.p;
     c->geo.has_dir = 1;
+    c->n_dir_stages = 0;
     sync(c);
     return DGB_OK;
   });
+}
+
+int dgb_set_dirichlet_stages(dgb_ctx* c, int n_tables, const double* tables) {
+  return guarded([&] {
+    set_device(c);
+    if (n_tables < 1 || n_tables > 8 || !tables) throw Fail{DGB_ERR_ARG, "expected 1..8 Dirichlet stage tables"};
+    const size_t per = 4 * static_cast<size_t>(c->n_bnd) * c->K;
+    c->bc_dir.assign(tables, tables + per);  // stage 0 (host diagnostics of a failing ghost state)
+    c->d_bstage.upload(tables, per * n_tables, c->stream);
+    c->geo.bstate = c->d_bstage.p;
+    c->geo.has_dir = 1;
+    c->n_dir_stages = n_tables;
+    sync(c);
+    return DGB_OK;
+  });
+}
+
+int dgb_scheme_stage_times(int scheme, double* tcoef, int* n_stages) {
+  std::vector<StageSpec> st;
+  if (!scheme_stages(scheme, st)) {
+    dgb::set_message("rk_order must be 2 or 4");
+    return DGB_ERR_ARG;
+  }
+  if (n_stages) *n_stages = static_cast<int>(st.size());
+  if (tcoef)
+    for (size_t k = 0; k < st.size(); ++k) tcoef[k] = st[k].tcoef;
+  return DGB_OK;
 }
 
 int dgb_upload(dgb_ctx* c, int slot, const double* host) {

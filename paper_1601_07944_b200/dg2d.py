@@ -746,8 +746,8 @@ def rk_step(ctx: SolverContext, state: SolverState, dt: float, op: Callable = No
     lim = ctx.options.limiting if limiting is None else limiting
     scheme = ctx.options.scheme_id()
     if op is None:
-        if ctx.bc.time_dependent:
-            ctx._refresh_bc(state.t)
+        if _time_dependent(ctx):
+            _set_stage_tables(ctx, state.t, dt)
         _push_state(ctx, state)
         res = C.c_double()
         try:
@@ -793,9 +793,60 @@ def rk_step(ctx: SolverContext, state: SolverState, dt: float, op: Callable = No
     return residual
 
 
+def _stage_times(scheme: int):
+    n = C.c_int()
+    tc = (C.c_double * 8)()
+    _check(lib.dgb_scheme_stage_times(scheme, tc, C.byref(n)))
+    return [tc[k] for k in range(n.value)]
+
+
+def _time_dependent(ctx: SolverContext) -> bool:
+    return bool(ctx.bc.time_dependent and ctx.bc.dirichlet is not None)
+
+
+def _set_stage_tables(ctx: SolverContext, t: float, dt: float):
+    """The Dirichlet closure at every stage time of the step (t + c_k dt), as the reference
+    evaluates it inside each surface pass (solver.cpp:198-211)."""
+    tabs = [ctx._bc_tables(t + ck * dt)[0] for ck in _stage_times(ctx.options.scheme_id())]
+    arr = np.ascontiguousarray(np.stack(tabs))
+    _check(lib.dgb_set_dirichlet_stages(ctx.handle, len(tabs), dptr(arr)))
+
+
+def _host_stepped(ctx: SolverContext, state: SolverState, max_steps: int, t_end: float = None,
+                  tol: float = None, on_step: Callable = None):
+    """The drivers for time-dependent Dirichlet data: the step loop of solver.cpp:559-613 on the
+    host (stable_dt, the stage-time tables, one device RK step), the state resident on the device.
+    Returns (steps, residual)."""
+    _push_state(ctx, state)
+    res, dt = C.c_double(), C.c_double()
+    t, s = C.c_double(), C.c_int64()
+    steps, residual = 0, 0.0
+    try:
+        _check(lib.dgb_get_time(ctx.handle, C.byref(t), C.byref(s)))
+        while steps < max_steps and (t_end is None or t.value < t_end):
+            _check(lib.dgb_stable_dt(ctx.handle, L.SLOT_STATE, ctx.options.cfl, C.byref(dt)))
+            h = dt.value
+            if t_end is not None and t.value + h > t_end:
+                h = t_end - t.value
+            _set_stage_tables(ctx, t.value, h)
+            _check(lib.dgb_rk_step(ctx.handle, ctx.options.scheme_id(), h, int(ctx.options.limiting), C.byref(res)))
+            steps += 1
+            residual = res.value
+            _check(lib.dgb_get_time(ctx.handle, C.byref(t), C.byref(s)))
+            if on_step:
+                on_step(steps, residual)
+            if tol is not None and residual <= tol:
+                break
+    finally:
+        _pull_state(ctx, state)
+    return steps, residual
+
+
 def run_fixed_steps(ctx: SolverContext, state: SolverState, n_steps: int,
                     on_step: Callable = None) -> float:
     """solver.cpp:600-613 with the state resident on the device."""
+    if _time_dependent(ctx):
+        return _host_stepped(ctx, state, int(n_steps), on_step=on_step)[1]
     _push_state(ctx, state)
     res = C.c_double()
     hist = np.zeros(max(int(n_steps), 1))
@@ -813,6 +864,11 @@ def run_fixed_steps(ctx: SolverContext, state: SolverState, n_steps: int,
 def run_to_time(ctx: SolverContext, state: SolverState, t_end: float, max_steps: int,
                 on_step: Callable = None) -> float:
     """solver.cpp:581-598"""
+    if _time_dependent(ctx):
+        steps, residual = _host_stepped(ctx, state, int(max_steps), t_end=t_end, on_step=on_step)
+        if state.t < t_end:
+            raise SolverAbort(f"t_end not reached within {int(max_steps)} steps")
+        return residual
     _push_state(ctx, state)
     res = C.c_double()
     steps = C.c_int64()
@@ -833,6 +889,9 @@ def run_to_time(ctx: SolverContext, state: SolverState, t_end: float, max_steps:
 def run_to_steady(ctx: SolverContext, state: SolverState, tol: float, max_steps: int,
                   on_step: Callable = None) -> SteadyResult:
     """solver.cpp:559-579"""
+    if _time_dependent(ctx):
+        steps, residual = _host_stepped(ctx, state, int(max_steps), tol=tol, on_step=on_step)
+        return SteadyResult(steps, residual, steps > 0 and residual <= tol)
     _push_state(ctx, state)
     steps, res, conv = C.c_int64(), C.c_double(), C.c_int()
     cap = int(min(max_steps, 1 << 22))

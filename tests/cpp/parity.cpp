@@ -165,6 +165,47 @@ static void case_run(int p, int rk_order, bool dmr, int steps) {
   CHECK(std::fabs(mr - mb) <= 1e-12 * std::fabs(mr), "mass");
 }
 
+// Time-dependent Dirichlet data: the reference evaluates its closure at every stage time inside
+// run_fixed_steps (solver.cpp:198-211); the mirror's drivers give the device one table per stage.
+static void case_time_dependent_bc(int p, int rk_order, int steps) {
+  Pair m = meshes(B::gen_vortex_msh(1));
+  const R::BasisTables rt = R::build_tables(p);
+  const B::BasisTables bt = B::build_tables(p);
+  const R::GasModel gas;
+  R::BoundaryConditions rbc = R::vortex_boundary({}, gas);
+  B::BoundaryConditions bbc = B::vortex_boundary({}, {});
+  auto scaled = [](auto s, double t) {
+    const double f = 1.0 + 0.05 * std::sin(40.0 * t);
+    for (int k = 0; k < 4; ++k) s[k] *= f;
+    return s;
+  };
+  const auto r0 = rbc.dirichlet;
+  const auto b0 = bbc.dirichlet;
+  rbc.dirichlet = [r0, scaled](R::Vec2 x, double t) { return scaled(r0(x, t), t); };
+  bbc.dirichlet = [b0, scaled](B::Vec2 x, double t) { return scaled(b0(x, t), t); };
+  bbc.time_dependent = true;
+  R::SolverContext rc{&m.rm, &rt, gas, &rbc, {rk_order, 0.3, false, 0, 256}, {}};
+  B::SolverContext bc;
+  bc.mesh = &m.bm;
+  bc.tables = &bt;
+  bc.bc = &bbc;
+  bc.options.rk_order = rk_order;
+  bc.options.cfl = 0.3;
+  R::SolverState rs;
+  rs.coeffs = R::project_initial([&](R::Vec2 x) { return R::vortex_exact(x, {}, gas); }, m.rm, rt, gas);
+  B::SolverState bs;
+  bs.coeffs = to_b(rs.coeffs);
+  const double rr = R::run_fixed_steps(rc, rs, steps);
+  const double br = B::run_fixed_steps(bc, bs, steps);
+  std::vector<double> scale(rs.coeffs.data.size());
+  for (size_t k = 0; k < scale.size(); ++k) scale[k] = std::fabs(rs.coeffs.data[k]);
+  const double e = rel(bs.coeffs.data, rs.coeffs.data, scale, rt.n_p, m.rm.n_elements());
+  std::printf("time-dependent Dirichlet p=%d rk%d x%d: rel err %.2e, t %.17g vs %.17g, residual %.3e vs %.3e\n", p,
+              rk_order, steps, e, bs.t, rs.t, br, rr);
+  CHECK(e <= 1e-9, "time-dependent BC run parity %.3e", e);
+  CHECK(std::fabs(bs.t - rs.t) <= 1e-12 * rs.t && bs.step_count == rs.step_count, "time/steps");
+}
+
 static void case_errors() {
   std::printf("error behaviour (test_limiter.cpp:170-175, test_solver.cpp:413-422, 504-512)\n");
   Pair m = meshes(B::gen_vortex_msh(0));
@@ -290,6 +331,8 @@ int main() {
   case_run(2, 4, false, 20);
   case_run(4, 2, false, 10);
   case_run(1, 2, true, 30);
+  case_time_dependent_bc(2, 4, 12);
+  case_time_dependent_bc(3, 2, 12);
   case_errors();
   case_operator_seam_and_checkpoint();
   case_output();

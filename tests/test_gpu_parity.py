@@ -590,3 +590,53 @@ def test_latency_forms_bitwise_equal_to_one_thread_forms(p, scheme, flux, limiti
     assert np.array_equal(out[0][0], out[1][0])
     assert out[0][1] == out[1][1] and out[0][2] == out[1][2]
     assert L.lib.dgb_set_latency_forms(None, 0, 0) == L.ERR_ARG
+
+
+@pytest.mark.parametrize("scheme", [4, 103])
+def test_time_dependent_dirichlet_at_every_stage_time(scheme):
+    """Time-dependent boundary data inside the step: the reference evaluates its Dirichlet
+    closure at every stage time (solver.cpp:198-211).  With ``time_dependent=True`` the drivers
+    hand the device one table per stage (dgb_set_dirichlet_stages); the run matches the host-side
+    RK around compute_rhs (the closure refreshed at each stage time) and differs from stepping
+    with the table of the step's start time (what the device loop alone would do)."""
+    geo, gas = dg2d.VortexGeometry(), dg2d.GasModel()
+
+    def dirichlet(xy, t):
+        s = np.array(dg2d.vortex_exact(xy, geo, gas), dtype=np.float64, copy=True)
+        return s * (1.0 + 0.05 * np.sin(40.0 * t))  # rho, m, E scaled alike: admissible
+
+    base = dg2d.vortex_boundary(geo, gas)
+    bc = dg2d.BoundaryConditions(inflow_state=base.inflow_state, dirichlet=dirichlet,
+                                 wall_normal=base.wall_normal, time_dependent=True)
+    mesh = dg2d.generate_mesh(L.MESH_VORTEX, 1, 0, geo.r_inner, geo.r_outer)
+    tb = dg2d.build_tables(2)
+    c0 = dg2d.project_initial(lambda xy: dg2d.vortex_exact(xy, geo, gas), mesh, tb)
+    opts = dg2d.SolverOptions(scheme=scheme, cfl=0.3)
+    steps = 8
+
+    ctx = dg2d.SolverContext(mesh, tb, bc=bc, options=opts)
+    st = dg2d.SolverState(c0.copy())
+    hist = []
+    res = dg2d.run_fixed_steps(ctx, st, steps, lambda s, r: hist.append(r))
+    assert st.step_count == steps and len(hist) == steps and hist[-1] == res
+
+    ref = dg2d.SolverContext(mesh, tb, bc=bc, options=opts)
+    sr = dg2d.SolverState(c0.copy())
+    for _ in range(steps):
+        dt = dg2d.stable_dt(ref, sr.coeffs)
+        dg2d.rk_step(ref, sr, dt, op=lambda c, tt: dg2d.compute_rhs(ref, c, tt))
+    assert rel_per_eq(st.coeffs, sr.coeffs) <= RUN_TOL
+    assert abs(st.t - sr.t) <= 1e-13 * sr.t
+
+    stale = dg2d.SolverContext(mesh, tb, bc=bc, options=opts)
+    ss = dg2d.SolverState(c0.copy())
+    for _ in range(steps):
+        dt = dg2d.stable_dt(stale, ss.coeffs)
+        stale._refresh_bc(ss.t)  # one table, at the step's start time
+        dg2d._push_state(stale, ss)
+        r = __import__("ctypes").c_double()
+        dg2d._check(L.lib.dgb_rk_step(stale.handle, scheme, dt, 0, __import__("ctypes").byref(r)))
+        dg2d._pull_state(stale, ss)
+    assert rel_per_eq(ss.coeffs, sr.coeffs) > 1e-6  # the test sees the stage times
+    for c_ in (ctx, ref, stale):
+        c_.close()
