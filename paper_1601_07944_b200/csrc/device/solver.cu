@@ -57,6 +57,12 @@ struct DevBuf {
     n = count;
     if (count) CU(cudaMalloc(&p, count * sizeof(T)));
   }
+  // alloc, then zero on `s` (coefficient buffers: the DMMA kernel's TMA boxes read the padding
+  // columns past N, never using them; zeroed they hold defined values)
+  void alloc_zero(size_t count, cudaStream_t s) {
+    alloc(count);
+    if (count) CU(cudaMemsetAsync(p, 0, count * sizeof(T), s));
+  }
   void upload(const T* h, size_t count, cudaStream_t s) {
     alloc(count);
     if (count) CU(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
@@ -627,19 +633,19 @@ double* slot_ptr(dgb_ctx* c, int slot) {
     case DGB_SLOT_STATE: return c->state[c->cur].p;
     case DGB_SLOT_INPUT:
       if (!c->input.p) {
-        c->input.alloc(c->coeff_count());
+        c->input.alloc_zero(c->coeff_count(), c->stream);
         CU(cudaMemsetAsync(c->input.p, 0, c->coeff_count() * 8, c->stream));
       }
       return c->input.p;
     case DGB_SLOT_VOLUME:
       if (!c->volume.p) {
-        c->volume.alloc(c->coeff_count());
+        c->volume.alloc_zero(c->coeff_count(), c->stream);
         CU(cudaMemsetAsync(c->volume.p, 0, c->coeff_count() * 8, c->stream));
       }
       return c->volume.p;
     case DGB_SLOT_DERIV:
       if (!c->deriv.p) {
-        c->deriv.alloc(c->coeff_count());
+        c->deriv.alloc_zero(c->coeff_count(), c->stream);
         CU(cudaMemsetAsync(c->deriv.p, 0, c->coeff_count() * 8, c->stream));
       }
       return c->deriv.p;
@@ -895,10 +901,10 @@ RunOut run_steps(dgb_ctx* c, const RunSpec& r) {
   check_bc(c);
   ensure_tables(c);
   const int S = static_cast<int>(st.size());
-  if (!c->stage[0].p) c->stage[0].alloc(c->coeff_count());
-  if (!c->stage[1].p) c->stage[1].alloc(c->coeff_count());
-  if (r.scheme == DGB_RK4_CLASSIC && !c->kacc.p) c->kacc.alloc(c->coeff_count());
-  if (!c->state[1 - c->cur].p) c->state[1 - c->cur].alloc(c->coeff_count());
+  if (!c->stage[0].p) c->stage[0].alloc_zero(c->coeff_count(), c->stream);
+  if (!c->stage[1].p) c->stage[1].alloc_zero(c->coeff_count(), c->stream);
+  if (r.scheme == DGB_RK4_CLASSIC && !c->kacc.p) c->kacc.alloc_zero(c->coeff_count(), c->stream);
+  if (!c->state[1 - c->cur].p) c->state[1 - c->cur].alloc_zero(c->coeff_count(), c->stream);
   double* d_hist = nullptr;
   if (r.hist && r.hist_cap > 0) {
     if (c->hist.n < static_cast<size_t>(r.hist_cap)) c->hist.alloc(r.hist_cap);
@@ -1469,15 +1475,12 @@ int dgb_part_create(const dgb_mesh_view* m, const dgb_tables_view* t, const dgb_
     CU(cudaMallocHost(&c->h_sc, sizeof(Scalars)));
     CU(cudaMalloc(&c->d_red, sizeof(unsigned long long)));
     CU(cudaMallocHost(&c->h_red, sizeof(unsigned long long)));
-    c->state[0].alloc(c->coeff_count());
-    CU(cudaMemsetAsync(c->state[0].p, 0, c->coeff_count() * sizeof(double), c->stream));
+    c->state[0].alloc_zero(c->coeff_count(), c->stream);
     if (c->partitioned) {
       // the peers address our rotating buffers directly, so they exist from the start
-      c->state[1].alloc(c->coeff_count());
-      c->stage[0].alloc(c->coeff_count());
-      c->stage[1].alloc(c->coeff_count());
-      for (DevBuf<double>* b : {&c->state[1], &c->stage[0], &c->stage[1]})
-        CU(cudaMemsetAsync(b->p, 0, c->coeff_count() * sizeof(double), c->stream));
+      c->state[1].alloc_zero(c->coeff_count(), c->stream);
+      c->stage[0].alloc_zero(c->coeff_count(), c->stream);
+      c->stage[1].alloc_zero(c->coeff_count(), c->stream);
       const size_t nx = dgbk::kMaxRanks + 2 * dgbk::kMaxRanks * 4;
       CU(cudaMalloc(&c->d_xch, nx * sizeof(unsigned long long)));
       CU(cudaMemsetAsync(c->d_xch, 0, nx * sizeof(unsigned long long), c->stream));

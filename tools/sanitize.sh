@@ -42,9 +42,23 @@ dm = dg2d.generate_mesh(L.MESH_DOUBLE_MACH, 12, 3, 1.0 / 6.0)
 tb = dg2d.build_tables(1)
 setup = dg2d.DoubleMachSetup()
 bc = dg2d.double_mach_boundary(setup)
-ctx = dg2d.SolverContext(dm, tb, bc=bc, options=dg2d.SolverOptions(rk_order=2, limiting=True))
-c = dg2d.limit(ctx, dg2d.project_initial(lambda xy: dg2d.double_mach_initial(xy, setup), dm, tb))
-dg2d.run_fixed_steps(ctx, dg2d.SolverState(c), 2)
+for fused, lat in ((-1, -1), (0, -1), (1, 0), (0, 0)):  # latency-form fused, two kernels + means, fused, one-thread
+    ctx = dg2d.SolverContext(dm, tb, bc=bc, options=dg2d.SolverOptions(rk_order=2, limiting=True))
+    L.lib.dgb_set_fused_limiter(ctx.handle, fused)
+    L.lib.dgb_set_latency_forms(ctx.handle, lat, lat)
+    c = dg2d.limit(ctx, dg2d.project_initial(lambda xy: dg2d.double_mach_initial(xy, setup), dm, tb))
+    dg2d.run_fixed_steps(ctx, dg2d.SolverState(c), 2)
+    ctx.close()
+# time-dependent Dirichlet tables per stage (vortex mesh, inflow boundary)
+vb = dg2d.vortex_boundary()
+tdb = dg2d.BoundaryConditions(inflow_state=vb.inflow_state, dirichlet=lambda xy, t: vb.dirichlet(xy, t),
+                              wall_normal=vb.wall_normal, time_dependent=True)
+vm = dg2d.generate_mesh(L.MESH_VORTEX, 1, 0, 1.0, 1.384)
+for p in (2, 3):
+    tbp = dg2d.build_tables(p)
+    ctx = dg2d.SolverContext(vm, tbp, bc=tdb, options=dg2d.SolverOptions(rk_order=4))
+    dg2d.run_fixed_steps(ctx, dg2d.SolverState(dg2d.project_initial(lambda xy: dg2d.vortex_exact(xy), vm, tbp)), 2)
+    ctx.close()
 print("sanitizer case done")
 PY
 for tool in ${TOOLS:-memcheck racecheck initcheck synccheck}; do
