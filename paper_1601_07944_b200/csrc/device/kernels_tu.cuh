@@ -111,9 +111,10 @@ void with_instance(int flux, int mode, int var, F&& f) {
     with_instance<kFluxLLF>(mode, var, f);
 }
 #ifndef DGB_VAR_MASK
-// variant bits specialised per degree (the others take the full path); measured per stage on the
-// periodic box: p=2 0.307 ms with the boundary code kept vs 0.341 without (register allocation)
-#define DGB_VAR_MASK(P) ((P) == 2 ? (kVarRk4 | kVarLambda) : 7)
+// variant bits specialised per degree (the others take the full path).  Round 1 kept the boundary
+// code in the p=2 periodic instance (0.307 vs 0.341 ms, register allocation); with the round-2
+// kernel the split is faster there too (0.294 vs 0.301 ms, interleaved A/B)
+#define DGB_VAR_MASK(P) 7
 #endif
 int variant_of(int mode, const Geo& g, const StageArgs& a) {
   constexpr int mask = DGB_VAR_MASK(DGB_P);
