@@ -627,7 +627,7 @@ def main():
     ap.add_argument("--orders", default="1,2,3,4,5")
     ap.add_argument("--scheme", default="ssp3", choices=list(SCHEMES))
     ap.add_argument("--cfl", type=float, default=0.3)
-    ap.add_argument("--e2e-steps", type=int, default=16)
+    ap.add_argument("--e2e-steps", type=int, default=32, help="requests per order in the end-to-end leg (the pipeline fills and drains once)")
     ap.add_argument("--cpu-box", dest="cpu_n", type=int, default=708, help="box size of the CPU sample")
     ap.add_argument("--ref-steps", type=int, default=3, help="RK2 steps per reference run_fixed_steps call")
     ap.add_argument("--no-cpu", action="store_true")
