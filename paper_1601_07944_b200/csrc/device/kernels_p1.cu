@@ -653,6 +653,15 @@ int stage_limit_grid() {
   return o * sm_count();
 }
 
+namespace {
+int stage_limit4_grid() {  // co-resident blocks of the latency form (its own register budget)
+  static std::atomic<int> occ{0};
+  int o = occ.load(std::memory_order_relaxed);
+  if (!o) occ.store(o = occupancy(k_stage_limit4<kFluxRoe, kVarRk4 | kVarBoundary, 3>), std::memory_order_relaxed);
+  return o * sm_count();
+}
+}  // namespace
+
 cudaError_t launch_stage_limit(int grid, const Geo& g, const StageArgs& a, const LimArgs& la, const FuseArgs& f,
                                cudaStream_t s) {
   if (a.e1 <= a.e0) return cudaSuccess;
@@ -663,7 +672,7 @@ cudaError_t launch_stage_limit(int grid, const Geo& g, const StageArgs& a, const
   cudaError_t err = cudaSuccess;
   // latency form: one warp per stage tile and per 8-element limiter subtile fit in one wave
   const int wpb = kBlock / 32;
-  const bool lat = f.n_tiles > 0 && 4 * f.n_tiles <= stage_limit_grid() * wpb &&
+  const bool lat = f.n_tiles > 0 && 4 * f.n_tiles <= stage_limit4_grid() * wpb &&
                    (g.lat_limit_n >= 0 ? a.e1 - a.e0 <= g.lat_limit_n : true);
   if (lat) grid = (4 * f.n_tiles + wpb - 1) / wpb;
   auto go = [&](auto k) {  // cooperative: every warp of the grid is resident (the tiles' waits need it)
