@@ -426,6 +426,7 @@ struct SolverContext {  // solver.hpp:80-87
       detail::bc_tables(*mesh, *tables, *bc, t + c[k] * dt, dir, wn);
       all.insert(all.end(), dir.begin(), dir.end());
     }
+    if (all.empty()) return;  // no boundary Gauss points (e.g. a periodic mesh)
     detail::check(dgb_set_dirichlet_stages(handle(), n, all.data()));
   }
   void read_timers() const {

@@ -808,6 +808,8 @@ def _set_stage_tables(ctx: SolverContext, t: float, dt: float):
     """The Dirichlet closure at every stage time of the step (t + c_k dt), as the reference
     evaluates it inside each surface pass (solver.cpp:198-211)."""
     tabs = [ctx._bc_tables(t + ck * dt)[0] for ck in _stage_times(ctx.options.scheme_id())]
+    if any(tb is None for tb in tabs):  # no boundary Gauss points (e.g. a periodic mesh)
+        return
     arr = np.ascontiguousarray(np.stack(tabs))
     _check(lib.dgb_set_dirichlet_stages(ctx.handle, len(tabs), dptr(arr)))
 
