@@ -230,6 +230,11 @@ def run_group(parts: Sequence, fn: Callable):
 def run_fixed_steps_group(parts: Sequence[PartContext], state: SolverState, n_steps: int) -> float:
     """run_fixed_steps over an in-process partition group; gathers the owned results back
     into ``state`` (reference layout) and returns the global residual."""
+    if any(p.bc.time_dependent and p.bc.dirichlet is not None for p in parts):
+        # the device step loop of a partition group keeps one Dirichlet table per run; the
+        # stage-time tables of dg2d's host-stepped drivers need a host dt, i.e. a host min over ranks
+        raise ValueError("time-dependent Dirichlet data are not supported by partitioned runs "
+                         "(use a whole-mesh context: dg2d.run_fixed_steps steps them on the host)")
     for p in parts:
         p.upload_global(L.SLOT_STATE, state.coeffs)
         _check(lib.dgb_set_time(p.handle, state.t, state.step_count))
