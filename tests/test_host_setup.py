@@ -231,3 +231,16 @@ def test_no_cpu_fallback_without_a_device():
     with pytest.raises(RuntimeError, match="no CUDA device"):
         dg2d.compute_rhs(ctx, np.zeros((4, 3, m.n_elements())), 0.0)
     del n
+
+
+def test_scheme_stage_times():
+    """Stage-time coefficients of each scheme (the stage k of a step runs at t + c_k dt), as the
+    reference's rk_step_ws evaluates its operator (solver.cpp:513-531) and the SSP schemes."""
+    import ctypes as C
+    n = C.c_int()
+    c = (C.c_double * 8)()
+    want = {2: [0.0, 0.5], 4: [0.0, 0.5, 0.5, 1.0], 102: [0.0, 1.0], 103: [0.0, 1.0, 0.5]}
+    for scheme, tc in want.items():
+        assert L.lib.dgb_scheme_stage_times(scheme, c, C.byref(n)) == 0
+        assert [c[k] for k in range(n.value)] == tc
+    assert L.lib.dgb_scheme_stage_times(3, c, C.byref(n)) == L.ERR_ARG
