@@ -101,11 +101,6 @@ struct Geo {
   double sh_x0, sh_cos, sh_sin, sh_speed;
   double sh_post[4], sh_pre[4];
   double gamma;
-  // halo sends: device columns [send_begin, N) may feed peers; entries
-  // send_ent[send_ptr[d - send_begin] .. send_ptr[d - send_begin + 1]) = (peer rank, peer column)
-  const int* __restrict__ send_ptr;
-  const int2* __restrict__ send_ent;
-  int send_begin;
   // basis tables in DMMA fragment order (element_mma.cuh), p >= 3
   const double* __restrict__ mma_tab;
   int flux;  // numerical flux: 0 local Lax-Friedrichs (euler.hpp:59-71), 1 Roe
@@ -152,9 +147,6 @@ struct StageArgs {
   Scalars* sc;
   double* hist;                   // optional residual history (on_step)
   int e0, e1;                     // device element range of this launch
-  int push;                       // write the new stage of send elements into the peers' halo columns
-  int out_buf;                    // index of `out` among the rotating buffers (peer addressing)
-  const PeerTab* peers;
 };
 
 // Fused stage + limiter launch (p = 1 with limiting, kernels_p1.cu k_stage_limit).  Work unit:
@@ -180,8 +172,6 @@ struct LimArgs {
   unsigned long long seq;         // error key for the CFL epilogue (next step)
   Scalars* sc;
   int e0, e1;                     // device element range of this launch
-  int push, out_buf;              // as StageArgs: push the limited element to the peers
-  const PeerTab* peers;
 };
 
 }  // namespace dgbk

@@ -440,25 +440,6 @@ __device__ __forceinline__ double pick_weight(const double (&we)[K], int k) {
   return r;
 }
 
-// Halo push: store the new values of variables
-// [m0, m0 + MG) of send element `e` into the halo columns of every peer that
-// needs it, over NVLink peer memory (plain global stores to IPC-mapped buffers).
-template <int NP, int MG>
-__device__ __forceinline__ void push_element(const Geo& geo, const PeerTab* __restrict__ pt, int out_buf, int e, int m0,
-                                             const double (&v)[MG][NP]) {
-  const int s0 = __ldg(geo.send_ptr + (e - geo.send_begin));
-  const int s1 = __ldg(geo.send_ptr + (e - geo.send_begin) + 1);
-  for (int s = s0; s < s1; ++s) {
-    const int2 ent = __ldg(geo.send_ent + s);
-    double* __restrict__ dst = pt->buf[ent.x][out_buf];
-    const long long pld = pt->ld[ent.x];
-#pragma unroll
-    for (int mm = 0; mm < MG; ++mm)
-#pragma unroll
-      for (int j = 0; j < NP; ++j) dst[(static_cast<long long>(m0 + mm) * NP + j) * pld + ent.y] = v[mm][j];
-  }
-}
-
 // Minimum registers per launch for the fused kernel (occupancy target per degree).
 #ifndef DGB_MINB
 #define DGB_MINB(P) ((P) == 1 ? 4 : (P) == 2 ? 3 : (P) == 3 ? 5 : (P) == 4 ? 4 : 3)  // p=1 0.129 vs 0.132 ms at 5, p=2 0.323 vs 0.328 at 4
@@ -754,10 +735,6 @@ __device__ __forceinline__ void g4_element(const Tab<P>& T, const Geo& geo, cons
       acc[j] = o;  // keep the new stage for the CFL epilogue
     }
     if (a.means && valid) a.means[4 * static_cast<long long>(e) + g] = acc[0];
-    if (a.push && valid && e >= geo.send_begin) {
-      const double(&v)[1][NP] = reinterpret_cast<const double(&)[1][NP]>(acc);
-      push_element<NP, 1>(geo, a.peers, a.out_buf, e, g, v);
-    }
     if (want_lambda) {
       double v[4];
 #pragma unroll
@@ -824,7 +801,6 @@ __device__ __forceinline__ void element_body(const Tab<P>& T, const Geo& geo, co
     const int par = a.step & 1;
     if (want_lambda) block_reduce_atomic<true>(lam_min, &sc->dtmin[par ^ 1]);
     if (a.want_resid) block_reduce_atomic<false>(res_max, &sc->resid[par]);
-    if (a.push) __threadfence_system();  // halo stores visible before the signal kernel's flag
   }
 }
 
@@ -1076,7 +1052,6 @@ __device__ __forceinline__ void g1_element(const Tab<P>& T, const Geo& geo, cons
         mp[0] = make_double2(acc[0][0], acc[1][0]);
         mp[1] = make_double2(acc[2][0], acc[3][0]);
       }
-      if (a.push && e >= geo.send_begin) push_element<NP, 4>(geo, a.peers, a.out_buf, e, 0, acc);
       if (want_lambda) {
         double lam = 0.0;
         double a0[4];  // mode-0 products of the midpoint states (the same at the three midpoints)
@@ -1160,7 +1135,6 @@ __device__ __forceinline__ void element_body_g1(const Tab<P>& T, const Geo& geo,
     const int par = a.step & 1;
     if (want_lambda) block_reduce_atomic<true>(lam_min, &sc->dtmin[par ^ 1]);
     if (a.want_resid) block_reduce_atomic<false>(res_max, &sc->resid[par]);
-    if (a.push) __threadfence_system();  // halo stores visible before the signal kernel's flag
   }
 }
 

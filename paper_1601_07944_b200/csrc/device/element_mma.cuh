@@ -756,29 +756,11 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
                 a.out[idx] = o;
                 if (a.want_resid) res_max = std_max(res_max, fabs(uu - o));
               }
-              R[m][jt][ii] = o;  // keep the new stage for the CFL epilogue / halo push
+              R[m][jt][ii] = o;  // keep the new stage for the CFL epilogue
             } else {
               R[m][jt][ii] = 0.0;
             }
           }
-      }
-      if (a.push && valid && e >= geo.send_begin) {
-        const int s0 = __ldg(geo.send_ptr + (e - geo.send_begin));
-        const int s1 = __ldg(geo.send_ptr + (e - geo.send_begin) + 1);
-        for (int sidx = s0; sidx < s1; ++sidx) {
-          const int2 ent = __ldg(geo.send_ent + sidx);
-          double* __restrict__ dst = a.peers->buf[ent.x][a.out_buf];
-          const long long pld = a.peers->ld[ent.x];
-#pragma unroll
-          for (int m = 0; m < 4; ++m)
-#pragma unroll
-            for (int jt = 0; jt < JT; ++jt)
-#pragma unroll
-              for (int ii = 0; ii < 2; ++ii) {
-                const int j = 8 * jt + 2 * t + ii;
-                if (j < NP) dst[(static_cast<long long>(m) * NP + j) * pld + ent.y] = R[m][jt][ii];
-              }
-        }
       }
       if (want_lambda) {
         // states at the 3 side midpoints: partial sums over this lane's modes, then
@@ -831,7 +813,6 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
     const int par = a.step & 1;
     if (want_lambda) block_reduce_atomic<true>(lam_min, &sc->dtmin[par ^ 1]);
     if (a.want_resid) block_reduce_atomic<false>(res_max, &sc->resid[par]);
-    if (a.push) __threadfence_system();
   }
 }
 

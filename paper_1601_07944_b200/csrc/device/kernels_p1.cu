@@ -201,10 +201,6 @@ __device__ __forceinline__ void limit_element(const Geo& geo, const LimArgs& a, 
       a.c[(m * NP + 1) * ld + e] = c1[m];
       a.c[(m * NP + 2) * ld + e] = c2[m];
     }
-    if (a.push && e >= geo.send_begin) {
-      const double v[4][NP] = {{c0[0], c1[0], c2[0]}, {c0[1], c1[1], c2[1]}, {c0[2], c1[2], c2[2]}, {c0[3], c1[3], c2[3]}};
-      push_element<NP, 4>(geo, a.peers, a.out_buf, e, 0, v);
-    }
     if (want_resid) {
 #pragma unroll
       for (int m = 0; m < 4; ++m) {
@@ -392,10 +388,6 @@ __device__ __forceinline__ void limit_element4(const Geo& geo, const LimArgs& a,
     double* __restrict__ cw = a.c + static_cast<long long>(v) * NP * ld;
     cw[ld + e] = c1;
     cw[2 * ld + e] = c2;
-    if (a.push && e >= geo.send_begin) {
-      const double w[1][NP] = {{c0, c1, c2}};
-      push_element<NP, 1>(geo, a.peers, a.out_buf, e, v, w);
-    }
     if (want_resid) {
       const double* __restrict__ uv = a.u + static_cast<long long>(v) * NP * ld;
       res_max = std_max(res_max, fabs(__ldg(uv + e) - c0));
@@ -445,7 +437,6 @@ __global__ void __launch_bounds__(kBlock) k_limit4(Geo geo, LimArgs a) {
   const int par = a.step & 1;
   if (want_lambda) block_reduce_atomic<true>(lam_min, &sc->dtmin[par ^ 1]);
   if (want_resid) block_reduce_atomic<false>(res_max, &sc->resid[par]);
-  if (a.push) __threadfence_system();
 }
 
 template <int NE, int NPT, int EPI>
@@ -463,7 +454,6 @@ __global__ void __launch_bounds__(kBlock, DGB_LIMIT_MINB) k_limit(Geo geo, LimAr
   const int par = a.step & 1;
   if (want_lambda) block_reduce_atomic<true>(lam_min, &sc->dtmin[par ^ 1]);
   if (want_resid) block_reduce_atomic<false>(res_max, &sc->resid[par]);
-  if (a.push) __threadfence_system();
 }
 
 constexpr unsigned long long kFuseTimeoutKey = (7ull << 35) | 1ull;  // sorts before every solver error

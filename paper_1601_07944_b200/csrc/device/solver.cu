@@ -115,9 +115,27 @@ __device__ __forceinline__ unsigned long long global_ns() {
   return t;
 }
 
+// Halo push: copy the new coefficient columns of the send elements into the halo columns of
+// every peer that needs them, over NVLink peer memory (plain global stores into the peers'
+// IPC-mapped buffers).  Entry i = (own column, peer rank, peer column); thread k covers row
+// k / n of entry k % n, so a warp stores one row of consecutive entries, which the host sorted
+// by (peer, peer column).  Kept out of the stage and limiter kernels: the push code there cost
+// the whole-mesh instances registers and issue slots.
+__global__ void k_push(const dgbk::PeerTab* __restrict__ pt, int buf, const double* __restrict__ src, long long ld,
+                       const int4* __restrict__ ent, int n, int rows) {
+  const long long total = static_cast<long long>(n) * rows;
+  for (long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; k < total;
+       k += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(k / n), i = static_cast<int>(k - static_cast<long long>(r) * n);
+    const int4 e = __ldg(ent + i);
+    pt->buf[e.y][buf][static_cast<long long>(r) * pt->ld[e.y] + e.z] = src[static_cast<long long>(r) * ld + e.x];
+  }
+  __threadfence_system();  // visible at the peers before the signal kernel's flag
+}
+
 // One warp: publish (optionally) this rank's step scalars into every peer of
-// `mask`, then raise our flag there to `epoch`.  The stage kernel that pushed
-// the halo values fenced them (system scope) before it completed.
+// `mask`, then raise our flag there to `epoch`.  The push kernel before it fenced
+// the halo values (system scope) before it completed.
 __global__ void k_signal(const dgbk::PeerTab* __restrict__ pt, unsigned mask, int me, unsigned long long epoch,
                          const dgbk::Scalars* __restrict__ sc, int publish, int slot, int dt_idx, int res_idx) {
   const int r = threadIdx.x;
@@ -350,8 +368,9 @@ struct dgb_ctx {
   dgbk::PeerTab* d_peers = nullptr;
   unsigned long long* d_xch = nullptr;        // flags[kMaxRanks] + scalar slots [2][kMaxRanks][4]
   std::vector<void*> ipc_opened;
-  DevBuf<int> d_cmp, d_send_ptr;
-  DevBuf<int2> d_send_ent;
+  DevBuf<int> d_cmp;
+  DevBuf<int4> d_push;                        // halo push entries (own column, peer, peer column)
+  int n_push = 0;
   unsigned long long epoch = 0;               // signals sent so far (same sequence on every rank)
   unsigned long long pub_epoch = 0;           // epoch of the last scalar publish
   int64_t n_pub = 0;                          // publishes so far (slot = n_pub & 1)
@@ -870,6 +889,17 @@ bool exchanging(const dgb_ctx* c) { return c->partitioned && c->world > 1; }
 
 unsigned all_peers(const dgb_ctx* c) { return ((1u << c->world) - 1u) & ~(1u << c->rank); }
 
+// Push the send elements' columns of `p` (one of the rotating buffers) to the peers.
+void xch_push(dgb_ctx* c, const double* p) {
+  if (c->n_push == 0) return;
+  const int rows = 4 * c->np;
+  const long long total = static_cast<long long>(c->n_push) * rows;
+  const int grid = static_cast<int>(std::min<long long>((total + 255) / 256, 148LL * 8));
+  k_push<<<grid, 256, 0, c->stream>>>(c->d_peers, buf_id(c, p), p, c->ld, c->d_push.p, c->n_push, rows);
+  CU(cudaGetLastError());
+  ++c->launches;
+}
+
 // Raise our flag at the peers in `mask` (publishing the step scalars to every
 // rank when `publish`).  Returns the epoch of this signal.
 unsigned long long xch_signal(dgb_ctx* c, unsigned mask, bool publish, int dt_idx, int res_idx) {
@@ -1004,8 +1034,6 @@ RunOut run_steps(dgb_ctx* c, const RunSpec& r) {
         a.seq_next = static_cast<unsigned long long>(s + 1) * 8;
         a.sc = c->d_sc;
         a.hist = d_hist && s <= r.hist_cap ? d_hist : nullptr;
-        a.peers = c->d_peers;
-        a.out_buf = buf_id(c, a.out);
         // step start: merge the previous step's scalars (dt bound, residual, error) from every rank
         if (X && k == 0) xch_wait(c, ALL, c->pub_epoch, true, par, par ^ 1);
         const unsigned long long prev = c->epoch;
@@ -1041,9 +1069,9 @@ RunOut run_steps(dgb_ctx* c, const RunSpec& r) {
             if (k > 0) xch_wait(c, c->nb_mask, prev, false, 0, 0);  // the peers' previous stage landed
             a.e0 = n_int;
             a.e1 = c->N;
-            a.push = 1;
             CU(launch_element(c, dgbk::kModeStage, a));
             ++c->launches;
+            xch_push(c, a.out);
           }
         }
         if (X) {
@@ -1062,8 +1090,6 @@ RunOut run_steps(dgb_ctx* c, const RunSpec& r) {
           la.means = means_buf;
           la.seq = static_cast<unsigned long long>(s + 1) * 8;
           la.sc = c->d_sc;
-          la.peers = c->d_peers;
-          la.out_buf = a.out_buf;
           const unsigned long long prev2 = c->epoch;
           Timed tm(c, 3);
           la.e0 = 0;
@@ -1075,9 +1101,9 @@ RunOut run_steps(dgb_ctx* c, const RunSpec& r) {
             xch_wait(c, c->nb_mask, prev2, false, 0, 0);
             la.e0 = n_int;
             la.e1 = c->N;
-            la.push = 1;
             CU(dgbk::launch_limit(0, c->geo, la, c->stream));
             ++c->launches;
+            xch_push(c, la.c);
             if (last)
               xch_signal(c, ALL, true, par ^ 1, par);
             else
@@ -1403,9 +1429,6 @@ int dgb_part_create(const dgb_mesh_view* m, const dgb_tables_view* t, const dgb_
     Geo& g = c->geo;
     g.N = N;
     g.ld = ld;
-    g.send_begin = N;  // no sends until dgb_part_finalize
-    g.send_ptr = nullptr;
-    g.send_ent = nullptr;
     g.tau = c->d_tau.p;
     g.inv_det = c->d_inv_det.p;
     g.inradius = c->d_inradius.p;
@@ -2282,29 +2305,24 @@ int dgb_part_finalize(dgb_ctx* c) {
     for (int r = 0; r < c->world; ++r)
       if (r != c->rank && (!c->h_peers.flag[r] || !c->h_peers.buf[r][0]))
         throw Fail{DGB_ERR_ARG, "peer " + std::to_string(r) + " not attached"};
-    const int nb = c->N - c->n_int;
-    std::vector<int> cnt(nb + 1, 0);
     c->send_mask = 0;
+    std::vector<int4> ent;
     for (int r = 0; r < c->world; ++r) {
       if (!c->sends[r].empty()) c->send_mask |= 1u << r;
-      for (auto& e : c->sends[r]) ++cnt[c->col_of[e.first] - c->n_int + 1];
+      std::vector<std::pair<int, int>> v;  // (peer column, own column)
+      for (auto& e : c->sends[r]) v.emplace_back(e.second, c->col_of[e.first]);
+      std::sort(v.begin(), v.end());
+      for (auto& x : v) ent.push_back(make_int4(x.second, r, x.first, 0));
     }
-    for (int d = 0; d < nb; ++d) cnt[d + 1] += cnt[d];
-    std::vector<int2> ent(std::max(cnt[nb], 1));
-    std::vector<int> fill(cnt.begin(), cnt.end() - 1);
-    for (int r = 0; r < c->world; ++r)
-      for (auto& e : c->sends[r]) ent[fill[c->col_of[e.first] - c->n_int]++] = make_int2(r, e.second);
-    c->d_send_ptr.upload(cnt.data(), cnt.size(), c->stream);
-    c->d_send_ent.upload(ent.data(), ent.size(), c->stream);
-    c->geo.send_ptr = c->d_send_ptr.p;
-    c->geo.send_ent = c->d_send_ent.p;
-    c->geo.send_begin = c->n_int;
+    c->n_push = static_cast<int>(ent.size());
+    if (!ent.empty()) c->d_push.upload(ent.data(), ent.size(), c->stream);
     CU(cudaMemcpyAsync(c->d_peers, &c->h_peers, sizeof(dgbk::PeerTab), cudaMemcpyHostToDevice, c->stream));
     // every kernel a step may launch is loaded now, not lazily while the peers spin in k_wait
     {
       cudaFuncAttributes fa;
       CU(cudaFuncGetAttributes(&fa, k_signal));
       CU(cudaFuncGetAttributes(&fa, k_wait));
+      CU(cudaFuncGetAttributes(&fa, k_push));
     }
     switch (c->p) {
       case 1: CU(dgbk::Launch<1>::preload()); CU(dgbk::preload_limit()); break;
