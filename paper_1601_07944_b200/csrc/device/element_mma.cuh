@@ -146,11 +146,21 @@ __device__ __forceinline__ void fetch_frag(double* __restrict__ slot, const doub
   }
 }
 
-// Projection k-step of a half-live 8-point tile (live points 2t+i only for t < 2): the
-// two k-steps (slot t <- point 2t+i, i = 0, 1) collapse into one whose slot t < 2 takes
-// this lane's point i=0 and slot t >= 2 the point i=1 of lane t-2 (one shuffle per value).
-// The B fragment of that slot is the existing table entry of k-step i=1 at lane-2, so the
-// caller offsets its table index by the returned flag * (one k-step of fragments - 2).
+// Half-live last tiles (p = 3): compact the points before the flux (one flux evaluation per
+// lane, DGB_HALF_* = 1) or after it (two per lane, the fluxes shuffled into the compacted
+// k-step by half_operands).  Measured at p = 3 (1M box, interleaved): volume compacted before
+// 0.681 vs 0.690 ms; the surface compacted before 0.709 ms (eight shuffled trace values and
+// the boundary / neighbour selects per lane cost more than the flux evaluation saved).
+#ifndef DGB_HALF_VOL
+#define DGB_HALF_VOL 1
+#endif
+#ifndef DGB_HALF_SURF
+#define DGB_HALF_SURF 0
+#endif
+// Projection k-step of a half-live 8-point tile from fluxes evaluated at both slots: slot
+// t < 2 takes this lane's point i=0, slot t >= 2 the point i=1 of lane t-2 (one shuffle per
+// value).  The B fragment of that slot is the existing table entry of k-step i=1 at lane-2, so
+// the caller offsets its table index by the returned flag * (one k-step of fragments - 2).
 __device__ __forceinline__ int half_operands(const double (&v)[4][2], double (&a)[4], int lane, int t) {
   const bool hi = t >= 2;
   const int src = (lane + 30) & 31;
@@ -233,7 +243,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
   // packed surface (p = 3, 4): a second neighbour buffer, side q lives in buffer q & 1
   constexpr bool kPk = D::kPacked && (MODE == kModeRhs || MODE == kModeStage);
   // last point tile / last packed surface tile with only slots t < 2 live (p = 3: Q = 12,
-  // 3K = 12): its projection is one compacted k-step (half_operands)
+  // 3K = 12): one compacted projection k-step (DGB_HALF_VOL / DGB_HALF_SURF, half_operands)
   constexpr bool kHalfQ = NQ % 8 == 4 && !D::kTail1;
   constexpr bool kHalfS = kPk && (3 * K) % 8 == 4;
   // stage mode: the epilogue reads the stage input from the own fragment buffer (shared
@@ -354,11 +364,8 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
         } else {
           interp(U[nt & 1], nt);
         }
-        double fr[4][2], fs[4][2];
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const int k = 8 * nt + 2 * t + i;
-          double v[4] = {U[nt & 1][0][i], U[nt & 1][1][i], U[nt & 1][2][i], U[nt & 1][3][i]};
+        // contravariant flux at interior point k from its interpolated state v
+        auto vol_point = [&](double(&v)[4], int k, double(&r_)[4], double(&s_)[4]) {
           Prim w = primitives(v, g1);
           const bool bad = !admissible(v, w);
           if (bad && valid && k < NQ) record_error(sc, err_key(a.seq, kPassVolume, __ldg(geo.ref_id + e), k));
@@ -366,8 +373,42 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
             v[0] = 1.0; v[1] = 0.0; v[2] = 0.0; v[3] = 2.5;
             w.inv = 1.0; w.vx = 0.0; w.vy = 0.0; w.p = 1.0;
           }
-          double r_[4], s_[4];
           contravariant_flux(v, w, ta, tb, tc, td, r_, s_);
+        };
+        if (DGB_HALF_VOL && kHalfQ && nt == NTD - 1) {
+          // half-live last tile (p = 3: points 8..11, live in slots t < 2): slots t >= 2 take the
+          // second point of lane t - 2 before the flux, so every lane evaluates one live point
+          // and its fluxes are already the operands of one compacted projection k-step
+          const bool hi = t >= 2;
+          const int src = (lane + 30) & 31;
+          double v[4];
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            const double o = __shfl_sync(0xffffffffu, U[nt & 1][m][1], src);
+            v[m] = hi ? o : U[nt & 1][m][0];
+          }
+          double ar[4], as[4];
+          vol_point(v, 8 * nt + (hi ? 2 * t - 3 : 2 * t), ar, as);
+          __syncwarp();
+          const int boff = hi ? JT * 32 - 2 : 0;  // the B fragment of k-step i=1 at lane - 2
+#pragma unroll
+          for (int jt = 0; jt < JT; ++jt) {
+            const double br = smem[D::kDr + (nt * 2 * JT + jt) * 32 + lane + boff];
+            const double bs = smem[D::kDs + (nt * 2 * JT + jt) * 32 + lane + boff];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) dmma(R[m][jt], ar[m], br);
+#pragma unroll
+            for (int m = 0; m < 4; ++m) dmma(R[m][jt], as[m], bs);
+          }
+          continue;
+        }
+        double fr[4][2], fs[4][2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int k = 8 * nt + 2 * t + i;
+          double v[4] = {U[nt & 1][0][i], U[nt & 1][1][i], U[nt & 1][2][i], U[nt & 1][3][i]};
+          double r_[4], s_[4];
+          vol_point(v, k, r_, s_);
           const bool live = k < NQ;  // padded points contribute nothing
 #pragma unroll
           for (int m = 0; m < 4; ++m) {
@@ -376,8 +417,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
           }
         }
         __syncwarp();
-        if (kHalfQ && nt == NTD - 1) {
-          // half-live last tile (p = 3: points 8..11): one compacted k-step instead of two
+        if (!DGB_HALF_VOL && kHalfQ && nt == NTD - 1) {
           double ar[4], as[4];
           const int boff = half_operands(fr, ar, lane, t) * (JT * 32 - 2);
           half_operands(fs, as, lane, t);
@@ -500,11 +540,8 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
           if (!kCSmem) own_fetch(tile + nwarps, e_next, nvalid);
         }
         cp_async_commit();
-        // numerical flux at this lane's two packed points, canonical orientation
-        double fn[4][2];
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const int pt = 8 * sp + 2 * t + i;
+        // numerical flux at packed point pt (side pt / K), canonical orientation
+        auto surf_point = [&](double(&UO)[4], double(&UN)[4], int pt, double(&f)[4]) {
           const bool live = pt < 3 * K;
           const int q = live ? pt / K : 0, ko = live ? pt % K : 0;
           const int nb = sel3(q, nbq[0], nbq[1], nbq[2]);
@@ -513,17 +550,10 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
           const double h = sel3(q, eh[0], eh[1], eh[2]);
           const bool left = (inf >> (6 + q)) & 1;
           const bool bnd = nb < 0;
-          double UO[4], UN[4];
-#pragma unroll
-          for (int m = 0; m < 4; ++m) {
-            UO[m] = Tw[m][i];
-            UN[m] = Tn[m][i];
-          }
           const int kc = left ? ko : K - 1 - ko;  // canonical (left-element) point index
           if (BND && bnd && live) ghost_state<K>(UO, nb, ed, kc, nx, ny, tstage, geo, UN);  // boundary: left
           const Prim wo = primitives(UO, g1), wn = primitives(UN, g1);
           const double wh = live ? h * smem[D::kWe + kc] : 0.0;
-          double f[4];
           if (admissible(UO, wo) && admissible(UN, wn)) {
             num_flux_own<FLUX>(UO, wo, UN, wn, nx, ny, gamma, wh, left, f);
           } else {
@@ -531,11 +561,46 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
 #pragma unroll
             for (int m = 0; m < 4; ++m) f[m] = 0.0;
           }
+        };
+        if (DGB_HALF_SURF && kHalfS && sp == D::NSP - 1) {
+          // half-live last packed tile (p = 3: points 8..11, live in slots t < 2): compacted
+          // before the flux as in the volume's last tile, one projection k-step
+          const bool hi = t >= 2;
+          const int src = (lane + 30) & 31;
+          double UO[4], UN[4], an[4];
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            const double oo = __shfl_sync(0xffffffffu, Tw[m][1], src);
+            const double on = __shfl_sync(0xffffffffu, Tn[m][1], src);
+            UO[m] = hi ? oo : Tw[m][0];
+            UN[m] = hi ? on : Tn[m][0];
+          }
+          surf_point(UO, UN, 8 * sp + (hi ? 2 * t - 3 : 2 * t), an);
+          __syncwarp();
+          const int boff = hi ? JT * 32 - 2 : 0;
+#pragma unroll
+          for (int jt = 0; jt < JT; ++jt) {
+            const double b = smem[D::kPkProj + (sp * 2 * JT + jt) * 32 + lane + boff];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) dmma(R[m][jt], an[m], b);
+          }
+          continue;
+        }
+        double fn[4][2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          double UO[4], UN[4], f[4];
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            UO[m] = Tw[m][i];
+            UN[m] = Tn[m][i];
+          }
+          surf_point(UO, UN, 8 * sp + 2 * t + i, f);
 #pragma unroll
           for (int m = 0; m < 4; ++m) fn[m][i] = f[m];
         }
         __syncwarp();
-        if (kHalfS && sp == D::NSP - 1) {  // half-live last packed tile (p = 3): one k-step
+        if (!DGB_HALF_SURF && kHalfS && sp == D::NSP - 1) {
           double an[4];
           const int boff = half_operands(fn, an, lane, t) * (JT * 32 - 2);
 #pragma unroll
