@@ -55,6 +55,9 @@ constexpr int kMmaPackUnroll = DGB_MMA_PACK_UNROLL;
 #ifndef DGB_MMA_TMA
 #define DGB_MMA_TMA(P) 1  // own coefficients of a tile by one TMA box (0: per-lane cp.async)
 #endif
+#ifndef DGB_MMA_SPLIT_J
+#define DGB_MMA_SPLIT_J 1
+#endif
 #ifndef DGB_MMA_PACK_MAXK
 #define DGB_MMA_PACK_MAXK 5  // largest edge-point count K that uses the packed surface
 #endif
@@ -246,6 +249,13 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
   // 3K = 12): one compacted projection k-step (DGB_HALF_VOL / DGB_HALF_SURF, half_operands)
   constexpr bool kHalfQ = NQ % 8 == 4 && !D::kTail1;
   constexpr bool kHalfS = kPk && (3 * K) % 8 == 4;
+  // the last output tile of the projections when it holds at most two live modes (p = 3: modes
+  // 8, 9 in 8 columns): the volume and packed-surface projections accumulate those modes with
+  // DFMAs into X (each lane its own points' share), reduced over the element's four lanes
+  // before the outputs, instead of DMMAs whose output tile is three quarters padding
+  constexpr int kNJR = NP - 8 * (JT - 1);
+  constexpr bool kSplitJ = DGB_MMA_SPLIT_J != 0 && JT > 1 && kNJR <= 2;
+  constexpr int JTD = kSplitJ ? JT - 1 : JT;  // output tiles done with DMMA there
   // stage mode: the epilogue reads the stage input from the own fragment buffer (shared
   // memory) instead of global memory; the next tile's own prefetch waits until then
   constexpr bool kCSmem = P >= DGB_MMA_C_SMEM_MINP && MODE == kModeStage;
@@ -337,6 +347,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
     for (int m = 0; m < 4; ++m)
 #pragma unroll
       for (int jt = 0; jt < JT; ++jt) R[m][jt][0] = R[m][jt][1] = 0.0;
+    double X[4][2] = {};  // kSplitJ: this lane's share of modes 8 (JT - 1) + gg
 
     // ------------------------------------------------------------ volume
     if constexpr (MODE != kModeSurface) {
@@ -392,13 +403,22 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
           __syncwarp();
           const int boff = hi ? JT * 32 - 2 : 0;  // the B fragment of k-step i=1 at lane - 2
 #pragma unroll
-          for (int jt = 0; jt < JT; ++jt) {
+          for (int jt = 0; jt < JTD; ++jt) {
             const double br = smem[D::kDr + (nt * 2 * JT + jt) * 32 + lane + boff];
             const double bs = smem[D::kDs + (nt * 2 * JT + jt) * 32 + lane + boff];
 #pragma unroll
             for (int m = 0; m < 4; ++m) dmma(R[m][jt], ar[m], br);
 #pragma unroll
             for (int m = 0; m < 4; ++m) dmma(R[m][jt], as[m], bs);
+          }
+          if constexpr (kSplitJ) {
+#pragma unroll
+            for (int gg = 0; gg < kNJR; ++gg) {
+              const double dr = smem[D::kDr + (nt * 2 * JT + JT - 1) * 32 + 4 * gg + t + boff];
+              const double ds = smem[D::kDs + (nt * 2 * JT + JT - 1) * 32 + 4 * gg + t + boff];
+#pragma unroll
+              for (int m = 0; m < 4; ++m) X[m][gg] = fma(dr, ar[m], fma(ds, as[m], X[m][gg]));
+            }
           }
           continue;
         }
@@ -422,7 +442,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
           const int boff = half_operands(fr, ar, lane, t) * (JT * 32 - 2);
           half_operands(fs, as, lane, t);
 #pragma unroll
-          for (int jt = 0; jt < JT; ++jt) {
+          for (int jt = 0; jt < JTD; ++jt) {
             const double br = smem[D::kDr + (nt * 2 * JT + jt) * 32 + lane + boff];
             const double bs = smem[D::kDs + (nt * 2 * JT + jt) * 32 + lane + boff];
 #pragma unroll
@@ -430,12 +450,21 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
 #pragma unroll
             for (int m = 0; m < 4; ++m) dmma(R[m][jt], as[m], bs);
           }
+          if constexpr (kSplitJ) {
+#pragma unroll
+            for (int gg = 0; gg < kNJR; ++gg) {
+              const double dr = smem[D::kDr + (nt * 2 * JT + JT - 1) * 32 + 4 * gg + t + boff];
+              const double ds = smem[D::kDs + (nt * 2 * JT + JT - 1) * 32 + 4 * gg + t + boff];
+#pragma unroll
+              for (int m = 0; m < 4; ++m) X[m][gg] = fma(dr, ar[m], fma(ds, as[m], X[m][gg]));
+            }
+          }
           continue;
         }
 #pragma unroll
         for (int i = 0; i < 2; ++i)
 #pragma unroll
-          for (int jt = 0; jt < JT; ++jt) {
+          for (int jt = 0; jt < JTD; ++jt) {
             const double br = smem[D::kDr + ((nt * 2 + i) * JT + jt) * 32 + lane];
 #pragma unroll
             for (int m = 0; m < 4; ++m) dmma(R[m][jt], fr[m][i], br);
@@ -443,11 +472,22 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
 #pragma unroll
         for (int i = 0; i < 2; ++i)
 #pragma unroll
-          for (int jt = 0; jt < JT; ++jt) {
+          for (int jt = 0; jt < JTD; ++jt) {
             const double bs = smem[D::kDs + ((nt * 2 + i) * JT + jt) * 32 + lane];
 #pragma unroll
             for (int m = 0; m < 4; ++m) dmma(R[m][jt], fs[m][i], bs);
           }
+        if constexpr (kSplitJ) {
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int gg = 0; gg < kNJR; ++gg) {
+              const double dr = smem[D::kDr + ((nt * 2 + i) * JT + JT - 1) * 32 + 4 * gg + t];
+              const double ds = smem[D::kDs + ((nt * 2 + i) * JT + JT - 1) * 32 + 4 * gg + t];
+#pragma unroll
+              for (int m = 0; m < 4; ++m) X[m][gg] = fma(dr, fr[m][i], fma(ds, fs[m][i], X[m][gg]));
+            }
+        }
       }
       if constexpr (D::kTail1) {
         // the last interior point: the 4 lanes of an element reduce their modes' share
@@ -579,10 +619,18 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
           __syncwarp();
           const int boff = hi ? JT * 32 - 2 : 0;
 #pragma unroll
-          for (int jt = 0; jt < JT; ++jt) {
+          for (int jt = 0; jt < JTD; ++jt) {
             const double b = smem[D::kPkProj + (sp * 2 * JT + jt) * 32 + lane + boff];
 #pragma unroll
             for (int m = 0; m < 4; ++m) dmma(R[m][jt], an[m], b);
+          }
+          if constexpr (kSplitJ) {
+#pragma unroll
+            for (int gg = 0; gg < kNJR; ++gg) {
+              const double b = smem[D::kPkProj + (sp * 2 * JT + JT - 1) * 32 + 4 * gg + t + boff];
+#pragma unroll
+              for (int m = 0; m < 4; ++m) X[m][gg] = fma(b, an[m], X[m][gg]);
+            }
           }
           continue;
         }
@@ -604,21 +652,39 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
           double an[4];
           const int boff = half_operands(fn, an, lane, t) * (JT * 32 - 2);
 #pragma unroll
-          for (int jt = 0; jt < JT; ++jt) {
+          for (int jt = 0; jt < JTD; ++jt) {
             const double b = smem[D::kPkProj + (sp * 2 * JT + jt) * 32 + lane + boff];
 #pragma unroll
             for (int m = 0; m < 4; ++m) dmma(R[m][jt], an[m], b);
+          }
+          if constexpr (kSplitJ) {
+#pragma unroll
+            for (int gg = 0; gg < kNJR; ++gg) {
+              const double b = smem[D::kPkProj + (sp * 2 * JT + JT - 1) * 32 + 4 * gg + t + boff];
+#pragma unroll
+              for (int m = 0; m < 4; ++m) X[m][gg] = fma(b, an[m], X[m][gg]);
+            }
           }
           continue;
         }
 #pragma unroll
         for (int i = 0; i < 2; ++i)
 #pragma unroll
-          for (int jt = 0; jt < JT; ++jt) {
+          for (int jt = 0; jt < JTD; ++jt) {
             const double b = smem[D::kPkProj + ((sp * 2 + i) * JT + jt) * 32 + lane];
 #pragma unroll
             for (int m = 0; m < 4; ++m) dmma(R[m][jt], fn[m][i], b);
           }
+        if constexpr (kSplitJ) {
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int gg = 0; gg < kNJR; ++gg) {
+              const double b = smem[D::kPkProj + ((sp * 2 + i) * JT + JT - 1) * 32 + 4 * gg + t];
+#pragma unroll
+              for (int m = 0; m < 4; ++m) X[m][gg] = fma(b, fn[m][i], X[m][gg]);
+            }
+        }
       }
     } else if constexpr (MODE != kModeVolume) {
       double enx[3], eny[3], eh[3];
@@ -738,6 +804,20 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
       __syncwarp();
       own_fetch(tile + nwarps, e_next, nvalid);
       cp_async_commit();
+    }
+
+    if constexpr (kSplitJ && MODE != kModeSurface) {
+      // modes 8 (JT - 1) + gg: the four lanes' shares, summed in the same order on every lane;
+      // lane t = 0 holds output columns 8 (JT - 1) + ii, the other lanes' columns are padding
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int gg = 0; gg < kNJR; ++gg) {
+          double x = X[m][gg];
+          x += __shfl_xor_sync(0xffffffffu, x, 1);
+          x += __shfl_xor_sync(0xffffffffu, x, 2);
+          R[m][JT - 1][gg] += t == 0 ? x : 0.0;
+        }
     }
 
     // ------------------------------------------------------------ outputs (lane: element g, modes 8jt+2t+ii)
