@@ -345,7 +345,7 @@ def run_b200(args, rank, world, local, pg):
                    "timing": "value: K steps without per-kernel events; roofline kernel_ms: median over >= 100 "
                              "stage-kernel launches timed with CUDA events on their stream in a second pass",
                    "parallelism": (f"element partition x{world} (contiguous strips), peer-memory halo "
-                                   "exchange fused into the stage kernel") if world > 1 else "single GPU"},
+                                   "exchange by a push kernel right behind the boundary-element stage launch") if world > 1 else "single GPU"},
         "roofline": dict(dom["roofline"], p=dom["p"],
                          note=f"dominant kernel = fused stage kernel at p={dom['p']} (median launch); "
                               f"HBM peak {hbm_src}; FP64 peak measured in-run (DFMA loop) {fp64_tf:.1f} TF/s"),
@@ -473,9 +473,9 @@ def leg_c5(args, local, stream, hbm_gbs, fp64_tf):
 def leg_c5_partitioned(args, rank, world, local, stream, pg, hbm_gbs, fp64_tf):
     """BASELINE configs[4] (C5) at N > 1: the 8M-triangle box (2000 x 2000, periodic, isentropic
     vortex), p = 2..4, SSP-RK3, partitioned across the N ranks (contiguous strips, peer-memory
-    halo exchange fused into the stage kernel, CUDA IPC between the processes): strong scaling of a
-    fixed mesh, device-timed as the max over ranks.  The halo bytes per stage are the send lists'
-    element columns x 4 Np doubles, pushed by the stage kernel over NVLink P2P."""
+    halo exchange, CUDA IPC between the processes): strong scaling of a fixed mesh, device-timed
+    as the max over ranks.  The halo bytes per stage are the send lists' element columns x 4 Np
+    doubles, pushed by the halo push kernel (k_push) over NVLink P2P."""
     from paper_1601_07944_b200 import _lib as L
     from paper_1601_07944_b200 import dg2d
     from paper_1601_07944_b200 import dist as D
