@@ -58,6 +58,12 @@ constexpr int kMmaPackUnroll = DGB_MMA_PACK_UNROLL;
 #ifndef DGB_MMA_SPLIT_J
 #define DGB_MMA_SPLIT_J 1
 #endif
+#ifndef DGB_MMA_SPLIT_K
+// the last mode k-step of interpolations and traces by DFMAs when <= 2 modes are live: p=3
+// 0.687 vs 0.666 ms, p=5 1.549 vs 1.533 (fewer DMMAs, 120 -> 92 per tile at p=3, but the
+// lane-indexed table loads and the dependent DFMA chains sit on the flux's critical path)
+#define DGB_MMA_SPLIT_K 0
+#endif
 #ifndef DGB_MMA_PACK_MAXK
 #define DGB_MMA_PACK_MAXK 5  // largest edge-point count K that uses the packed surface
 #endif
@@ -256,6 +262,13 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
   constexpr int kNJR = NP - 8 * (JT - 1);
   constexpr bool kSplitJ = DGB_MMA_SPLIT_J != 0 && JT > 1 && kNJR <= 2;
   constexpr int JTD = kSplitJ ? JT - 1 : JT;  // output tiles done with DMMA there
+  // the last mode k-step of the interpolations and traces when it holds at most two live modes
+  // (p = 3: modes 8, 9 of 8..11; p = 5: mode 20): DFMAs on the lane's own output columns instead
+  // of a half- or quarter-live DMMA.  Own and neighbour traces take the same path in the same
+  // order, so the two sides of an edge still see bit-identical traces.
+  constexpr int kNKR = NP - 4 * (KS - 1);
+  constexpr bool kSplitK = DGB_MMA_SPLIT_K != 0 && kNKR <= 2;
+  constexpr int KSD = kSplitK ? KS - 1 : KS;  // k-steps done with DMMA
   // stage mode: the epilogue reads the stage input from the own fragment buffer (shared
   // memory) instead of global memory; the next tile's own prefetch waits until then
   constexpr bool kCSmem = P >= DGB_MMA_C_SMEM_MINP && MODE == kModeStage;
@@ -291,6 +304,32 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
     } else {
       return w_own[(m * KS + ks) * 32 + lane];
     }
+  };
+
+  // coefficient j >= 4 (KS - 1) of element g from the own buffer / a neighbour fragment buffer
+  auto own_c = [&](int m, int j) -> double {
+    if constexpr (kTma) {
+      return w_own[(m * NP + j) * 8 + g];
+    } else {
+      return w_own[(m * KS + KS - 1) * 32 + 4 * g + (j - 4 * (KS - 1))];
+    }
+  };
+  // kSplitK: acc[m][ii] += sum_jj c(m, jj) B[jj][2t + ii] over the live modes of the last
+  // k-step, B the k-step's fragment (B[t'][g'] at 4 g' + t')
+  auto ktail = [&](double(&acc)[4][2], const double* __restrict__ frag, auto cval) {
+    double ph[2][2];
+#pragma unroll
+    for (int ii = 0; ii < 2; ++ii)
+#pragma unroll
+      for (int jj = 0; jj < kNKR; ++jj) ph[ii][jj] = frag[4 * (2 * t + ii) + jj];
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+#pragma unroll
+      for (int jj = 0; jj < kNKR; ++jj) {
+        const double c = cval(m, jj);
+#pragma unroll
+        for (int ii = 0; ii < 2; ++ii) acc[m][ii] = fma(c, ph[ii][jj], acc[m][ii]);
+      }
   };
 
   double lam_min = __longlong_as_double(0x7ff0000000000000ll);
@@ -358,11 +397,13 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
 #pragma unroll
         for (int m = 0; m < 4; ++m) u[m][0] = u[m][1] = 0.0;
 #pragma unroll
-        for (int ks = 0; ks < KS; ++ks) {
+        for (int ks = 0; ks < KSD; ++ks) {
           const double b = smem[D::kPhi + (ks * NT + nt) * 32 + lane];
 #pragma unroll
           for (int m = 0; m < 4; ++m) dmma(u[m], own_a(m, ks), b);
         }
+        if constexpr (kSplitK)
+          ktail(u, smem + D::kPhi + ((KS - 1) * NT + nt) * 32, [&](int m, int jj) { return own_c(m, 4 * (KS - 1) + jj); });
       };
       constexpr int NTD = D::NTD;
       if (DGB_MMA_VOL_PIPE(P)) interp(U[0], 0);
@@ -542,11 +583,13 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
 #pragma unroll
         for (int m = 0; m < 4; ++m) Tw[m][0] = Tw[m][1] = Tn[m][0] = Tn[m][1] = 0.0;
 #pragma unroll
-        for (int ks = 0; ks < KS; ++ks) {
+        for (int ks = 0; ks < KSD; ++ks) {
           const double b = smem[D::kPkOwn + (sp * KS + ks) * 32 + lane];
 #pragma unroll
           for (int m = 0; m < 4; ++m) dmma(Tw[m], own_a(m, ks), b);
         }
+        if constexpr (kSplitK)
+          ktail(Tw, smem + D::kPkOwn + (sp * KS + KS - 1) * 32, [&](int m, int jj) { return own_c(m, 4 * (KS - 1) + jj); });
         // neighbour traces of the sides present in this tile (their columns only)
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
@@ -559,7 +602,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
             todo &= todo - 1;
             const bool mine = snb_q == cls;
 #pragma unroll
-            for (int ks = 0; ks < KS; ++ks) {
+            for (int ks = 0; ks < KSD; ++ks) {
               const double b = smem[D::kPkNb + (((sp * 3 + q) * 3 + (cls - 1)) * KS + ks) * 32 + lane];
 #pragma unroll
               for (int m = 0; m < 4; ++m) {
@@ -567,6 +610,10 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
                 dmma(Tn[m], mine ? an : 0.0, b);
               }
             }
+            if constexpr (kSplitK)
+              ktail(Tn, smem + D::kPkNb + (((sp * 3 + q) * 3 + (cls - 1)) * KS + KS - 1) * 32, [&](int m, int jj) {
+                return mine ? nbuf[(m * KS + KS - 1) * 32 + 4 * g + jj] : 0.0;
+              });
           }
         }
         __syncwarp();
@@ -714,11 +761,13 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
 #pragma unroll
         for (int m = 0; m < 4; ++m) Tw[m][0] = Tw[m][1] = 0.0;
 #pragma unroll
-        for (int ks = 0; ks < KS; ++ks) {
+        for (int ks = 0; ks < KSD; ++ks) {
           const double b = smem[D::kPhe + (q * KS + ks) * 32 + lane];
 #pragma unroll
           for (int m = 0; m < 4; ++m) dmma(Tw[m], own_a(m, ks), b);
         }
+        if constexpr (kSplitK)
+          ktail(Tw, smem + D::kPhe + (q * KS + KS - 1) * 32, [&](int m, int jj) { return own_c(m, 4 * (KS - 1) + jj); });
         // neighbour trace (reversed points) — one pass per neighbour side label
         // present in the warp (class renumbering makes that one pass almost always)
         double Tn[4][2];
@@ -730,7 +779,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
           todo &= todo - 1;
           const bool mine = snb == s;
 #pragma unroll
-          for (int ks = 0; ks < KS; ++ks) {
+          for (int ks = 0; ks < KSD; ++ks) {
             const double b = smem[D::kPheR + ((s - 1) * KS + ks) * 32 + lane];
 #pragma unroll
             for (int m = 0; m < 4; ++m) {
@@ -738,6 +787,10 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
               dmma(Tn[m], mine ? an : 0.0, b);  // a select, not an FP64 multiply
             }
           }
+          if constexpr (kSplitK)
+            ktail(Tn, smem + D::kPheR + ((s - 1) * KS + KS - 1) * 32, [&](int m, int jj) {
+              return mine ? w_nbr[(m * KS + KS - 1) * 32 + 4 * g + jj] : 0.0;
+            });
         }
         __syncwarp();
         // the neighbour buffer is consumed: prefetch the next side (after side 2: the
