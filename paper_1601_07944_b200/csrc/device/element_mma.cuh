@@ -58,6 +58,11 @@ constexpr int kMmaPackUnroll = DGB_MMA_PACK_UNROLL;
 #ifndef DGB_MMA_SPLIT_J
 #define DGB_MMA_SPLIT_J 1
 #endif
+#ifndef DGB_MMA_SPLIT_JV
+// p=5 volume projection of modes 16..20 by DFMAs (288 -> 240 DMMAs per tile): 1.632 vs 1.553 ms,
+// the 20 partial sums push the 168-register kernel into more spills
+#define DGB_MMA_SPLIT_JV 0
+#endif
 #ifndef DGB_MMA_SPLIT_K
 // the last mode k-step of interpolations and traces by DFMAs when <= 2 modes are live: p=3
 // 0.687 vs 0.666 ms, p=5 1.549 vs 1.533 (fewer DMMAs, 120 -> 92 per tile at p=3, but the
@@ -262,6 +267,11 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
   constexpr int kNJR = NP - 8 * (JT - 1);
   constexpr bool kSplitJ = DGB_MMA_SPLIT_J != 0 && JT > 1 && kNJR <= 2;
   constexpr int JTD = kSplitJ ? JT - 1 : JT;  // output tiles done with DMMA there
+  // the volume projection alone split the same way when the last output tile holds up to five
+  // live modes (p = 5: modes 16..20), X folded into R right after the volume integral
+  constexpr bool kSplitJV = !kSplitJ && DGB_MMA_SPLIT_JV != 0 && JT > 1 && kNJR <= 5;
+  constexpr bool kSplitJVol = kSplitJ || kSplitJV;
+  constexpr int JTDV = kSplitJVol ? JT - 1 : JT;
   // the last mode k-step of the interpolations and traces when it holds at most two live modes
   // (p = 3: modes 8, 9 of 8..11; p = 5: mode 20): DFMAs on the lane's own output columns instead
   // of a half- or quarter-live DMMA.  Own and neighbour traces take the same path in the same
@@ -386,7 +396,20 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
     for (int m = 0; m < 4; ++m)
 #pragma unroll
       for (int jt = 0; jt < JT; ++jt) R[m][jt][0] = R[m][jt][1] = 0.0;
-    double X[4][2] = {};  // kSplitJ: this lane's share of modes 8 (JT - 1) + gg
+    double X[4][kNJR] = {};  // kSplitJ / kSplitJV: this lane's share of modes 8 (JT - 1) + gg
+    // the four lanes' shares of X summed in the same order on every lane; lane t holds output
+    // columns 8 (JT - 1) + 2t + ii (the columns >= NP are padding)
+    auto fold_x = [&]() {
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int gg = 0; gg < kNJR; ++gg) {
+          double x = X[m][gg];
+          x += __shfl_xor_sync(0xffffffffu, x, 1);
+          x += __shfl_xor_sync(0xffffffffu, x, 2);
+          R[m][JT - 1][gg & 1] += (gg >> 1) == t ? x : 0.0;
+        }
+    };
 
     // ------------------------------------------------------------ volume
     if constexpr (MODE != kModeSurface) {
@@ -444,7 +467,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
           __syncwarp();
           const int boff = hi ? JT * 32 - 2 : 0;  // the B fragment of k-step i=1 at lane - 2
 #pragma unroll
-          for (int jt = 0; jt < JTD; ++jt) {
+          for (int jt = 0; jt < JTDV; ++jt) {
             const double br = smem[D::kDr + (nt * 2 * JT + jt) * 32 + lane + boff];
             const double bs = smem[D::kDs + (nt * 2 * JT + jt) * 32 + lane + boff];
 #pragma unroll
@@ -452,7 +475,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
 #pragma unroll
             for (int m = 0; m < 4; ++m) dmma(R[m][jt], as[m], bs);
           }
-          if constexpr (kSplitJ) {
+          if constexpr (kSplitJVol) {
 #pragma unroll
             for (int gg = 0; gg < kNJR; ++gg) {
               const double dr = smem[D::kDr + (nt * 2 * JT + JT - 1) * 32 + 4 * gg + t + boff];
@@ -483,7 +506,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
           const int boff = half_operands(fr, ar, lane, t) * (JT * 32 - 2);
           half_operands(fs, as, lane, t);
 #pragma unroll
-          for (int jt = 0; jt < JTD; ++jt) {
+          for (int jt = 0; jt < JTDV; ++jt) {
             const double br = smem[D::kDr + (nt * 2 * JT + jt) * 32 + lane + boff];
             const double bs = smem[D::kDs + (nt * 2 * JT + jt) * 32 + lane + boff];
 #pragma unroll
@@ -491,7 +514,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
 #pragma unroll
             for (int m = 0; m < 4; ++m) dmma(R[m][jt], as[m], bs);
           }
-          if constexpr (kSplitJ) {
+          if constexpr (kSplitJVol) {
 #pragma unroll
             for (int gg = 0; gg < kNJR; ++gg) {
               const double dr = smem[D::kDr + (nt * 2 * JT + JT - 1) * 32 + 4 * gg + t + boff];
@@ -505,7 +528,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
 #pragma unroll
         for (int i = 0; i < 2; ++i)
 #pragma unroll
-          for (int jt = 0; jt < JTD; ++jt) {
+          for (int jt = 0; jt < JTDV; ++jt) {
             const double br = smem[D::kDr + ((nt * 2 + i) * JT + jt) * 32 + lane];
 #pragma unroll
             for (int m = 0; m < 4; ++m) dmma(R[m][jt], fr[m][i], br);
@@ -513,12 +536,12 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
 #pragma unroll
         for (int i = 0; i < 2; ++i)
 #pragma unroll
-          for (int jt = 0; jt < JTD; ++jt) {
+          for (int jt = 0; jt < JTDV; ++jt) {
             const double bs = smem[D::kDs + ((nt * 2 + i) * JT + jt) * 32 + lane];
 #pragma unroll
             for (int m = 0; m < 4; ++m) dmma(R[m][jt], fs[m][i], bs);
           }
-        if constexpr (kSplitJ) {
+        if constexpr (kSplitJVol) {
 #pragma unroll
           for (int i = 0; i < 2; ++i)
 #pragma unroll
@@ -563,6 +586,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
           }
         __syncwarp();
       }
+      if constexpr (kSplitJV) fold_x();
     }
 
     // ------------------------------------------------------------ surface
@@ -859,19 +883,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
       cp_async_commit();
     }
 
-    if constexpr (kSplitJ && MODE != kModeSurface) {
-      // modes 8 (JT - 1) + gg: the four lanes' shares, summed in the same order on every lane;
-      // lane t = 0 holds output columns 8 (JT - 1) + ii, the other lanes' columns are padding
-#pragma unroll
-      for (int m = 0; m < 4; ++m)
-#pragma unroll
-        for (int gg = 0; gg < kNJR; ++gg) {
-          double x = X[m][gg];
-          x += __shfl_xor_sync(0xffffffffu, x, 1);
-          x += __shfl_xor_sync(0xffffffffu, x, 2);
-          R[m][JT - 1][gg] += t == 0 ? x : 0.0;
-        }
-    }
+    if constexpr (kSplitJ && MODE != kModeSurface) fold_x();
 
     // ------------------------------------------------------------ outputs (lane: element g, modes 8jt+2t+ii)
     if constexpr (MODE == kModeVolume || MODE == kModeRhs) {
