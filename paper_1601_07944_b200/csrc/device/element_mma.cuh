@@ -63,6 +63,11 @@ constexpr int kMmaPackUnroll = DGB_MMA_PACK_UNROLL;
 // the 20 partial sums push the 168-register kernel into more spills
 #define DGB_MMA_SPLIT_JV 0
 #endif
+#ifndef DGB_MMA_EDGE_EARLY
+// issue the edge-normal gathers before the volume integral instead of at the surface: p=3, 4
+// unchanged (0.667 / 0.980 ms), p=5 1.598 vs 1.550 (nine more live doubles across the volume)
+#define DGB_MMA_EDGE_EARLY(P) 0
+#endif
 #ifndef DGB_MMA_SPLIT_K
 // the last mode k-step of interpolations and traces by DFMAs when <= 2 modes are live: p=3
 // 0.687 vs 0.666 ms, p=5 1.549 vs 1.533 (fewer DMMAs, 120 -> 92 per tile at p=3, but the
@@ -276,6 +281,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
   // (p = 3: modes 8, 9 of 8..11; p = 5: mode 20): DFMAs on the lane's own output columns instead
   // of a half- or quarter-live DMMA.  Own and neighbour traces take the same path in the same
   // order, so the two sides of an edge still see bit-identical traces.
+  constexpr bool kEdgeEarly = DGB_MMA_EDGE_EARLY(P) != 0;
   constexpr int kNKR = NP - 4 * (KS - 1);
   constexpr bool kSplitK = DGB_MMA_SPLIT_K != 0 && kNKR <= 2;
   constexpr int KSD = kSplitK ? KS - 1 : KS;  // k-steps done with DMMA
@@ -390,6 +396,17 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
       own_phase ^= 1u;
     }
     __syncwarp();
+    // edge normals and lengths of the tile's three sides (gathered by edge id)
+    double enx[3], eny[3], eh[3];
+    auto load_edges = [&]() {
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        enx[q] = __ldg(geo.enx + edq[q]);
+        eny[q] = __ldg(geo.eny + edq[q]);
+        eh[q] = __ldg(geo.eh + edq[q]);
+      }
+    };
+    if constexpr (kEdgeEarly && MODE != kModeVolume) load_edges();  // in flight during the volume integral
 
     double R[4][JT][2];
 #pragma unroll
@@ -591,13 +608,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
 
     // ------------------------------------------------------------ surface
     if constexpr (kPk) {
-      double enx[3], eny[3], eh[3];
-#pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        enx[q] = __ldg(geo.enx + edq[q]);
-        eny[q] = __ldg(geo.eny + edq[q]);
-        eh[q] = __ldg(geo.eh + edq[q]);
-      }
+      if constexpr (!kEdgeEarly) load_edges();
       auto sel3 = [](int q, auto x0, auto x1, auto x2) { return q == 0 ? x0 : (q == 1 ? x1 : x2); };
 #pragma unroll kMmaPackUnroll
       for (int sp = 0; sp < D::NSP; ++sp) {
@@ -758,13 +769,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
         }
       }
     } else if constexpr (MODE != kModeVolume) {
-      double enx[3], eny[3], eh[3];
-#pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        enx[q] = __ldg(geo.enx + edq[q]);
-        eny[q] = __ldg(geo.eny + edq[q]);
-        eh[q] = __ldg(geo.eh + edq[q]);
-      }
+      if constexpr (!kEdgeEarly) load_edges();
 #pragma unroll kMmaSideUnroll
       for (int q = 0; q < 3; ++q) {
         const int nb = nbq[q];
