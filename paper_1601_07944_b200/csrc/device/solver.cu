@@ -892,10 +892,12 @@ unsigned all_peers(const dgb_ctx* c) { return ((1u << c->world) - 1u) & ~(1u << 
 // Push the send elements' columns of `p` (one of the rotating buffers) to the peers.
 void xch_push(dgb_ctx* c, const double* p) {
   if (c->n_push == 0) return;
+  const int buf = buf_id(c, p);
+  if (buf < 0) throw Fail{DGB_ERR_ARG, "halo push from a buffer the peers do not map"};
   const int rows = 4 * c->np;
   const long long total = static_cast<long long>(c->n_push) * rows;
   const int grid = static_cast<int>(std::min<long long>((total + 255) / 256, 148LL * 8));
-  k_push<<<grid, 256, 0, c->stream>>>(c->d_peers, buf_id(c, p), p, c->ld, c->d_push.p, c->n_push, rows);
+  k_push<<<grid, 256, 0, c->stream>>>(c->d_peers, buf, p, c->ld, c->d_push.p, c->n_push, rows);
   CU(cudaGetLastError());
   ++c->launches;
 }
