@@ -510,7 +510,7 @@ def leg_c5_partitioned(args, rank, world, local, stream, pg, hbm_gbs, fp64_tf):
                                  "roofline_rank0": roofline(p, e, int(info.n_owned), k, hbm_gbs, fp64_tf)})
     out["value"] = upd_tot / (ms_tot * 1e-3)
     out["unit"] = "DOF-updates/s/stage"
-    out["exchange"] = "CUDA IPC peer mappings (dgb_part_attach_peer_ipc); halo columns written by the stage kernel"
+    out["exchange"] = "CUDA IPC peer mappings (dgb_part_attach_peer_ipc); halo columns written by the push kernel (k_push) behind the boundary stage launch"
     return out
 
 
