@@ -113,6 +113,12 @@ int dgb_set_flux(dgb_ctx* ctx, int flux);
  * the fused launch on meshes up to 400K triangles, where it saves a launch per stage, the two
  * kernels above (measured).  All give bit-identical results. */
 int dgb_set_fused_limiter(dgb_ctx* ctx, int enable);
+/* Trace buffers (no reference counterpart: a data-layout choice of the device step loop).  With
+ * enable = 1, the stages of a run at p = 3, 4 on a whole mesh without limiting write the edge
+ * traces of their output and the next stage reads its own and its neighbours' traces instead of
+ * interpolating them from the coefficient columns; 0 interpolates every stage.  Default from
+ * env DGB_TRACE_BUF at creation.  Both give bit-identical results. */
+int dgb_set_trace_buffers(dgb_ctx* ctx, int enable);
 /* Launch forms for small meshes (no reference counterpart: the CPU has no launch shape).  A p <= 2
  * stage launch of at most stage_max_n elements, and a limiter launch of at most limit_max_n, take
  * the four-lanes-per-element latency form instead of one thread per element; -1 = the built-in

@@ -138,6 +138,7 @@ _sig("dgb_launch_count", C.c_int64, _vp)
 _sig("dgb_stage_kernel_ms", C.c_int, _vp, c_double_p, c_int64_p)
 _sig("dgb_set_fused_limiter", C.c_int, _vp, C.c_int)
 _sig("dgb_set_latency_forms", C.c_int, _vp, C.c_int, C.c_int)
+_sig("dgb_set_trace_buffers", C.c_int, _vp, C.c_int)
 _sig("dgb_set_dirichlet_stages", C.c_int, _vp, C.c_int, c_double_p)
 _sig("dgb_scheme_stage_times", C.c_int, C.c_int, c_double_p, C.POINTER(C.c_int))
 _sig("dgb_timer_samples", C.c_int, _vp, C.c_int, c_double_p, C.c_int64, c_int64_p)

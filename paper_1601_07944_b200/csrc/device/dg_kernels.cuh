@@ -116,7 +116,10 @@ enum : int { kModeVolume = 0, kModeSurface = 1, kModeRhs = 2, kModeStage = 3 };
 // use, the CFL wave speeds are wanted (last stage of a step), the partition has elements
 // on the physical boundary.  Each unused path is compiled out of its instance, which
 // frees registers in the common case (SSP / midpoint stages, periodic meshes).
-enum : int { kVarRk4 = 1, kVarLambda = 2, kVarBoundary = 4 };
+enum : int { kVarRk4 = 1, kVarLambda = 2, kVarBoundary = 4, kVarTrace = 8 };
+// kVarTrace (stage mode, packed-surface degrees p = 3, 4): the own and neighbour edge traces of
+// the stage input are read from the trace buffer its producing stage wrote (StageArgs::tr_in)
+// instead of being interpolated from the coefficient columns.
 
 struct StageArgs {
   const double* __restrict__ in;  // stage input coefficients
@@ -128,6 +131,10 @@ struct StageArgs {
   double* __restrict__ out;       // output (volume / slots / deriv / next stage)
   double* __restrict__ kacc;      // RK4 derivative accumulator
   double* __restrict__ means;     // p <= 2 with a limiter kernel next: the new cell means, [ld][4] (null: none)
+  // edge traces, [4][3K][ld] (packed point pt = side * K + point, the element's own orientation):
+  // tr_in those of `in` (kVarTrace instances), tr_out those of `out` (written when non-null)
+  const double* __restrict__ tr_in;
+  double* __restrict__ tr_out;
   double alpha, beta, gcoef;      // out = alpha u + beta in + (gcoef dt) L(in)
   double tcoef;                   // stage time = t + tcoef dt
   int kmode;                      // 0 none, 1 kacc = L, 2 kacc += 2L, 3 out = u + dt/6 (kacc + L)

@@ -55,6 +55,12 @@ constexpr int kMmaPackUnroll = DGB_MMA_PACK_UNROLL;
 #ifndef DGB_MMA_TMA
 #define DGB_MMA_TMA(P) 1  // own coefficients of a tile by one TMA box (0: per-lane cp.async)
 #endif
+#ifndef DGB_TRACE_P
+// degrees with trace-buffer stage instances (kVarTrace) and the epilogue's trace write; measured
+// per stage (interleaved): p=4 0.930 vs 0.980 ms; p=3 0.670 vs 0.666 (its tensor work is not what
+// bounds it), and the epilogue branch alone costs the p=3 instances 1 %
+#define DGB_TRACE_P(P) ((P) == 4)
+#endif
 #ifndef DGB_MMA_SPLIT_J
 #define DGB_MMA_SPLIT_J 1
 #endif
@@ -265,6 +271,12 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
   // 3K = 12): one compacted projection k-step (DGB_HALF_VOL / DGB_HALF_SURF, half_operands)
   constexpr bool kHalfQ = NQ % 8 == 4 && !D::kTail1;
   constexpr bool kHalfS = kPk && (3 * K) % 8 == 4;
+  // trace-buffer instance: the packed surface reads the own and neighbour traces of the stage
+  // input from a.tr_in (staged into the two neighbour buffers by cp.async one tile ahead, own
+  // traces in w_nbr, the neighbours' reversed traces in w_nbr2, both [4][3K][8 elements])
+  // instead of interpolating them; the epilogue writes the traces of the new stage (a.tr_out)
+  constexpr bool kTrIn = kPk && MODE == kModeStage && DGB_TRACE_P(P) && (VAR & kVarTrace) != 0;
+  constexpr int K3 = 3 * K;
   // the last output tile of the projections when it holds at most two live modes (p = 3: modes
   // 8, 9 in 8 columns): the volume and packed-surface projections accumulate those modes with
   // DFMAs into X (each lane its own points' share), reduced over the element's four lanes
@@ -357,6 +369,23 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
     return ok ? e : a.e1 - 1;
   };
   auto nbr_of = [&](int e, int q) { return __ldg(geo.nbr + q * ld + e); };
+  // kTrIn: traces of element column col (lane group g) and of its neighbours nb[] (side labels in
+  // inf_) into the neighbour buffers; lane t copies rows t, t + 4, ... of the 4 * 3K rows
+  auto fetch_traces = [&](int col, bool ok, const int (&nb)[3], int inf_) {
+    if constexpr (kTrIn) {
+#pragma unroll
+      for (int i = 0; i < K3; ++i) {
+        const int r = 4 * i + t;
+        const int m = r / K3, pt = r - m * K3, q = pt / K, ko = pt - q * K;
+        cp_async8(w_nbr + r * 8 + g, ok ? a.tr_in + static_cast<long long>(r) * ld + col : a.tr_in, ok);
+        const int nbc = q == 0 ? nb[0] : (q == 1 ? nb[1] : nb[2]);
+        const int sl = (inf_ >> (2 * q)) & 3;  // the neighbour's side label (1..3), 0 = boundary
+        const bool okn = ok && nbc >= 0 && sl != 0;
+        const int rn = m * K3 + (sl - 1) * K + (K - 1 - ko);
+        cp_async8(w_nbr2 + r * 8 + g, okn ? a.tr_in + static_cast<long long>(rn) * ld + nbc : a.tr_in, okn);
+      }
+    }
+  };
 
   // pipeline prologue: own coefficients and side-0 neighbours of the first tile
   int nbq[3] = {-4, -4, -4};  // neighbour columns of the current tile's element
@@ -368,8 +397,12 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
     if constexpr (MODE != kModeVolume) {
 #pragma unroll
       for (int q = 0; q < 3; ++q) nbq[q] = nbr_of(e, q);
-      fetch_frag<NP, KS>(w_nbr, a.in, ld, nbq[0], ok && nbq[0] >= 0, lane, t);
-      if constexpr (kPk) fetch_frag<NP, KS>(w_nbr2, a.in, ld, nbq[1], ok && nbq[1] >= 0, lane, t);
+      if constexpr (kTrIn) {
+        fetch_traces(e, ok, nbq, __ldg(geo.info + e));
+      } else {
+        fetch_frag<NP, KS>(w_nbr, a.in, ld, nbq[0], ok && nbq[0] >= 0, lane, t);
+        if constexpr (kPk) fetch_frag<NP, KS>(w_nbr2, a.in, ld, nbq[1], ok && nbq[1] >= 0, lane, t);
+      }
     }
     cp_async_commit();
   }
@@ -381,7 +414,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
     const int e_next = elem_of(tile + nwarps, nvalid);
     // side data of this tile and the next tile's neighbour columns, issued early so
     // they land during the volume integral
-    int nbn[3] = {-4, -4, -4}, edq[3] = {0, 0, 0}, inf = 0;
+    int nbn[3] = {-4, -4, -4}, edq[3] = {0, 0, 0}, inf = 0, inf_next = 0;
     if constexpr (MODE != kModeVolume) {
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
@@ -389,6 +422,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
         edq[q] = __ldg(geo.eid + q * ld + e);
       }
       inf = __ldg(geo.info + e);
+      if constexpr (kTrIn) inf_next = __ldg(geo.info + e_next);
     }
     cp_async_wait<0>();  // own coefficients and side-0 neighbours of this tile
     if constexpr (kTma) {
@@ -612,11 +646,21 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
       auto sel3 = [](int q, auto x0, auto x1, auto x2) { return q == 0 ? x0 : (q == 1 ? x1 : x2); };
 #pragma unroll kMmaPackUnroll
       for (int sp = 0; sp < D::NSP; ++sp) {
-        if (sp > 0) cp_async_wait<0>();  // side 2's neighbour column (prefetched during tile 0)
+        if (!kTrIn && sp > 0) cp_async_wait<0>();  // side 2's neighbour column (prefetched during tile 0)
         // own trace of the packed tile
         double Tw[4][2], Tn[4][2];
 #pragma unroll
         for (int m = 0; m < 4; ++m) Tw[m][0] = Tw[m][1] = Tn[m][0] = Tn[m][1] = 0.0;
+        if constexpr (kTrIn) {  // from the staged trace rows (waited for at the tile start)
+#pragma unroll
+          for (int m = 0; m < 4; ++m)
+#pragma unroll
+            for (int ii = 0; ii < 2; ++ii) {
+              const int pt = 8 * sp + 2 * t + ii;
+              Tw[m][ii] = pt < K3 ? w_nbr[(m * K3 + pt) * 8 + g] : 0.0;
+              Tn[m][ii] = pt < K3 ? w_nbr2[(m * K3 + pt) * 8 + g] : 0.0;
+            }
+        } else {
 #pragma unroll
         for (int ks = 0; ks < KSD; ++ks) {
           const double b = smem[D::kPkOwn + (sp * KS + ks) * 32 + lane];
@@ -651,10 +695,16 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
               });
           }
         }
+        }  // !kTrIn
         __syncwarp();
         // buffers consumed: tile 0 frees side 0's buffer (side 2 goes there); the last
         // tile frees everything (the next tile's sides 0, 1 and own coefficients)
-        if (sp + 1 < D::NSP) {
+        if constexpr (kTrIn) {
+          if (sp + 1 == D::NSP) {
+            fetch_traces(e_next, nvalid, nbn, inf_next);
+            if (!kCSmem) own_fetch(tile + nwarps, e_next, nvalid);
+          }
+        } else if (sp + 1 < D::NSP) {
           fetch_frag<NP, KS>(w_nbr, a.in, ld, nbq[2], valid && nbq[2] >= 0, lane, t);
         } else {
           fetch_frag<NP, KS>(w_nbr, a.in, ld, nbn[0], nvalid && nbn[0] >= 0, lane, t);
@@ -1012,6 +1062,48 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
         lam = std_max(lam, __shfl_xor_sync(0xffffffffu, lam, 1));
         lam = std_max(lam, __shfl_xor_sync(0xffffffffu, lam, 2));
         if (valid && t == 0) lam_min = std_min(lam_min, 2.0 * __ldg(geo.inradius + e) / ((2.0 * P + 1.0) * lam));
+      }
+    }
+    if constexpr (MODE == kModeStage && D::kPacked && DGB_TRACE_P(P)) {
+      if (a.tr_out) {
+        // traces of the new stage for the next stage's kVarTrace instance: the new coefficients
+        // go through the own buffer into the A-fragment order, then the surface's packed
+        // own-trace contraction (same tables, same order: the values the next stage would
+        // interpolate itself, for this element and as the neighbour of its neighbours)
+        __syncwarp();
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+#pragma unroll
+          for (int jt = 0; jt < JT; ++jt)
+#pragma unroll
+            for (int ii = 0; ii < 2; ++ii) {
+              const int j = 8 * jt + 2 * t + ii;
+              if (j < NP) w_own[kTma ? (m * NP + j) * 8 + g : (m * KS + (j >> 2)) * 32 + (g << 2) + (j & 3)] = R[m][jt][ii];
+            }
+        __syncwarp();
+#pragma unroll
+        for (int sp = 0; sp < D::NSP; ++sp) {
+          double Tw[4][2];
+#pragma unroll
+          for (int m = 0; m < 4; ++m) Tw[m][0] = Tw[m][1] = 0.0;
+#pragma unroll
+          for (int ks = 0; ks < KSD; ++ks) {
+            const double b = smem[D::kPkOwn + (sp * KS + ks) * 32 + lane];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) dmma(Tw[m], own_a(m, ks), b);
+          }
+          if constexpr (kSplitK)
+            ktail(Tw, smem + D::kPkOwn + (sp * KS + KS - 1) * 32, [&](int m, int jj) { return own_c(m, 4 * (KS - 1) + jj); });
+          if (valid) {
+#pragma unroll
+            for (int m = 0; m < 4; ++m)
+#pragma unroll
+              for (int ii = 0; ii < 2; ++ii) {
+                const int pt = 8 * sp + 2 * t + ii;
+                if (pt < K3) a.tr_out[static_cast<long long>(m * K3 + pt) * ld + e] = Tw[m][ii];
+              }
+          }
+        }
       }
     }
     if constexpr (kCSmem) {  // the own buffer is free only now

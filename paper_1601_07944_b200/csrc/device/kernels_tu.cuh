@@ -32,6 +32,8 @@ constexpr int kG = Lanes<DGB_P>::value;  // lanes per element
 constexpr int kG4PerSm = DGB_G4_PER_SM;  // latency-form stage kernel up to this many elements per SM
 
 constexpr bool kMma = DGB_P >= DGB_MMA_MINP;
+// trace-buffer stage instances (kVarTrace) exist for the packed-surface DMMA degrees
+constexpr bool kTraceOK = kMma && MmaDim<DGB_P>::kPacked && DGB_TRACE_P(DGB_P);
 constexpr int kMinB = kMma ? DGB_MMA_MINB(DGB_P) : MinBlocks<DGB_P>::value;
 constexpr int kThreads = kMma ? DGB_MMA_THREADS(DGB_P) : kBlock;  // threads per block of k_element
 // dynamic shared memory (bytes): tables + per-warp staging buffers
@@ -90,6 +92,21 @@ void with_instance(int mode, int var, F&& f) {
       if (var & kVarBoundary) f(k_element<kModeRhs, FLUX, kVarBoundary>); else f(k_element<kModeRhs, FLUX, 0>);
       break;
     default:
+      if constexpr (kTraceOK) {
+        if (var & kVarTrace) {
+          switch (var & 7) {
+            case 0: f(k_element<kModeStage, FLUX, 8>); break;
+            case 1: f(k_element<kModeStage, FLUX, 9>); break;
+            case 2: f(k_element<kModeStage, FLUX, 10>); break;
+            case 3: f(k_element<kModeStage, FLUX, 11>); break;
+            case 4: f(k_element<kModeStage, FLUX, 12>); break;
+            case 5: f(k_element<kModeStage, FLUX, 13>); break;
+            case 6: f(k_element<kModeStage, FLUX, 14>); break;
+            default: f(k_element<kModeStage, FLUX, 15>); break;
+          }
+          break;
+        }
+      }
       switch (var & 7) {
         case 0: f(k_element<kModeStage, FLUX, 0>); break;
         case 1: f(k_element<kModeStage, FLUX, 1>); break;
@@ -120,7 +137,7 @@ int variant_of(int mode, const Geo& g, const StageArgs& a) {
   constexpr int mask = DGB_VAR_MASK(DGB_P);
   int v = g.has_bnd ? kVarBoundary : 0;
   if (mode == kModeStage) v |= (a.kmode != 0 ? kVarRk4 : 0) | (a.want_lambda ? kVarLambda : 0);
-  return (v & mask) | (7 & ~mask);
+  return (v & mask) | (7 & ~mask) | (kTraceOK && mode == kModeStage && a.tr_in ? kVarTrace : 0);
 }
 
 __global__ void __launch_bounds__(kBlock) k_dt(Geo geo, const double* __restrict__ c, Scalars* sc, int slot,
@@ -170,7 +187,7 @@ cudaError_t Launch<DGB_P>::upload(const Tab<DGB_P>& t, cudaStream_t s) {
       cudaError_t err = cudaSuccess;
       for (int flux = 0; flux < 2; ++flux)
         for (int mode = 0; mode < 4; ++mode)
-          for (int var = 0; var < 8; ++var)
+          for (int var = 0; var < 16; ++var)
             with_instance(flux, mode, var, [&](auto k) {
               const cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
               if (e != cudaSuccess) err = e;
@@ -204,13 +221,18 @@ cudaError_t Launch<DGB_P>::preload() {
   };
   for (int flux = 0; flux < 2; ++flux)
     for (int mode = 0; mode < 4; ++mode)
-      for (int var = 0; var < 8; ++var) with_instance(flux, mode, var, touch);
+      for (int var = 0; var < 16; ++var) with_instance(flux, mode, var, touch);
   for (int var = 0; var < 8; ++var) {
     with_instance4<kFluxLLF>(var, touch);
     with_instance4<kFluxRoe>(var, touch);
   }
   touch(k_dt);
   return err;
+}
+
+template <>
+int Launch<DGB_P>::trace_points() {
+  return kTraceOK ? 3 * Dim<DGB_P>::K : 0;
 }
 
 template <>

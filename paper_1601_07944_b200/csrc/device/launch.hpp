@@ -18,6 +18,7 @@ struct Launch {
                         cudaStream_t s);
   static int resident_blocks(int mode);  // blocks per SM for the element kernel
   static int lanes();                    // G (0 = DMMA tile kernel)
+  static int trace_points();             // 3K when the stage kernel has trace-buffer instances, else 0
   // DMMA fragment-ordered tables: size in doubles (0 when the degree does not use
   // the DMMA kernel); fills `out` when non-null
   static int mma_table(const Tab<P>& t, double* out);

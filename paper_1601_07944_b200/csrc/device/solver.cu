@@ -41,6 +41,9 @@ struct Fail {
   std::string msg;
 };
 
+#ifndef DGB_TRACE_BUF_DEFAULT
+#define DGB_TRACE_BUF_DEFAULT 1  // trace-buffer stage instances (the degrees of DGB_TRACE_P) by default
+#endif
 #define CU(call)                                                                   \
   do {                                                                             \
     cudaError_t e_ = (call);                                                       \
@@ -393,6 +396,8 @@ struct dgb_ctx {
   // coefficient buffers (device order [4][np][ld])
   DevBuf<double> state[2], input, volume, deriv, stage[2], kacc, slots, staging, hist, staging_in, staging_out;
   DevBuf<double> means;  // [ld][4] cell means of the last stage output (two-kernel limiter path)
+  DevBuf<double> trace[4];  // edge traces [4][3K][ld] of the rotating buffers state0/1, stage0/1 (trace mode)
+  int trace_mode = -1;      // 1 on, 0 off, -1 default (env DGB_TRACE_BUF, else on)
   int cur = 0;
   Scalars* d_sc = nullptr;
   Scalars* h_sc = nullptr;  // pinned mirror
@@ -877,6 +882,14 @@ struct RunOut {
   bool halted = false;
 };
 
+int trace_points(int p) {
+  switch (p) {
+    case 3: return dgbk::Launch<3>::trace_points();
+    case 4: return dgbk::Launch<4>::trace_points();
+    default: return 0;
+  }
+}
+
 int buf_id(const dgb_ctx* c, const double* p) {
   if (p == c->state[0].p) return 0;
   if (p == c->state[1].p) return 1;
@@ -978,6 +991,19 @@ RunOut run_steps(dgb_ctx* c, const RunSpec& r) {
   // column (an interior element computed after the halo wait is harmless): the DMMA kernel's
   // TMA boxes start at e0 + 8 k and must be 16-byte aligned.
   const int n_int = X ? (c->n_int & ~1) : c->N;
+  // trace mode (p = 4, whole mesh, no limiter): each stage writes the edge traces of its
+  // output, the next stage reads its own and its neighbours' traces instead of interpolating
+  // them (results bit-identical)
+  const int k3 = trace_points(c->p);
+  const bool use_tr = c->trace_mode != 0 && k3 > 0 && !X && !r.limiting && !fused;
+  if (use_tr)
+    for (int b = 0; b < 4; ++b)
+      if (c->trace[b].n < static_cast<size_t>(4) * k3 * c->ld) c->trace[b].alloc(static_cast<size_t>(4) * k3 * c->ld);
+  auto trace_of = [&](const double* p) -> double* {
+    const int b = buf_id(c, p);
+    if (b < 0) throw Fail{DGB_ERR_ARG, "trace of a buffer outside the rotation"};
+    return c->trace[b].p;
+  };
 
   const int cur0 = c->cur;
   reset_scalars(c, c->t);
@@ -1036,6 +1062,10 @@ RunOut run_steps(dgb_ctx* c, const RunSpec& r) {
         a.seq_next = static_cast<unsigned long long>(s + 1) * 8;
         a.sc = c->d_sc;
         a.hist = d_hist && s <= r.hist_cap ? d_hist : nullptr;
+        if (use_tr) {  // the run's first stage interpolates; its last writes no traces
+          a.tr_in = (s == 0 && k == 0) ? nullptr : trace_of(a.in);
+          a.tr_out = (s + 1 == r.max_steps && last) ? nullptr : trace_of(a.out);
+        }
         // step start: merge the previous step's scalars (dt bound, residual, error) from every rank
         if (X && k == 0) xch_wait(c, ALL, c->pub_epoch, true, par, par ^ 1);
         const unsigned long long prev = c->epoch;
@@ -1370,6 +1400,10 @@ int dgb_part_create(const dgb_mesh_view* m, const dgb_tables_view* t, const dgb_
       const char* env = std::getenv("DGB_FUSED_LIMIT");
       c->fuse_limit = env ? (env[0] == '0' ? 0 : (env[0] == '1' ? 1 : -1)) : -1;
     }
+    {
+      const char* env = std::getenv("DGB_TRACE_BUF");
+      c->trace_mode = env ? (env[0] == '0' ? 0 : 1) : DGB_TRACE_BUF_DEFAULT;
+    }
     c->d_tau.upload(tau.data(), tau.size(), c->stream);
     c->d_inv_det.upload(inv_det.data(), ld, c->stream);
     c->d_inradius.upload(inr.data(), ld, c->stream);
@@ -1582,6 +1616,12 @@ int dgb_set_flux(dgb_ctx* c, int flux) {
 int dgb_set_fused_limiter(dgb_ctx* c, int enable) {
   if (!c || enable < -1 || enable > 1) return DGB_ERR_ARG;
   c->fuse_limit = enable;
+  return DGB_OK;
+}
+
+int dgb_set_trace_buffers(dgb_ctx* c, int enable) {
+  if (!c || enable < 0 || enable > 1) return DGB_ERR_ARG;
+  c->trace_mode = enable;
   return DGB_OK;
 }
 

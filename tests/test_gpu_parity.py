@@ -640,3 +640,37 @@ def test_time_dependent_dirichlet_at_every_stage_time(scheme):
     assert rel_per_eq(ss.coeffs, sr.coeffs) > 1e-6  # the test sees the stage times
     for c_ in (ctx, ref, stale):
         c_.close()
+
+
+@pytest.mark.parametrize("p", [3, 4])
+@pytest.mark.parametrize("scheme,flux", [(103, "llf"), (4, "llf"), (2, "roe"), (102, "llf")])
+@pytest.mark.parametrize("mesh_kind", ["box", "vortex"])
+def test_trace_buffers_bitwise_equal_to_interpolated_traces(p, scheme, flux, mesh_kind):
+    """Trace-buffer stages (each stage writes the edge traces of its output, the next reads its own
+    and its neighbours' traces, dgb_set_trace_buffers) give the same bits as interpolating every
+    trace from the coefficient columns: fixed steps over several device batches, run_to_time with
+    its stop rule, RK4 / SSP / midpoint, both fluxes, the boundary-code instance (p = 3 has no
+    trace instances: the setter must be harmless there)."""
+    if mesh_kind == "vortex":
+        mesh = dg2d.generate_mesh(L.MESH_VORTEX, 3, 0, 1.0, 1.384)
+        bc, u0 = dg2d.vortex_boundary(), dg2d.vortex_exact
+    else:
+        mesh = dg2d.generate_mesh(L.MESH_PERIODIC_BOX, 41, 38, 10.0, 10.0)
+        bc, u0 = None, dg2d.IsentropicVortex()
+    tb = dg2d.build_tables(p)
+    c0 = dg2d.project_initial(u0, mesh, tb)
+    opts = dg2d.SolverOptions(scheme=scheme, cfl=0.3, flux=flux)
+    out = []
+    for tr in (0, 1):
+        ctx = dg2d.SolverContext(mesh, tb, bc=bc, options=opts)
+        assert L.lib.dgb_set_trace_buffers(ctx.handle, tr) == 0
+        st = dg2d.SolverState(c0.copy())
+        r1 = dg2d.run_fixed_steps(ctx, st, 9)
+        r2 = dg2d.run_fixed_steps(ctx, st, 4)  # a second call: its first stage interpolates again
+        t_end = st.t + 0.37 * (st.t / st.step_count) * 5
+        dg2d.run_to_time(ctx, st, t_end, 1000)
+        out.append((st.coeffs.copy(), st.t, st.step_count, r1, r2))
+        ctx.close()
+    assert np.array_equal(out[0][0], out[1][0])
+    assert out[0][1:] == out[1][1:]
+    assert L.lib.dgb_set_trace_buffers(None, 1) == L.ERR_ARG
