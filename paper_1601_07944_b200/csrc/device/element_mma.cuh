@@ -57,9 +57,9 @@ constexpr int kMmaPackUnroll = DGB_MMA_PACK_UNROLL;
 #endif
 #ifndef DGB_TRACE_P
 // degrees with trace-buffer stage instances (kVarTrace) and the epilogue's trace write; measured
-// per stage (interleaved): p=4 0.930 vs 0.980 ms; p=3 0.670 vs 0.666 (its tensor work is not what
-// bounds it), and the epilogue branch alone costs the p=3 instances 1 %
-#define DGB_TRACE_P(P) ((P) == 4)
+// per stage (interleaved): p=4 0.930 vs 0.980 ms, p=5 1.468 vs 1.549; p=3 0.670 vs 0.666 (its
+// tensor work is not what bounds it), and the epilogue branch alone costs the p=3 instances 1 %
+#define DGB_TRACE_P(P) ((P) == 4 || (P) == 5)
 #endif
 #ifndef DGB_MMA_SPLIT_J
 #define DGB_MMA_SPLIT_J 1
@@ -276,6 +276,9 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
   // traces in w_nbr, the neighbours' reversed traces in w_nbr2, both [4][3K][8 elements])
   // instead of interpolating them; the epilogue writes the traces of the new stage (a.tr_out)
   constexpr bool kTrIn = kPk && MODE == kModeStage && DGB_TRACE_P(P) && (VAR & kVarTrace) != 0;
+  // the same for the per-side surface (p = 5): side q's own rows and its neighbour's reversed rows
+  // staged into w_nbr one side ahead, [own | neighbour][4][K][8 elements]
+  constexpr bool kTrInS = !kPk && MODE == kModeStage && DGB_TRACE_P(P) && (VAR & kVarTrace) != 0;
   constexpr int K3 = 3 * K;
   // the last output tile of the projections when it holds at most two live modes (p = 3: modes
   // 8, 9 in 8 columns): the volume and packed-surface projections accumulate those modes with
@@ -371,6 +374,20 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
   auto nbr_of = [&](int e, int q) { return __ldg(geo.nbr + q * ld + e); };
   // kTrIn: traces of element column col (lane group g) and of its neighbours nb[] (side labels in
   // inf_) into the neighbour buffers; lane t copies rows t, t + 4, ... of the 4 * 3K rows
+  auto fetch_side_traces = [&](int col, bool ok, int q, int nbc, int inf_) {
+    if constexpr (kTrInS) {
+      const int sl = (inf_ >> (2 * q)) & 3;
+      const bool okn = ok && nbc >= 0 && sl != 0;
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        const int r = 4 * i + t;  // row (m, ko) of this side, m = r / K
+        const int m = r / K, ko = r - m * K;
+        cp_async8(w_nbr + r * 8 + g, ok ? a.tr_in + static_cast<long long>(m * K3 + q * K + ko) * ld + col : a.tr_in, ok);
+        const int rn = m * K3 + (sl - 1) * K + (K - 1 - ko);
+        cp_async8(w_nbr + (4 * K + r) * 8 + g, okn ? a.tr_in + static_cast<long long>(rn) * ld + nbc : a.tr_in, okn);
+      }
+    }
+  };
   auto fetch_traces = [&](int col, bool ok, const int (&nb)[3], int inf_) {
     if constexpr (kTrIn) {
 #pragma unroll
@@ -399,6 +416,8 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
       for (int q = 0; q < 3; ++q) nbq[q] = nbr_of(e, q);
       if constexpr (kTrIn) {
         fetch_traces(e, ok, nbq, __ldg(geo.info + e));
+      } else if constexpr (kTrInS) {
+        fetch_side_traces(e, ok, 0, nbq[0], __ldg(geo.info + e));
       } else {
         fetch_frag<NP, KS>(w_nbr, a.in, ld, nbq[0], ok && nbq[0] >= 0, lane, t);
         if constexpr (kPk) fetch_frag<NP, KS>(w_nbr2, a.in, ld, nbq[1], ok && nbq[1] >= 0, lane, t);
@@ -422,7 +441,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
         edq[q] = __ldg(geo.eid + q * ld + e);
       }
       inf = __ldg(geo.info + e);
-      if constexpr (kTrIn) inf_next = __ldg(geo.info + e_next);
+      if constexpr (kTrIn || kTrInS) inf_next = __ldg(geo.info + e_next);
     }
     cp_async_wait<0>();  // own coefficients and side-0 neighbours of this tile
     if constexpr (kTma) {
@@ -828,7 +847,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
         const bool bnd = nb < 0;
         const int snb = bnd ? 0 : ((inf >> (2 * q)) & 3);
         const double nx = enx[q], ny = eny[q], h = eh[q];
-        if (q > 0) cp_async_wait<0>();  // this side's neighbour column (prefetched during the previous side)
+        if (q > 0) cp_async_wait<0>();  // this side's neighbour column / traces (prefetched during the previous side)
         if constexpr (MODE == kModeSurface) {
 #pragma unroll
           for (int m = 0; m < 4; ++m)
@@ -836,9 +855,19 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
             for (int jt = 0; jt < JT; ++jt) R[m][jt][0] = R[m][jt][1] = 0.0;
         }
         // own trace of side q
-        double Tw[4][2];
+        double Tw[4][2], Tn[4][2];
 #pragma unroll
-        for (int m = 0; m < 4; ++m) Tw[m][0] = Tw[m][1] = 0.0;
+        for (int m = 0; m < 4; ++m) Tw[m][0] = Tw[m][1] = Tn[m][0] = Tn[m][1] = 0.0;
+        if constexpr (kTrInS) {
+#pragma unroll
+          for (int m = 0; m < 4; ++m)
+#pragma unroll
+            for (int ii = 0; ii < 2; ++ii) {
+              const int ko = 2 * t + ii;
+              Tw[m][ii] = ko < K ? w_nbr[(m * K + ko) * 8 + g] : 0.0;
+              Tn[m][ii] = ko < K ? w_nbr[(4 * K + m * K + ko) * 8 + g] : 0.0;
+            }
+        } else {
 #pragma unroll
         for (int ks = 0; ks < KSD; ++ks) {
           const double b = smem[D::kPhe + (q * KS + ks) * 32 + lane];
@@ -849,9 +878,6 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
           ktail(Tw, smem + D::kPhe + (q * KS + KS - 1) * 32, [&](int m, int jj) { return own_c(m, 4 * (KS - 1) + jj); });
         // neighbour trace (reversed points) — one pass per neighbour side label
         // present in the warp (class renumbering makes that one pass almost always)
-        double Tn[4][2];
-#pragma unroll
-        for (int m = 0; m < 4; ++m) Tn[m][0] = Tn[m][1] = 0.0;
         unsigned todo = __reduce_or_sync(0xffffffffu, snb ? (1u << snb) : 0u);
         while (todo) {
           const int s = __ffs(todo) - 1;
@@ -871,10 +897,18 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
               return mine ? w_nbr[(m * KS + KS - 1) * 32 + 4 * g + jj] : 0.0;
             });
         }
+        }  // !kTrInS
         __syncwarp();
         // the neighbour buffer is consumed: prefetch the next side (after side 2: the
         // next tile's side 0 and, the own buffer being free too, its own coefficients)
-        if (q < 2) {
+        if constexpr (kTrInS) {
+          if (q < 2) {
+            fetch_side_traces(e, valid, q + 1, q == 0 ? nbq[1] : nbq[2], inf);
+          } else {
+            fetch_side_traces(e_next, nvalid, 0, nbn[0], inf_next);
+            if (!kCSmem) own_fetch(tile + nwarps, e_next, nvalid);
+          }
+        } else if (q < 2) {
           fetch_frag<NP, KS>(w_nbr, a.in, ld, nbq[q + 1], valid && nbq[q + 1] >= 0, lane, t);
         } else {
           fetch_frag<NP, KS>(w_nbr, a.in, ld, nbn[0], nvalid && nbn[0] >= 0, lane, t);
@@ -1064,7 +1098,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
         if (valid && t == 0) lam_min = std_min(lam_min, 2.0 * __ldg(geo.inradius + e) / ((2.0 * P + 1.0) * lam));
       }
     }
-    if constexpr (MODE == kModeStage && D::kPacked && DGB_TRACE_P(P)) {
+    if constexpr (MODE == kModeStage && DGB_TRACE_P(P)) {
       if (a.tr_out) {
         // traces of the new stage for the next stage's kVarTrace instance: the new coefficients
         // go through the own buffer into the A-fragment order, then the surface's packed
@@ -1081,6 +1115,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
               if (j < NP) w_own[kTma ? (m * NP + j) * 8 + g : (m * KS + (j >> 2)) * 32 + (g << 2) + (j & 3)] = R[m][jt][ii];
             }
         __syncwarp();
+        if constexpr (D::kPacked) {
 #pragma unroll
         for (int sp = 0; sp < D::NSP; ++sp) {
           double Tw[4][2];
@@ -1103,6 +1138,31 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
                 if (pt < K3) a.tr_out[static_cast<long long>(m * K3 + pt) * ld + e] = Tw[m][ii];
               }
           }
+        }
+        } else {  // per-side surface: side q's own-trace contraction (kPhe)
+#pragma unroll kMmaSideUnroll
+        for (int q = 0; q < 3; ++q) {
+          double Tw[4][2];
+#pragma unroll
+          for (int m = 0; m < 4; ++m) Tw[m][0] = Tw[m][1] = 0.0;
+#pragma unroll
+          for (int ks = 0; ks < KSD; ++ks) {
+            const double b = smem[D::kPhe + (q * KS + ks) * 32 + lane];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) dmma(Tw[m], own_a(m, ks), b);
+          }
+          if constexpr (kSplitK)
+            ktail(Tw, smem + D::kPhe + (q * KS + KS - 1) * 32, [&](int m, int jj) { return own_c(m, 4 * (KS - 1) + jj); });
+          if (valid) {
+#pragma unroll
+            for (int m = 0; m < 4; ++m)
+#pragma unroll
+              for (int ii = 0; ii < 2; ++ii) {
+                const int ko = 2 * t + ii;
+                if (ko < K) a.tr_out[static_cast<long long>(m * K3 + q * K + ko) * ld + e] = Tw[m][ii];
+              }
+          }
+        }
         }
       }
     }

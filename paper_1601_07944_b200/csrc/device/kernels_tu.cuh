@@ -33,7 +33,7 @@ constexpr int kG4PerSm = DGB_G4_PER_SM;  // latency-form stage kernel up to this
 
 constexpr bool kMma = DGB_P >= DGB_MMA_MINP;
 // trace-buffer stage instances (kVarTrace) exist for the packed-surface DMMA degrees
-constexpr bool kTraceOK = kMma && MmaDim<DGB_P>::kPacked && DGB_TRACE_P(DGB_P);
+constexpr bool kTraceOK = kMma && DGB_TRACE_P(DGB_P);
 constexpr int kMinB = kMma ? DGB_MMA_MINB(DGB_P) : MinBlocks<DGB_P>::value;
 constexpr int kThreads = kMma ? DGB_MMA_THREADS(DGB_P) : kBlock;  // threads per block of k_element
 // dynamic shared memory (bytes): tables + per-warp staging buffers

@@ -886,6 +886,7 @@ int trace_points(int p) {
   switch (p) {
     case 3: return dgbk::Launch<3>::trace_points();
     case 4: return dgbk::Launch<4>::trace_points();
+    case 5: return dgbk::Launch<5>::trace_points();
     default: return 0;
   }
 }

@@ -642,7 +642,7 @@ def test_time_dependent_dirichlet_at_every_stage_time(scheme):
         c_.close()
 
 
-@pytest.mark.parametrize("p", [3, 4])
+@pytest.mark.parametrize("p", [3, 4, 5])
 @pytest.mark.parametrize("scheme,flux", [(103, "llf"), (4, "llf"), (2, "roe"), (102, "llf")])
 @pytest.mark.parametrize("mesh_kind", ["box", "vortex"])
 def test_trace_buffers_bitwise_equal_to_interpolated_traces(p, scheme, flux, mesh_kind):
