@@ -396,7 +396,7 @@ struct dgb_ctx {
   // coefficient buffers (device order [4][np][ld])
   DevBuf<double> state[2], input, volume, deriv, stage[2], kacc, slots, staging, hist, staging_in, staging_out;
   DevBuf<double> means;  // [ld][4] cell means of the last stage output (two-kernel limiter path)
-  DevBuf<double> trace[4];  // edge traces [4][3K][ld] of the rotating buffers state0/1, stage0/1 (trace mode)
+  int k3 = 0;               // 3K when the degree has trace-buffer stage instances, else 0
   int trace_mode = -1;      // 1 on, 0 off, -1 default (env DGB_TRACE_BUF, else on)
   int cur = 0;
   Scalars* d_sc = nullptr;
@@ -444,6 +444,10 @@ struct dgb_ctx {
   dgbk::LimTab lim{};
 
   size_t coeff_count() const { return static_cast<size_t>(4) * np * ld; }
+  // rotating buffers (state0/1, stage0/1): the coefficients, then at the degrees with
+  // trace-buffer stage instances the edge traces [4][3K][ld] of those coefficients (trace mode,
+  // DESIGN.md section 3.1); one allocation, so a peer's mapping of a buffer covers both
+  size_t rot_count() const { return coeff_count() + static_cast<size_t>(4) * k3 * ld; }
 };
 
 namespace {
@@ -904,11 +908,12 @@ bool exchanging(const dgb_ctx* c) { return c->partitioned && c->world > 1; }
 unsigned all_peers(const dgb_ctx* c) { return ((1u << c->world) - 1u) & ~(1u << c->rank); }
 
 // Push the send elements' columns of `p` (one of the rotating buffers) to the peers.
-void xch_push(dgb_ctx* c, const double* p) {
+void xch_push(dgb_ctx* c, const double* p, bool traces) {
   if (c->n_push == 0) return;
   const int buf = buf_id(c, p);
   if (buf < 0) throw Fail{DGB_ERR_ARG, "halo push from a buffer the peers do not map"};
-  const int rows = 4 * c->np;
+  // the coefficient rows, then (trace mode) the trace rows that follow them in the same buffer
+  const int rows = 4 * c->np + (traces ? 4 * c->k3 : 0);
   const long long total = static_cast<long long>(c->n_push) * rows;
   const int grid = static_cast<int>(std::min<long long>((total + 255) / 256, 148LL * 8));
   k_push<<<grid, 256, 0, c->stream>>>(c->d_peers, buf, p, c->ld, c->d_push.p, c->n_push, rows);
@@ -947,10 +952,10 @@ RunOut run_steps(dgb_ctx* c, const RunSpec& r) {
   check_bc(c);
   ensure_tables(c);
   const int S = static_cast<int>(st.size());
-  if (!c->stage[0].p) c->stage[0].alloc_zero(c->coeff_count(), c->stream);
-  if (!c->stage[1].p) c->stage[1].alloc_zero(c->coeff_count(), c->stream);
+  if (!c->stage[0].p) c->stage[0].alloc_zero(c->rot_count(), c->stream);
+  if (!c->stage[1].p) c->stage[1].alloc_zero(c->rot_count(), c->stream);
   if (r.scheme == DGB_RK4_CLASSIC && !c->kacc.p) c->kacc.alloc_zero(c->coeff_count(), c->stream);
-  if (!c->state[1 - c->cur].p) c->state[1 - c->cur].alloc_zero(c->coeff_count(), c->stream);
+  if (!c->state[1 - c->cur].p) c->state[1 - c->cur].alloc_zero(c->rot_count(), c->stream);
   double* d_hist = nullptr;
   if (r.hist && r.hist_cap > 0) {
     if (c->hist.n < static_cast<size_t>(r.hist_cap)) c->hist.alloc(r.hist_cap);
@@ -992,18 +997,14 @@ RunOut run_steps(dgb_ctx* c, const RunSpec& r) {
   // column (an interior element computed after the halo wait is harmless): the DMMA kernel's
   // TMA boxes start at e0 + 8 k and must be 16-byte aligned.
   const int n_int = X ? (c->n_int & ~1) : c->N;
-  // trace mode (p = 4, whole mesh, no limiter): each stage writes the edge traces of its
-  // output, the next stage reads its own and its neighbours' traces instead of interpolating
-  // them (results bit-identical)
-  const int k3 = trace_points(c->p);
-  const bool use_tr = c->trace_mode != 0 && k3 > 0 && !X && !r.limiting && !fused;
-  if (use_tr)
-    for (int b = 0; b < 4; ++b)
-      if (c->trace[b].n < static_cast<size_t>(4) * k3 * c->ld) c->trace[b].alloc(static_cast<size_t>(4) * k3 * c->ld);
+  // trace mode (p = 4, 5, no limiter): each stage writes the edge traces of its output, the
+  // next stage reads its own and its neighbours' traces instead of interpolating them (results
+  // bit-identical).  A partition pushes the send elements' trace rows
+  // with their coefficient rows, so the halo columns carry traces too.
+  const bool use_tr = c->trace_mode != 0 && c->k3 > 0 && !r.limiting && !fused;
   auto trace_of = [&](const double* p) -> double* {
-    const int b = buf_id(c, p);
-    if (b < 0) throw Fail{DGB_ERR_ARG, "trace of a buffer outside the rotation"};
-    return c->trace[b].p;
+    if (buf_id(c, p) < 0) throw Fail{DGB_ERR_ARG, "trace of a buffer outside the rotation"};
+    return const_cast<double*>(p) + c->coeff_count();
   };
 
   const int cur0 = c->cur;
@@ -1104,7 +1105,7 @@ RunOut run_steps(dgb_ctx* c, const RunSpec& r) {
             a.e1 = c->N;
             CU(launch_element(c, dgbk::kModeStage, a));
             ++c->launches;
-            xch_push(c, a.out);
+            xch_push(c, a.out, a.tr_out != nullptr);
           }
         }
         if (X) {
@@ -1136,7 +1137,7 @@ RunOut run_steps(dgb_ctx* c, const RunSpec& r) {
             la.e1 = c->N;
             CU(dgbk::launch_limit(0, c->geo, la, c->stream));
             ++c->launches;
-            xch_push(c, la.c);
+            xch_push(c, la.c, false);
             if (last)
               xch_signal(c, ALL, true, par ^ 1, par);
             else
@@ -1535,12 +1536,13 @@ int dgb_part_create(const dgb_mesh_view* m, const dgb_tables_view* t, const dgb_
     CU(cudaMallocHost(&c->h_sc, sizeof(Scalars)));
     CU(cudaMalloc(&c->d_red, sizeof(unsigned long long)));
     CU(cudaMallocHost(&c->h_red, sizeof(unsigned long long)));
-    c->state[0].alloc_zero(c->coeff_count(), c->stream);
+    c->k3 = trace_points(c->p);
+    c->state[0].alloc_zero(c->rot_count(), c->stream);
     if (c->partitioned) {
       // the peers address our rotating buffers directly, so they exist from the start
-      c->state[1].alloc_zero(c->coeff_count(), c->stream);
-      c->stage[0].alloc_zero(c->coeff_count(), c->stream);
-      c->stage[1].alloc_zero(c->coeff_count(), c->stream);
+      c->state[1].alloc_zero(c->rot_count(), c->stream);
+      c->stage[0].alloc_zero(c->rot_count(), c->stream);
+      c->stage[1].alloc_zero(c->rot_count(), c->stream);
       const size_t nx = dgbk::kMaxRanks + 2 * dgbk::kMaxRanks * 4;
       CU(cudaMalloc(&c->d_xch, nx * sizeof(unsigned long long)));
       CU(cudaMemsetAsync(c->d_xch, 0, nx * sizeof(unsigned long long), c->stream));

@@ -188,7 +188,7 @@ def test_in_process_partitions_bit_identical_to_whole_mesh(name, p, scheme, worl
 
 @pytest.mark.gpu
 @pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs in this process")
-@pytest.mark.parametrize("p,limiting", [(1, True), (3, False)])
+@pytest.mark.parametrize("p,limiting", [(1, True), (3, False), (5, False)])
 def test_partitions_on_different_devices_bit_identical(p, limiting):
     """connect_local across devices: dgb_part_attach_peer enables P2P access between the
     devices, and the halo stores cross NVLink; bit-identical to the whole-mesh solve."""
@@ -250,11 +250,11 @@ def test_partition_run_to_time_halts_together():
     assert np.array_equal(out, ref.coeffs)
 
 
-def _ipc_worker(rank, world, port, q):
+def _ipc_worker(rank, world, port, q, p=3):
     try:
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         dist.init_process_group("gloo", rank=rank, world_size=world)
-        mesh, tb, bc, c0 = _problem("periodic", 3)
+        mesh, tb, bc, c0 = _problem("periodic", p)
         opts = dg2d.SolverOptions(scheme=L.SSP_RK3, cfl=0.3)
         part = D.PartContext(mesh, tb, rank, world, options=opts, device=0)
         part.set_timeout(60.0)
@@ -282,14 +282,15 @@ def _ipc_worker(rank, world, port, q):
 
 
 @pytest.mark.gpu
-def test_two_processes_ipc_halo_exchange_bit_identical():
-    mesh, tb, bc, c0 = _problem("periodic", 3)
+@pytest.mark.parametrize("p", [3, 5])  # p = 5: the trace rows travel with the coefficient rows
+def test_two_processes_ipc_halo_exchange_bit_identical(p):
+    mesh, tb, bc, c0 = _problem("periodic", p)
     opts = dg2d.SolverOptions(scheme=L.SSP_RK3, cfl=0.3)
     ref, res_ref = _whole(mesh, tb, bc, c0, opts, 6)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q, p)) for r in range(2)]
     for pr in procs:
         pr.start()
     out = sorted([q.get(timeout=300) for _ in procs], key=lambda x: x[0])
