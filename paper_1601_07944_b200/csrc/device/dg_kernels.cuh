@@ -131,7 +131,7 @@ struct StageArgs {
   double* __restrict__ out;       // output (volume / slots / deriv / next stage)
   double* __restrict__ kacc;      // RK4 derivative accumulator
   double* __restrict__ means;     // p <= 2 with a limiter kernel next: the new cell means, [ld][4] (null: none)
-  // edge traces, [4][3K][ld] (packed point pt = side * K + point, the element's own orientation):
+  // edge traces, element-major [ld][3 sides][4 variables][K points] (the element's own orientation):
   // tr_in those of `in` (kVarTrace instances), tr_out those of `out` (written when non-null)
   const double* __restrict__ tr_in;
   double* __restrict__ tr_out;

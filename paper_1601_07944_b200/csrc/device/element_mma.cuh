@@ -57,8 +57,9 @@ constexpr int kMmaPackUnroll = DGB_MMA_PACK_UNROLL;
 #endif
 #ifndef DGB_TRACE_P
 // degrees with trace-buffer stage instances (kVarTrace) and the epilogue's trace write; measured
-// per stage (interleaved): p=4 0.930 vs 0.980 ms, p=5 1.468 vs 1.549; p=3 0.670 vs 0.666 (its
-// tensor work is not what bounds it), and the epilogue branch alone costs the p=3 instances 1 %
+// per stage (interleaved): p=4 0.848 vs 0.980 ms, p=5 1.387 vs 1.549; p=3 0.670 vs 0.666 with the
+// first (row-major) layout (its tensor work is not what bounds it), and the epilogue branch
+// alone costs the p=3 instances 1 %
 #define DGB_TRACE_P(P) ((P) == 4 || (P) == 5)
 #endif
 #ifndef DGB_MMA_SPLIT_J
@@ -197,6 +198,12 @@ __device__ __forceinline__ int half_operands(const double (&v)[4][2], double (&a
   return hi ? 1 : 0;
 }
 
+// 16-byte cp.async (L2 only), zero-filled when !pred
+__device__ __forceinline__ void cp_async16(double* dst, const double* src, bool pred) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(src), "r"(pred ? 16 : 0) : "memory");
+}
+
 // ---- TMA load of a tile's own coefficients (one cp.async.bulk.tensor per tile, lane 0)
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
 __device__ __forceinline__ void mbar_init(unsigned long long* bar) {
@@ -280,6 +287,12 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
   // staged into w_nbr one side ahead, [own | neighbour][4][K][8 elements]
   constexpr bool kTrInS = !kPk && MODE == kModeStage && DGB_TRACE_P(P) && (VAR & kVarTrace) != 0;
   constexpr int K3 = 3 * K;
+  // trace layout (element-major, so a neighbour's side is one contiguous 4K-double block):
+  // tr[e][side][var][point], kTS doubles per element; in shared memory kTSP (kTS padded so the 8
+  // elements of a tile start in different banks), kSSP per element for one staged side
+  constexpr int kTS = 4 * K3;
+  constexpr int kTSP = kTS + 2;
+  constexpr int kSSP = 8 * K + 2;
   // the last output tile of the projections when it holds at most two live modes (p = 3: modes
   // 8, 9 in 8 columns): the volume and packed-surface projections accumulate those modes with
   // DFMAs into X (each lane its own points' share), reduced over the element's four lanes
@@ -376,30 +389,42 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
   // inf_) into the neighbour buffers; lane t copies rows t, t + 4, ... of the 4 * 3K rows
   auto fetch_side_traces = [&](int col, bool ok, int q, int nbc, int inf_) {
     if constexpr (kTrInS) {
+      // element g's side q block and its neighbour's side block (4K doubles each) into
+      // w_nbr[g kSSP + (own | 4K + neighbour)], 16 bytes per copy, lane t every fourth chunk
       const int sl = (inf_ >> (2 * q)) & 3;
       const bool okn = ok && nbc >= 0 && sl != 0;
+      const double* so = a.tr_in + static_cast<long long>(col) * kTS + q * 4 * K;
+      const double* sn = a.tr_in + static_cast<long long>(okn ? nbc : 0) * kTS + (okn ? sl - 1 : 0) * 4 * K;
 #pragma unroll
-      for (int i = 0; i < K; ++i) {
-        const int r = 4 * i + t;  // row (m, ko) of this side, m = r / K
-        const int m = r / K, ko = r - m * K;
-        cp_async8(w_nbr + r * 8 + g, ok ? a.tr_in + static_cast<long long>(m * K3 + q * K + ko) * ld + col : a.tr_in, ok);
-        const int rn = m * K3 + (sl - 1) * K + (K - 1 - ko);
-        cp_async8(w_nbr + (4 * K + r) * 8 + g, okn ? a.tr_in + static_cast<long long>(rn) * ld + nbc : a.tr_in, okn);
+      for (int i = 0; i < K; ++i) {  // 4K chunks of 16 bytes: K per lane
+        const int c = 4 * i + t;      // chunk < 4K: own (c < 2K) or neighbour
+        const bool own = c < 2 * K;
+        const int cc = own ? c : c - 2 * K;
+        cp_async16(w_nbr + g * kSSP + (own ? 0 : 4 * K) + 2 * cc, (own ? so : sn) + 2 * cc, own ? ok : okn);
       }
     }
   };
   auto fetch_traces = [&](int col, bool ok, const int (&nb)[3], int inf_) {
     if constexpr (kTrIn) {
+      // element g's whole block into w_nbr[g kTSP], its neighbours' side blocks (4K doubles each,
+      // side q's neighbour at q 4K) into w_nbr2[g kTSP]; 16 bytes per copy
+      const double* so = a.tr_in + static_cast<long long>(col) * kTS;
 #pragma unroll
-      for (int i = 0; i < K3; ++i) {
-        const int r = 4 * i + t;
-        const int m = r / K3, pt = r - m * K3, q = pt / K, ko = pt - q * K;
-        cp_async8(w_nbr + r * 8 + g, ok ? a.tr_in + static_cast<long long>(r) * ld + col : a.tr_in, ok);
-        const int nbc = q == 0 ? nb[0] : (q == 1 ? nb[1] : nb[2]);
-        const int sl = (inf_ >> (2 * q)) & 3;  // the neighbour's side label (1..3), 0 = boundary
-        const bool okn = ok && nbc >= 0 && sl != 0;
-        const int rn = m * K3 + (sl - 1) * K + (K - 1 - ko);
-        cp_async8(w_nbr2 + r * 8 + g, okn ? a.tr_in + static_cast<long long>(rn) * ld + nbc : a.tr_in, okn);
+      for (int i = 0; i < (kTS / 2 + 3) / 4; ++i) {
+        const int c = 4 * i + t;
+        if (c < kTS / 2) cp_async16(w_nbr + g * kTSP + 2 * c, so + 2 * c, ok);
+      }
+#pragma unroll
+      for (int i = 0; i < (kTS / 2 + 3) / 4; ++i) {
+        const int c = 4 * i + t;
+        if (c < kTS / 2) {
+          const int q = c / (2 * K), cc = c - q * 2 * K;
+          const int nbc = q == 0 ? nb[0] : (q == 1 ? nb[1] : nb[2]);
+          const int sl = (inf_ >> (2 * q)) & 3;
+          const bool okn = ok && nbc >= 0 && sl != 0;
+          const double* sn = a.tr_in + static_cast<long long>(okn ? nbc : 0) * kTS + (okn ? sl - 1 : 0) * 4 * K;
+          cp_async16(w_nbr2 + g * kTSP + q * 4 * K + 2 * cc, sn + 2 * cc, okn);
+        }
       }
     }
   };
@@ -676,8 +701,9 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
 #pragma unroll
             for (int ii = 0; ii < 2; ++ii) {
               const int pt = 8 * sp + 2 * t + ii;
-              Tw[m][ii] = pt < K3 ? w_nbr[(m * K3 + pt) * 8 + g] : 0.0;
-              Tn[m][ii] = pt < K3 ? w_nbr2[(m * K3 + pt) * 8 + g] : 0.0;
+              const int q = pt < K3 ? pt / K : 0, ko = pt - q * K;
+              Tw[m][ii] = pt < K3 ? w_nbr[g * kTSP + (q * 4 + m) * K + ko] : 0.0;
+              Tn[m][ii] = pt < K3 ? w_nbr2[g * kTSP + (q * 4 + m) * K + (K - 1 - ko)] : 0.0;
             }
         } else {
 #pragma unroll
@@ -864,8 +890,8 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
 #pragma unroll
             for (int ii = 0; ii < 2; ++ii) {
               const int ko = 2 * t + ii;
-              Tw[m][ii] = ko < K ? w_nbr[(m * K + ko) * 8 + g] : 0.0;
-              Tn[m][ii] = ko < K ? w_nbr[(4 * K + m * K + ko) * 8 + g] : 0.0;
+              Tw[m][ii] = ko < K ? w_nbr[g * kSSP + m * K + ko] : 0.0;
+              Tn[m][ii] = ko < K ? w_nbr[g * kSSP + 4 * K + m * K + (K - 1 - ko)] : 0.0;
             }
         } else {
 #pragma unroll
@@ -1135,7 +1161,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
 #pragma unroll
               for (int ii = 0; ii < 2; ++ii) {
                 const int pt = 8 * sp + 2 * t + ii;
-                if (pt < K3) a.tr_out[static_cast<long long>(m * K3 + pt) * ld + e] = Tw[m][ii];
+                if (pt < K3) a.tr_out[static_cast<long long>(e) * kTS + ((pt / K) * 4 + m) * K + pt % K] = Tw[m][ii];
               }
           }
         }
@@ -1159,7 +1185,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
 #pragma unroll
               for (int ii = 0; ii < 2; ++ii) {
                 const int ko = 2 * t + ii;
-                if (ko < K) a.tr_out[static_cast<long long>(m * K3 + q * K + ko) * ld + e] = Tw[m][ii];
+                if (ko < K) a.tr_out[static_cast<long long>(e) * kTS + (q * 4 + m) * K + ko] = Tw[m][ii];
               }
           }
         }

@@ -125,13 +125,23 @@ __device__ __forceinline__ unsigned long long global_ns() {
 // by (peer, peer column).  Kept out of the stage and limiter kernels: the push code there cost
 // the whole-mesh instances registers and issue slots.
 __global__ void k_push(const dgbk::PeerTab* __restrict__ pt, int buf, const double* __restrict__ src, long long ld,
-                       const int4* __restrict__ ent, int n, int rows) {
-  const long long total = static_cast<long long>(n) * rows;
+                       const int4* __restrict__ ent, int n, int rows, int tblock) {
+  // rows [0, rows): coefficient rows (column e of row r at r ld + e); then (trace mode) the
+  // element-major trace blocks after them (tblock doubles per element at rows ld + e tblock)
+  const long long total = static_cast<long long>(n) * (rows + tblock);
   for (long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; k < total;
        k += static_cast<long long>(gridDim.x) * blockDim.x) {
     const int r = static_cast<int>(k / n), i = static_cast<int>(k - static_cast<long long>(r) * n);
     const int4 e = __ldg(ent + i);
-    pt->buf[e.y][buf][static_cast<long long>(r) * pt->ld[e.y] + e.z] = src[static_cast<long long>(r) * ld + e.x];
+    const long long pld = pt->ld[e.y];
+    double* dst = pt->buf[e.y][buf];
+    if (r < rows) {
+      dst[static_cast<long long>(r) * pld + e.z] = src[static_cast<long long>(r) * ld + e.x];
+    } else {
+      const int o = r - rows;
+      dst[static_cast<long long>(rows) * pld + static_cast<long long>(e.z) * tblock + o] =
+          src[static_cast<long long>(rows) * ld + static_cast<long long>(e.x) * tblock + o];
+    }
   }
   __threadfence_system();  // visible at the peers before the signal kernel's flag
 }
@@ -912,11 +922,11 @@ void xch_push(dgb_ctx* c, const double* p, bool traces) {
   if (c->n_push == 0) return;
   const int buf = buf_id(c, p);
   if (buf < 0) throw Fail{DGB_ERR_ARG, "halo push from a buffer the peers do not map"};
-  // the coefficient rows, then (trace mode) the trace rows that follow them in the same buffer
-  const int rows = 4 * c->np + (traces ? 4 * c->k3 : 0);
-  const long long total = static_cast<long long>(c->n_push) * rows;
+  // the coefficient rows, then (trace mode) the element-major trace blocks that follow them
+  const int rows = 4 * c->np, tblock = traces ? 4 * c->k3 : 0;
+  const long long total = static_cast<long long>(c->n_push) * (rows + tblock);
   const int grid = static_cast<int>(std::min<long long>((total + 255) / 256, 148LL * 8));
-  k_push<<<grid, 256, 0, c->stream>>>(c->d_peers, buf, p, c->ld, c->d_push.p, c->n_push, rows);
+  k_push<<<grid, 256, 0, c->stream>>>(c->d_peers, buf, p, c->ld, c->d_push.p, c->n_push, rows, tblock);
   CU(cudaGetLastError());
   ++c->launches;
 }
