@@ -57,10 +57,9 @@ constexpr int kMmaPackUnroll = DGB_MMA_PACK_UNROLL;
 #endif
 #ifndef DGB_TRACE_P
 // degrees with trace-buffer stage instances (kVarTrace) and the epilogue's trace write; measured
-// per stage (interleaved): p=4 0.848 vs 0.980 ms, p=5 1.387 vs 1.549; p=3 0.670 vs 0.666 with the
-// first (row-major) layout (its tensor work is not what bounds it), and the epilogue branch
-// alone costs the p=3 instances 1 %
-#define DGB_TRACE_P(P) ((P) == 4 || (P) == 5)
+// per stage (interleaved, element-major traces): p=4 0.848 vs 0.980 ms, p=5 1.387 vs 1.549, p=3
+// 0.657 vs 0.665 (row-major traces had been neutral at p=3: 0.670 vs 0.666)
+#define DGB_TRACE_P(P) ((P) >= 3)
 #endif
 #ifndef DGB_MMA_SPLIT_J
 #define DGB_MMA_SPLIT_J 1
@@ -119,7 +118,12 @@ struct MmaDim {
   static constexpr int kBufOff = (kSize + 15) / 16 * 16;
   // per-warp staging after the tables: own [4 KS][32] + neighbour [4 KS][32] (two
   // neighbour buffers when the surface is packed: a tile spans two sides)
-  static constexpr int kWarpBuf = (kPacked ? 3 : 2) * 4 * KS * 32;
+  // one fragment buffer: 4 KS k-steps of 32 lanes, at least a tile's staged trace blocks in the
+  // trace-buffer degrees (8 elements x (12K + 2) doubles, packed; a side is smaller), rounded to 16
+  static constexpr int kFR = (DGB_TRACE_P(P) && kPacked && 8 * (12 * K + 2) > 4 * KS * 32)
+                                 ? (8 * (12 * K + 2) + 15) / 16 * 16
+                                 : 4 * KS * 32;
+  static constexpr int kWarpBuf = (kPacked ? 3 : 2) * kFR;
 };
 
 // volatile: a non-volatile asm may be duplicated into both arms of a per-lane
@@ -241,7 +245,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
                                                  double* __restrict__ smem) {
   using D = MmaDim<P>;
   constexpr int NP = D::NP, NQ = D::NQ, K = D::K, KS = D::KS, NT = D::NT, JT = D::JT;
-  constexpr int FR = 4 * KS * 32;  // doubles of one fragment buffer
+  constexpr int FR = D::kFR;  // doubles of one fragment buffer (spacing of the per-warp buffers)
   const long long ld = geo.ld;
   const double gamma = geo.gamma, g1 = gamma - 1.0;
   Scalars* sc = a.sc;
@@ -293,6 +297,7 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
   constexpr int kTS = 4 * K3;
   constexpr int kTSP = kTS + 2;
   constexpr int kSSP = 8 * K + 2;
+  static_assert(!DGB_TRACE_P(P) || (kPk ? 8 * kTSP : 8 * kSSP) <= FR, "staged trace blocks exceed a fragment buffer");
   // the last output tile of the projections when it holds at most two live modes (p = 3: modes
   // 8, 9 in 8 columns): the volume and packed-surface projections accumulate those modes with
   // DFMAs into X (each lane its own points' share), reduced over the element's four lanes

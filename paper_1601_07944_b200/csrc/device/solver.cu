@@ -1007,7 +1007,7 @@ RunOut run_steps(dgb_ctx* c, const RunSpec& r) {
   // column (an interior element computed after the halo wait is harmless): the DMMA kernel's
   // TMA boxes start at e0 + 8 k and must be 16-byte aligned.
   const int n_int = X ? (c->n_int & ~1) : c->N;
-  // trace mode (p = 4, 5, no limiter): each stage writes the edge traces of its output, the
+  // trace mode (p >= 3, no limiter): each stage writes the edge traces of its output, the
   // next stage reads its own and its neighbours' traces instead of interpolating them (results
   // bit-identical).  A partition pushes the send elements' trace rows
   // with their coefficient rows, so the halo columns carry traces too.

@@ -649,8 +649,8 @@ def test_trace_buffers_bitwise_equal_to_interpolated_traces(p, scheme, flux, mes
     """Trace-buffer stages (each stage writes the edge traces of its output, the next reads its own
     and its neighbours' traces, dgb_set_trace_buffers) give the same bits as interpolating every
     trace from the coefficient columns: fixed steps over several device batches, run_to_time with
-    its stop rule, RK4 / SSP / midpoint, both fluxes, the boundary-code instance (p = 3 has no
-    trace instances: the setter must be harmless there)."""
+    its stop rule, RK4 / SSP / midpoint, both fluxes, the boundary-code instance; p = 3, 4 take the
+    packed surface, p = 5 the per-side one."""
     if mesh_kind == "vortex":
         mesh = dg2d.generate_mesh(L.MESH_VORTEX, 3, 0, 1.0, 1.384)
         bc, u0 = dg2d.vortex_boundary(), dg2d.vortex_exact
