@@ -878,7 +878,12 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
         const bool bnd = nb < 0;
         const int snb = bnd ? 0 : ((inf >> (2 * q)) & 3);
         const double nx = enx[q], ny = eny[q], h = eh[q];
-        if (q > 0) cp_async_wait<0>();  // this side's neighbour column / traces (prefetched during the previous side)
+        if (q > 0) {
+          cp_async_wait<0>();  // this side's neighbour column / traces (prefetched during the previous side)
+          // the trace blocks are copied by other lanes than the ones reading them (each lane's wait
+          // covers only its own copies); the coefficient fragments are read by their own copier
+          if constexpr (kTrInS) __syncwarp();
+        }
         if constexpr (MODE == kModeSurface) {
 #pragma unroll
           for (int m = 0; m < 4; ++m)
