@@ -114,7 +114,7 @@ int dgb_set_flux(dgb_ctx* ctx, int flux);
  * kernels above (measured).  All give bit-identical results. */
 int dgb_set_fused_limiter(dgb_ctx* ctx, int enable);
 /* Trace buffers (no reference counterpart: a data-layout choice of the device step loop).  With
- * enable = 1, the stages of a run at p >= 3 without limiting write the edge
+ * enable = 1, the stages of a run at p >= 2 without limiting write the edge
  * traces of their output and the next stage reads its own and its neighbours' traces instead of
  * interpolating them from the coefficient columns; 0 interpolates every stage.  Default from
  * env DGB_TRACE_BUF at creation.  Both give bit-identical results. */

@@ -467,6 +467,16 @@ __device__ __forceinline__ double ld_nc(const double* p) {
   asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(r) : "l"(p));
   return r;
 }
+#ifndef DGB_TRACE_P
+// degrees with trace-buffer stage instances (kVarTrace) and the epilogue's trace write; measured
+// per stage (interleaved, element-major traces): p=5 1.387 vs 1.549 ms, p=4 0.848 vs 0.980, p=3
+// 0.657 vs 0.665, p=2 (one-thread kernel, large meshes) 0.281 vs 0.286; p=1 0.170 vs 0.117 (the
+// trace bytes outweigh the three 12-row gathers they replace), so p=1 interpolates
+#define DGB_TRACE_P(P) ((P) >= 2)
+#endif
+#ifndef DGB_G1_OWN_TRACE_READ
+#define DGB_G1_OWN_TRACE_READ 1  // p=2: own traces read 0.281 ms, re-interpolated from the coefficients 0.304
+#endif
 #ifndef DGB_G1_HOIST_MAXP
 #define DGB_G1_HOIST_MAXP 2  // one-thread kernel: mode-0 products formed once per variable (not per point)
 #endif
@@ -824,6 +834,12 @@ __device__ __forceinline__ void g1_element(const Tab<P>& T, const Geo& geo, cons
   const int kmode = RK4 ? a.kmode : 0;
   const bool want_lambda = LAM && a.want_lambda;
   constexpr bool kHoist0 = P <= DGB_G1_HOIST_MAXP;
+  // trace-buffer instance: the own and neighbour traces of the stage
+  // input come from a.tr_in, element-major [e][side][var][point] (one contiguous 4K block per
+  // side), instead of being interpolated from the coefficient columns
+  constexpr bool kTrG = MODE == kModeStage && !PF && DGB_TRACE_P(P) && (VAR & kVarTrace) != 0;
+  constexpr bool kTrOwn = kTrG && DGB_G1_OWN_TRACE_READ;  // own traces read too (else interpolated)
+  constexpr int kTS = 12 * K;  // trace doubles per element
   {
     double c[4][NP];
     if constexpr (PF) {
@@ -913,7 +929,33 @@ __device__ __forceinline__ void g1_element(const Tab<P>& T, const Geo& geo, cons
         const double nx = __ldg(geo.enx + ed), ny = __ldg(geo.eny + ed), h = __ldg(geo.eh + ed);
         const bool bnd = nb < 0;
         double un[K][4];
-        if constexpr (PF) {
+        double ut[4 * K];  // kTrG: this side's own traces [m][ko]
+        if constexpr (kTrG) {
+          if constexpr (kTrOwn) {
+            const double2* ob = reinterpret_cast<const double2*>(a.tr_in + static_cast<long long>(e) * kTS + q * 4 * K);
+#pragma unroll
+            for (int i = 0; i < 2 * K; ++i) {
+              const double2 v = __ldg(ob + i);
+              ut[2 * i] = v.x;
+              ut[2 * i + 1] = v.y;
+            }
+          }
+          if (!bnd) {  // the neighbour's side block, its points reversed
+            const double2* nbk =
+                reinterpret_cast<const double2*>(a.tr_in + static_cast<long long>(nb) * kTS + (snb - 1) * 4 * K);
+            double v4[4 * K];
+#pragma unroll
+            for (int i = 0; i < 2 * K; ++i) {
+              const double2 v = __ldg(nbk + i);
+              v4[2 * i] = v.x;
+              v4[2 * i + 1] = v.y;
+            }
+#pragma unroll
+            for (int ko = 0; ko < K; ++ko)
+#pragma unroll
+              for (int m = 0; m < 4; ++m) un[ko][m] = v4[m * K + (K - 1 - ko)];
+          }
+        } else if constexpr (PF) {
           cp_async_wait<3>();  // side q's neighbour column
           const double* col = pipe->base + (q + 1) * 4 * NP * pipe->stride;
           if (!bnd) {
@@ -945,7 +987,7 @@ __device__ __forceinline__ void g1_element(const Tab<P>& T, const Geo& geo, cons
             for (int j = 0; j < NP; ++j) acc[m][j] = 0.0;
         }
         const double* __restrict__ phq = &T.phe[q][0][0];  // own side, uniform runtime offset
-        constexpr bool kReload = P >= DGB_G1_RELOAD_MINP;
+        constexpr bool kReload = P >= DGB_G1_RELOAD_MINP && !kTrOwn;
         // own trace of the side from a fresh (L1) read of the coefficients, so that they
         // need not stay in registers past the volume integral
         double uoa[K][4];
@@ -962,13 +1004,15 @@ __device__ __forceinline__ void g1_element(const Tab<P>& T, const Geo& geo, cons
         }
         double c0q[4];  // mode-0 products of the own trace, once per side (not kept across the loop)
 #pragma unroll
-        for (int m = 0; m < 4; ++m) c0q[m] = (kReload || !kHoist0) ? 0.0 : phq[0] * c[m][0];
+        for (int m = 0; m < 4; ++m) c0q[m] = (kReload || !kHoist0 || kTrOwn) ? 0.0 : phq[0] * c[m][0];
 #pragma unroll
         for (int ko = 0; ko < K; ++ko) {
           double uo[4];
 #pragma unroll
           for (int m = 0; m < 4; ++m) {
-            if constexpr (kReload) {
+            if constexpr (kTrOwn) {
+              uo[m] = ut[m * K + ko];
+            } else if constexpr (kReload) {
               uo[m] = uoa[ko][m];
             } else {
               double s = kHoist0 ? c0q[m] : phq[ko * NP] * c[m][0];
@@ -1045,6 +1089,32 @@ __device__ __forceinline__ void g1_element(const Tab<P>& T, const Geo& geo, cons
           a.out[idx] = o;
           if (a.want_resid) res_max = std_max(res_max, fabs(uu - o));
           acc[m][j] = o;
+        }
+      }
+      if constexpr (DGB_TRACE_P(P) && !PF) {
+        if (a.tr_out) {
+          // traces of the new stage for the next stage's kVarTrace instance: the own-trace chain of
+          // the surface (mode-0 product, then the modes in order), side by side, one contiguous
+          // 4K block per side
+          double2* tb = reinterpret_cast<double2*>(a.tr_out + static_cast<long long>(e) * kTS);
+#pragma unroll kG1SideUnroll
+          for (int q = 0; q < 3; ++q) {
+            const double* __restrict__ phq = &T.phe[q][0][0];
+            double v4[4 * K];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+              const double t0 = phq[0] * acc[m][0];
+#pragma unroll
+              for (int ko = 0; ko < K; ++ko) {
+                double s = t0;
+#pragma unroll
+                for (int j = 1; j < NP; ++j) s = fma(phq[ko * NP + j], acc[m][j], s);
+                v4[m * K + ko] = s;
+              }
+            }
+#pragma unroll
+            for (int i = 0; i < 2 * K; ++i) tb[q * 2 * K + i] = make_double2(v4[2 * i], v4[2 * i + 1]);
+          }
         }
       }
       if (a.means) {  // the limiter's neighbour means as one 32-byte sector per element

@@ -55,12 +55,6 @@ constexpr int kMmaPackUnroll = DGB_MMA_PACK_UNROLL;
 #ifndef DGB_MMA_TMA
 #define DGB_MMA_TMA(P) 1  // own coefficients of a tile by one TMA box (0: per-lane cp.async)
 #endif
-#ifndef DGB_TRACE_P
-// degrees with trace-buffer stage instances (kVarTrace) and the epilogue's trace write; measured
-// per stage (interleaved, element-major traces): p=4 0.848 vs 0.980 ms, p=5 1.387 vs 1.549, p=3
-// 0.657 vs 0.665 (row-major traces had been neutral at p=3: 0.670 vs 0.666)
-#define DGB_TRACE_P(P) ((P) >= 3)
-#endif
 #ifndef DGB_MMA_SPLIT_J
 #define DGB_MMA_SPLIT_J 1
 #endif

@@ -33,7 +33,7 @@ constexpr int kG4PerSm = DGB_G4_PER_SM;  // latency-form stage kernel up to this
 
 constexpr bool kMma = DGB_P >= DGB_MMA_MINP;
 // trace-buffer stage instances (kVarTrace) exist for the packed-surface DMMA degrees
-constexpr bool kTraceOK = kMma && DGB_TRACE_P(DGB_P);
+constexpr bool kTraceOK = (kMma || kG == 1) && DGB_TRACE_P(DGB_P);
 constexpr int kMinB = kMma ? DGB_MMA_MINB(DGB_P) : MinBlocks<DGB_P>::value;
 constexpr int kThreads = kMma ? DGB_MMA_THREADS(DGB_P) : kBlock;  // threads per block of k_element
 // dynamic shared memory (bytes): tables + per-warp staging buffers
@@ -235,6 +235,7 @@ int Launch<DGB_P>::trace_points() {
   return kTraceOK ? 3 * Dim<DGB_P>::K : 0;
 }
 
+
 template <>
 int Launch<DGB_P>::lanes() {
   return kMma ? 0 : kG;
@@ -269,7 +270,9 @@ template <>
 cudaError_t Launch<DGB_P>::element(int mode, int grid, const Geo& g, const StageArgs& a, cudaStream_t s) {
   if (a.e1 <= a.e0) return cudaSuccess;
   if constexpr (!kMma && kG == 1) {
-    if (mode == kModeStage && a.e1 - a.e0 <= (g.lat_stage_n >= 0 ? g.lat_stage_n : stage_latency_max_n())) {
+    // (trace mode always takes the one-thread form: the latency form has no trace path)
+    if (mode == kModeStage && !a.tr_in && !a.tr_out &&
+        a.e1 - a.e0 <= (g.lat_stage_n >= 0 ? g.lat_stage_n : stage_latency_max_n())) {
       if (grid <= 0) grid = grid_for(static_cast<long long>((a.e1 - a.e0 + 31) & ~31) * 4, 16);
       cudaError_t err = cudaSuccess;
       auto go = [&](auto k) {
@@ -304,6 +307,17 @@ cudaError_t Launch<DGB_P>::dt(int grid, const Geo& g, const double* c, Scalars* 
   if (grid <= 0) grid = grid_for(g.ld, o);
   k_dt<<<grid, kBlock, 0, s>>>(g, c, sc, slot, seq);
   return cudaGetLastError();
+}
+
+template <>
+bool Launch<DGB_P>::trace_wanted(int n, const Geo& g) {
+  if constexpr (!kTraceOK) {
+    return false;
+  } else if constexpr (kMma) {
+    return true;
+  } else {  // the one-thread kernel: not where the four-lane latency form serves the mesh
+    return n > (g.lat_stage_n >= 0 ? g.lat_stage_n : stage_latency_max_n());
+  }
 }
 
 }  // namespace dgbk

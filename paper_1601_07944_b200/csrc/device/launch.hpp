@@ -19,6 +19,7 @@ struct Launch {
   static int resident_blocks(int mode);  // blocks per SM for the element kernel
   static int lanes();                    // G (0 = DMMA tile kernel)
   static int trace_points();             // 3K when the stage kernel has trace-buffer instances, else 0
+  static bool trace_wanted(int n, const Geo& g);  // trace mode pays for whole-mesh runs of n elements
   // DMMA fragment-ordered tables: size in doubles (0 when the degree does not use
   // the DMMA kernel); fills `out` when non-null
   static int mma_table(const Tab<P>& t, double* out);

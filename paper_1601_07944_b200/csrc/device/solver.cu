@@ -898,10 +898,22 @@ struct RunOut {
 
 int trace_points(int p) {
   switch (p) {
+    case 1: return dgbk::Launch<1>::trace_points();
+    case 2: return dgbk::Launch<2>::trace_points();
     case 3: return dgbk::Launch<3>::trace_points();
     case 4: return dgbk::Launch<4>::trace_points();
     case 5: return dgbk::Launch<5>::trace_points();
     default: return 0;
+  }
+}
+
+bool trace_wanted(const dgb_ctx* c) {
+  switch (c->p) {
+    case 1: return dgbk::Launch<1>::trace_wanted(c->N, c->geo);
+    case 2: return dgbk::Launch<2>::trace_wanted(c->N, c->geo);
+    case 3: return dgbk::Launch<3>::trace_wanted(c->N, c->geo);
+    case 4: return dgbk::Launch<4>::trace_wanted(c->N, c->geo);
+    default: return dgbk::Launch<5>::trace_wanted(c->N, c->geo);
   }
 }
 
@@ -1007,11 +1019,11 @@ RunOut run_steps(dgb_ctx* c, const RunSpec& r) {
   // column (an interior element computed after the halo wait is harmless): the DMMA kernel's
   // TMA boxes start at e0 + 8 k and must be 16-byte aligned.
   const int n_int = X ? (c->n_int & ~1) : c->N;
-  // trace mode (p >= 3, no limiter): each stage writes the edge traces of its output, the
+  // trace mode (p >= 2, no limiter, p = 2 above the latency-form size): each stage writes the edge traces of its output, the
   // next stage reads its own and its neighbours' traces instead of interpolating them (results
   // bit-identical).  A partition pushes the send elements' trace rows
   // with their coefficient rows, so the halo columns carry traces too.
-  const bool use_tr = c->trace_mode != 0 && c->k3 > 0 && !r.limiting && !fused;
+  const bool use_tr = c->trace_mode != 0 && c->k3 > 0 && !r.limiting && !fused && trace_wanted(c);
   auto trace_of = [&](const double* p) -> double* {
     if (buf_id(c, p) < 0) throw Fail{DGB_ERR_ARG, "trace of a buffer outside the rotation"};
     return const_cast<double*>(p) + c->coeff_count();

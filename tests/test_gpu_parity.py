@@ -642,7 +642,7 @@ def test_time_dependent_dirichlet_at_every_stage_time(scheme):
         c_.close()
 
 
-@pytest.mark.parametrize("p", [3, 4, 5])
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5])
 @pytest.mark.parametrize("scheme,flux", [(103, "llf"), (4, "llf"), (2, "roe"), (102, "llf")])
 @pytest.mark.parametrize("mesh_kind", ["box", "vortex"])
 def test_trace_buffers_bitwise_equal_to_interpolated_traces(p, scheme, flux, mesh_kind):
@@ -650,7 +650,8 @@ def test_trace_buffers_bitwise_equal_to_interpolated_traces(p, scheme, flux, mes
     and its neighbours' traces, dgb_set_trace_buffers) give the same bits as interpolating every
     trace from the coefficient columns: fixed steps over several device batches, run_to_time with
     its stop rule, RK4 / SSP / midpoint, both fluxes, the boundary-code instance; p = 3, 4 take the
-    packed surface, p = 5 the per-side one."""
+    packed surface, p = 5 the per-side one, p = 1, 2 the one-thread kernel (when it has trace
+    instances, DGB_TRACE_P)."""
     if mesh_kind == "vortex":
         mesh = dg2d.generate_mesh(L.MESH_VORTEX, 3, 0, 1.0, 1.384)
         bc, u0 = dg2d.vortex_boundary(), dg2d.vortex_exact
@@ -664,6 +665,7 @@ def test_trace_buffers_bitwise_equal_to_interpolated_traces(p, scheme, flux, mes
     for tr in (0, 1):
         ctx = dg2d.SolverContext(mesh, tb, bc=bc, options=opts)
         assert L.lib.dgb_set_trace_buffers(ctx.handle, tr) == 0
+        assert L.lib.dgb_set_latency_forms(ctx.handle, 0, 0) == 0  # p <= 2: the one-thread form (trace mode)
         st = dg2d.SolverState(c0.copy())
         r1 = dg2d.run_fixed_steps(ctx, st, 9)
         r2 = dg2d.run_fixed_steps(ctx, st, 4)  # a second call: its first stage interpolates again
