@@ -18,6 +18,11 @@ for p in (1, 2, 3, 4, 5):
         dg2d.run_fixed_steps(ctx, st, 2)
         dg2d.compute_rhs(ctx, c0, 0.0); dg2d.eval_volume_pass(ctx, c0); dg2d.eval_surface_pass(ctx, c0, 0.0)
         ctx.close()
+    if p <= 2:  # the one-thread kernel and its trace-buffer instances (latency forms off)
+        ctx = dg2d.SolverContext(mesh, tb, options=dg2d.SolverOptions(scheme=103))
+        L.lib.dgb_set_latency_forms(ctx.handle, 0, 0)
+        dg2d.run_fixed_steps(ctx, dg2d.SolverState(c0.copy()), 3)
+        ctx.close()
     # RK4 accumulator instances and the asynchronous copy path
     ctx = dg2d.SolverContext(mesh, tb, options=dg2d.SolverOptions(rk_order=4))
     dg2d.run_fixed_steps(ctx, dg2d.SolverState(c0.copy()), 2)
