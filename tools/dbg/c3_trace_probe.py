@@ -1,10 +1,13 @@
+"""Stage-kernel median on the C3 vortex mesh (level 6, walls) with trace buffers off / on:
+  P=3 python tools/dbg/c3_trace_probe.py"""
 import ctypes as C, json, os, sys
 sys.path.insert(0, os.getcwd())
 from paper_1601_07944_b200 import _lib as L, dg2d
 mesh = dg2d.generate_mesh(L.MESH_VORTEX, 6, 0, 1.0, 1.384)
-tb = dg2d.build_tables(3)
+P = int(os.environ.get("P", "3"))
+tb = dg2d.build_tables(P)
 c0 = dg2d.project_initial(lambda xy: dg2d.vortex_exact(xy), mesh, tb)
-out = {}
+out = {"p": P}
 for tr in (0, 1, 0, 1):
     ctx = dg2d.SolverContext(mesh, tb, bc=dg2d.vortex_boundary(), options=dg2d.SolverOptions(scheme=103, cfl=0.3))
     L.lib.dgb_set_trace_buffers(ctx.handle, tr)
