@@ -1160,13 +1160,23 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
           if constexpr (kSplitK)
             ktail(Tw, smem + D::kPkOwn + (sp * KS + KS - 1) * 32, [&](int m, int jj) { return own_c(m, 4 * (KS - 1) + jj); });
           if (valid) {
+            if constexpr (K % 2 == 0) {  // the lane's two points are adjacent in one side: one 16-byte store
+              const int pt = 8 * sp + 2 * t;
+              if (pt < K3) {
 #pragma unroll
-            for (int m = 0; m < 4; ++m)
-#pragma unroll
-              for (int ii = 0; ii < 2; ++ii) {
-                const int pt = 8 * sp + 2 * t + ii;
-                if (pt < K3) a.tr_out[static_cast<long long>(e) * kTS + ((pt / K) * 4 + m) * K + pt % K] = Tw[m][ii];
+                for (int m = 0; m < 4; ++m)
+                  *reinterpret_cast<double2*>(a.tr_out + static_cast<long long>(e) * kTS + ((pt / K) * 4 + m) * K + pt % K) =
+                      make_double2(Tw[m][0], Tw[m][1]);
               }
+            } else {
+#pragma unroll
+              for (int m = 0; m < 4; ++m)
+#pragma unroll
+                for (int ii = 0; ii < 2; ++ii) {
+                  const int pt = 8 * sp + 2 * t + ii;
+                  if (pt < K3) a.tr_out[static_cast<long long>(e) * kTS + ((pt / K) * 4 + m) * K + pt % K] = Tw[m][ii];
+                }
+            }
           }
         }
         } else {  // per-side surface: side q's own-trace contraction (kPhe)
@@ -1184,13 +1194,22 @@ __device__ __forceinline__ void element_body_mma(const Tab<P>& T, const Geo& geo
           if constexpr (kSplitK)
             ktail(Tw, smem + D::kPhe + (q * KS + KS - 1) * 32, [&](int m, int jj) { return own_c(m, 4 * (KS - 1) + jj); });
           if (valid) {
+            if constexpr (K % 2 == 0) {
+              if (2 * t < K) {
 #pragma unroll
-            for (int m = 0; m < 4; ++m)
-#pragma unroll
-              for (int ii = 0; ii < 2; ++ii) {
-                const int ko = 2 * t + ii;
-                if (ko < K) a.tr_out[static_cast<long long>(e) * kTS + (q * 4 + m) * K + ko] = Tw[m][ii];
+                for (int m = 0; m < 4; ++m)
+                  *reinterpret_cast<double2*>(a.tr_out + static_cast<long long>(e) * kTS + (q * 4 + m) * K + 2 * t) =
+                      make_double2(Tw[m][0], Tw[m][1]);
               }
+            } else {
+#pragma unroll
+              for (int m = 0; m < 4; ++m)
+#pragma unroll
+                for (int ii = 0; ii < 2; ++ii) {
+                  const int ko = 2 * t + ii;
+                  if (ko < K) a.tr_out[static_cast<long long>(e) * kTS + (q * 4 + m) * K + ko] = Tw[m][ii];
+                }
+            }
           }
         }
         }
