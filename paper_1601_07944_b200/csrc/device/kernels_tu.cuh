@@ -314,9 +314,9 @@ bool Launch<DGB_P>::trace_wanted(int n, const Geo& g) {
   if constexpr (!kTraceOK) {
     return false;
   } else if constexpr (kMma) {
-    // p=3 with physical-boundary sides (the boundary-code instance): 0.513 vs 0.505 ms per stage on
-    // the C3 vortex mesh, where the periodic box gains (0.657 vs 0.665): interpolate there
-    return DGB_P != 3 || !g.has_bnd;
+    // (p=3 on the C3 vortex mesh, the boundary-code instance: 0.478 vs 0.509 ms per stage with the
+    // 16-byte trace stores; 0.513 vs 0.505 before them)
+    return true;
   } else {  // the one-thread kernel: not where the four-lane latency form serves the mesh
     return n > (g.lat_stage_n >= 0 ? g.lat_stage_n : stage_latency_max_n());
   }
